@@ -1,0 +1,158 @@
+"""Pins of the oracle's iteration space and schedule (o1, o2, o3).
+
+Each pin is something other than the oracle itself: SPEC.md's worked
+examples (tests/golden/spec_examples.json), GCC libgomp's static schedules
+(tests/golden/libgomp_static.json, an independent OpenMP runtime), closed
+forms, brute-force enumeration and partition invariants.
+"""
+import itertools
+import json
+import math
+import os
+import random
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import GOLDEN
+
+SPEC = json.load(open(os.path.join(GOLDEN, "spec_examples.json")))
+
+
+# ---- o1 trip count ------------------------------------------------------------
+@pytest.mark.parametrize("lb,ub,step", [(0, 10, 1), (0, 10, 3), (5, 5, 1), (7, 3, 1),
+                                        (10, 0, -1), (10, 0, -3), (-4, 9, 2), (3, 7, -1),
+                                        (0, 1, 100), (-10, -20, -4)])
+def test_trip_count_bruteforce(lb, ub, step):
+    # brute force: count the induction values a C for-loop would visit
+    cnt, i = 0, lb
+    while (i < ub) if step > 0 else (i > ub):
+        cnt += 1
+        i += step
+    assert oracle.trip_count(lb, ub, step) == cnt
+
+
+def test_trip_count_zero_step_invalid():
+    assert oracle.trip_count(0, 10, 0) == -1
+
+
+def test_trip_count_large_int64():
+    # reading c2: int64 everywhere; T = 2^34 (C5) must not overflow
+    assert oracle.trip_count(0, 1 << 34, 1) == 1 << 34
+    assert oracle.trip_count(0, (1 << 34) + 1, 2) == (1 << 33) + 1
+
+
+# ---- o1 collapse --------------------------------------------------------------
+def test_collapse_spec_example():
+    T = SPEC["collapse_4x3"]["T"]
+    seq = [oracle.delinearize(T, t) for t in range(12)]
+    assert seq == list(itertools.product(range(4), range(3)))
+
+
+@pytest.mark.parametrize("T", [(3, 5), (1, 7), (2, 3, 4), (5, 1, 2), (6,)])
+def test_collapse_lexicographic_bruteforce(T):
+    n = math.prod(T)
+    seq = [oracle.delinearize(list(T), t) for t in range(n)]
+    assert seq == list(itertools.product(*[range(d) for d in T]))
+
+
+# ---- o2 static: SPEC worked examples -----------------------------------------
+@pytest.mark.parametrize("key", ["static_T10_p3", "static_chunk2_T8_p2", "static_p1"])
+def test_static_spec_examples(key):
+    ex = SPEC[key]
+    for u, exp in enumerate(ex["expect"]):
+        got = oracle.schedule_chunks(oracle.STATIC, ex["chunk"], ex["T"], ex["p"], u)
+        assert [list(c) for c in got] == exp, ex["cite"]
+
+
+def test_empty_T0():
+    ex = SPEC["empty_T0"]
+    for policy, c in ((oracle.STATIC, 0), (oracle.STATIC, 2), (oracle.DYNAMIC, 1)):
+        for u in range(ex["p"]):
+            assert oracle.schedule_chunks(policy, c, 0, ex["p"], u) == []
+
+
+# ---- o2 static vs GCC libgomp (independent library) --------------------------
+def test_static_matches_libgomp():
+    data = json.load(open(os.path.join(GOLDEN, "libgomp_static.json")))
+    assert len(data["cases"]) > 1000
+    for T, p, c, own in data["cases"]:
+        got = oracle.owner_map(oracle.STATIC, c, T, p)
+        assert got.tolist() == own, (T, p, c)
+
+
+def test_runtime_auto_resolve_to_static():
+    for pol in (oracle.RUNTIME, oracle.AUTO):
+        assert (oracle.owner_map(pol, 0, 37, 5) == oracle.owner_map(oracle.STATIC, 0, 37, 5)).all()
+
+
+# ---- o2/o3 partition invariants (SPEC.md:363 property) -----------------------
+def _check_partition(policy, c, T, p):
+    seen = np.zeros(T, dtype=np.int64)
+    for u in range(p):
+        chunks = oracle.schedule_chunks(policy, c, T, p, u)
+        prev = -1
+        for lo, hi in chunks:
+            assert 0 <= lo < hi <= T
+            assert lo > prev            # each unit's chunks strictly increasing
+            prev = lo
+            seen[lo:hi] += 1
+    assert (seen == 1).all()           # disjoint, union = [0, T)
+
+
+def test_partition_exhaustive_small():
+    for T in range(0, 65):
+        for p in range(1, 10):
+            for c in (0, 1, 2, 3, 7, 17):
+                _check_partition(oracle.STATIC, c, T, p)
+                if c:
+                    _check_partition(oracle.DYNAMIC, c, T, p)
+
+
+def test_partition_sampled_large():
+    rng = random.Random(2209)
+    for _ in range(60):
+        T = rng.randrange(0, 10_001)
+        p = rng.randrange(1, 65)
+        c = rng.randrange(0, 18)
+        _check_partition(oracle.STATIC, c, T, p)
+
+
+def test_static_block_sizes_closed_form():
+    # static without chunk: first T mod p units get ceil(T/p), rest floor(T/p)
+    for T, p in ((10, 3), (1000, 7), (5, 8), (2 ** 20 + 3, 148 * 256)):
+        for u in (0, p // 2, p - 1):
+            ch = oracle.schedule_chunks(oracle.STATIC, 0, T, p, u)
+            length = sum(h - l for l, h in ch)
+            assert length == (T // p + (1 if u < T % p else 0))
+
+
+# ---- o3 dynamic ---------------------------------------------------------------
+def test_dynamic_spec_example():
+    ex = SPEC["dynamic_c1_T4_p2"]
+    got = oracle.owner_map(oracle.DYNAMIC, ex["chunk"], ex["T"], ex["p"])
+    assert got.tolist() == ex["expect_owner"], ex["cite"]
+
+
+def test_dynamic_default_chunk_is_one():
+    assert (oracle.owner_map(oracle.DYNAMIC, 0, 9, 4) == oracle.owner_map(oracle.DYNAMIC, 1, 9, 4)).all()
+
+
+def test_dynamic_chunk_boundaries():
+    # the chunk partition of dynamic,c is {[kc, min((k+1)c, T))}
+    T, p, c = 103, 5, 8
+    allchunks = sorted(ch for u in range(p) for ch in oracle.schedule_chunks(oracle.DYNAMIC, c, T, p, u))
+    assert allchunks == [(k * c, min((k + 1) * c, T)) for k in range((T + c - 1) // c)]
+
+
+def test_guided_is_rejected():
+    with pytest.raises(ValueError):
+        oracle.schedule_chunks(oracle.GUIDED, 1, 10, 2, 0)
+
+
+def test_tile_owner_static1_round_robin():
+    # tile loop static,1 over p teams: tile tau -> team tau mod p (chunk rule)
+    own = oracle.tile_owner(10, 20, 3, 7, oracle.STATIC, 1, 4)
+    ntiles = 4 * 3
+    assert own.tolist() == [t % 4 for t in range(ntiles)]
