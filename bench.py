@@ -1,0 +1,387 @@
+"""Benchmark of the UPIR data-parallel loop path on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl upir|reference]
+                    [--workload reduce|axpy|jacobi|matmul] [--sched static|static1|dynamic]
+
+For N > 1 launch under torchrun (one rank per GPU, NCCL).  Rank 0 prints ONE
+JSON line.  Default workload = BASELINE.json configs[1]: int64 and fp32
+sum/max reduction over n = 2^30 elements per GPU, teams x units = 148*4 x 256
+SPMD region, worksharing loop under schedule(static) with the two reductions
+fused into the loop (one pass per array), map to/from; at N > 1 each rank
+reduces its own 2^30-element arrays and the four results are combined over
+ranks with upir_reduce(WORLD) (weak scaling).
+
+A step = one pass of the whole path over the step's input:
+  value : the loop kernels + world combine with inputs resident in HBM
+  e2e   : through the C-ABI with HOST buffers -- upir_data_map(TO) of the
+          pinned host arrays (H2D), the loops, the world combine, the result
+          scalars mapped FROM (D2H) and unmap, every step.
+Inputs (12 GiB per GPU) are far larger than L2 (126 MB): no flush needed.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GIB = 1 << 30
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="upir", choices=["upir", "reference"])
+    ap.add_argument("--workload", default="reduce", choices=["reduce", "axpy", "jacobi", "matmul"])
+    ap.add_argument("--sched", default="static", choices=["static", "static1", "dynamic"])
+    ap.add_argument("--n-log2", type=int, default=30)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+# --------------------------------------------------------------------------- clocks
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [v.strip() for v in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d, "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+def ncu_traffic(kernel_key):
+    p = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(p):
+        d = json.load(open(p))
+        return d.get(kernel_key)
+    return None
+
+
+# --------------------------------------------------------------------------- dist
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# --------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    """The oracle (plain sequential CPU interpreter) as the reference arm, on a
+    bounded sample of the same workload, timed on this host's cores."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    import synth
+    n = 1 << 24
+    xi = synth.c_i64_sym(6, 0, n)
+    xf = synth.c_f32_unit(7, 0, n)
+    p = 148 * 4 * 256
+
+    def step():
+        oracle.reduce_i64(oracle.SUM, xi, p=p)
+        oracle.reduce_i64(oracle.MAX, xi, p=p)
+        oracle.reduce_f32(oracle.SUM, xf, p=p)
+        oracle.reduce_f32(oracle.MAX, xf, p=p)
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        step()
+    dt = (time.perf_counter() - t0) / args.steps
+    gbs = n * 12 / dt / 1e9
+    print(json.dumps({
+        "impl": "reference", "metric": "reduction GB/s (int64+fp32 sum/max, n=2^30 per GPU)",
+        "value": gbs, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": dt * 1e3 * (1 << 30) / n, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "i64+f32", "data": "synthetic",
+        "config": {"workload": "C2: int64 and fp32 sum/max reduction, n=2^30, teams x units SPMD, map to/from",
+                   "sample": "n=2^24 of the same stream"},
+        "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle",
+                         "sample": "2^24 int64 + 2^24 fp32 elements (sum and max each), scaled by bytes"},
+        "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }), flush=True)
+
+
+def cpu_baseline_reduce():
+    import oracle
+    import synth
+    n = 1 << 26
+    xi = synth.c_i64_sym(6, 0, n)
+    xf = synth.c_f32_unit(7, 0, n)
+    p = 148 * 4 * 256
+    t0 = time.perf_counter()
+    oracle.reduce_i64(oracle.SUM, xi, p=p)
+    oracle.reduce_i64(oracle.MAX, xi, p=p)
+    oracle.reduce_f32(oracle.SUM, xf, p=p)
+    oracle.reduce_f32(oracle.MAX, xf, p=p)
+    dt = time.perf_counter() - t0
+    return {"value": n * 12 / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
+            "sample": "2^26 int64 + 2^26 fp32 elements, sum and max each (one pass per op), "
+                      "GB/s counted as 12 B per element pair like the GPU metric"}
+
+
+# --------------------------------------------------------------------------- UPIR arm
+def run_upir(args):
+    import torch
+    import paper_2209_10643_b200 as U
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        pg = dist
+        idb = [U.upir_comm_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(idb, src=0)
+        ctx = U.upir_init(local, rank=rank, nranks=world, nccl_id=idb[0])
+    else:
+        ctx = U.upir_init(local)
+    stream = torch.cuda.ExternalStream(U.upir_ctx_stream(ctx, 0))
+    peaks, peak_src = measured_peaks()
+
+    def barrier():
+        U.upir_sync(ctx)
+        if pg:
+            pg.barrier()
+        torch.cuda.synchronize()
+
+    if args.workload == "reduce":
+        res = bench_reduce(args, U, ctx, stream, barrier, rank, world, peaks, peak_src)
+    else:
+        raise SystemExit(f"workload {args.workload} not built yet")
+    # max over ranks of the timed values
+    if pg:
+        t = torch.tensor([res["ms_per_step"], res["e2e_ms"]], device="cuda")
+        pg.all_reduce(t, op=pg.ReduceOp.MAX)
+        res["ms_per_step"], res["e2e_ms"] = t.tolist()
+    res["value"] = res["bytes_all_ranks"] / (res["ms_per_step"] / 1e3) / 1e9
+    res["e2e"]["value"] = res["bytes_all_ranks"] / (res["e2e_ms"] / 1e3) / 1e9
+    if rank == 0:
+        out = {k: v for k, v in res.items() if k not in ("bytes_all_ranks", "e2e_ms")}
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline_reduce()
+        print(json.dumps(out), flush=True)
+    U.upir_finalize(ctx)
+    if pg:
+        pg.destroy_process_group()
+
+
+def bench_reduce(args, U, ctx, stream, barrier, rank, world, peaks, peak_src):
+    import torch
+    n = 1 << args.n_log2
+    teams, units = 148 * 4, 256
+    pol, chunk = {"static": (U.SCHED_STATIC, 0), "static1": (U.SCHED_STATIC, 2),
+                  "dynamic": (U.SCHED_DYNAMIC, 2)}[args.sched]
+    # device-resident inputs: map(alloc) + on-device synthetic fill (rank r
+    # holds global elements [r*n, (r+1)*n) of each stream)
+    hi = np.empty(1, np.int64)          # host key objects for the alloc maps
+    hf = np.empty(1, np.float32)
+    xi_t = torch.empty(n, dtype=torch.int64, device="cuda")
+    xf_t = torch.empty(n, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    mi = U.upir_data_adopt(ctx, xi_t)
+    mf = U.upir_data_adopt(ctx, xf_t)
+    U.upir_synth_fill(ctx, mi, 2, 6, rank * n)
+    U.upir_synth_fill(ctx, mf, 0, 7, rank * n)
+    res_t = torch.zeros(8, dtype=torch.float64, device="cuda")   # 4 local + 4 world results (8 B each)
+    torch.cuda.synchronize()
+    base = res_t.data_ptr()
+    reds_i = [U.reduction(U.OP_SUM, U.I64, base + 0), U.reduction(U.OP_MAX, U.I64, base + 8)]
+    reds_f = [U.reduction(U.OP_SUM, U.F32, base + 16), U.reduction(U.OP_MAX, U.F32, base + 24)]
+    loop = U.loop_desc(0, n, policy=pol, chunk=chunk)
+    spmd = U.upir_spmd_launch(ctx, U.spmd_desc(teams, units))
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+
+    def step(timed_events=None):
+        e = timed_events
+        if e:
+            e[0].record(stream)
+        U.upir_loop_exec(spmd, loop, U.body(U.BODY_REDUCE, U.I64, in0=mi), reds_i)
+        if e:
+            e[1].record(stream)
+        U.upir_loop_exec(spmd, loop, U.body(U.BODY_REDUCE, U.F32, in0=mf), reds_f)
+        if e:
+            e[2].record(stream)
+        if world > 1:
+            U.upir_reduce(ctx, U.OP_SUM, U.I64, base + 0, 1, base + 32, U.SCOPE_WORLD)
+            U.upir_reduce(ctx, U.OP_MAX, U.I64, base + 8, 1, base + 40, U.SCOPE_WORLD)
+            U.upir_reduce(ctx, U.OP_SUM, U.F32, base + 16, 1, base + 48, U.SCOPE_WORLD)
+            U.upir_reduce(ctx, U.OP_MAX, U.F32, base + 24, 1, base + 56, U.SCOPE_WORLD)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    st0 = U.upir_ctx_stats(ctx)["launches"]
+    clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    clk.start()
+    t0 = torch.cuda.Event(enable_timing=True)
+    t1 = torch.cuda.Event(enable_timing=True)
+    t0.record(stream)
+    for k in range(args.steps):
+        step(evs[k])
+    t1.record(stream)
+    barrier()
+    k_i = [e[0].elapsed_time(e[1]) for e in evs]
+    k_f = [e[1].elapsed_time(e[2]) for e in evs]
+    clocks = clk.stop()
+    launches = U.upir_ctx_stats(ctx)["launches"] - st0
+    ms = t0.elapsed_time(t1) / args.steps
+    # correctness guard on the last step (cheap properties)
+    r = res_t.cpu()
+    assert -(1 << 28) <= r[1:2].view(torch.int64).item() < (1 << 28)
+    U.upir_spmd_end(spmd)
+
+    # ---- e2e: host buffers through the C-ABI ------------------------------------
+    import ctypes
+    e2e_n = n
+    hx_i = torch.empty(e2e_n, dtype=torch.int64, pin_memory=True)
+    hx_f = torch.empty(e2e_n, dtype=torch.float32, pin_memory=True)
+    hx_i.copy_(xi_t[:e2e_n])
+    hx_f.copy_(xf_t[:e2e_n])
+    hres = np.zeros(8, np.float64)
+    U.upir_data_unmap(ctx, mi)
+    U.upir_data_unmap(ctx, mf)
+    del xi_t, xf_t
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+
+    def host_arr(t):
+        return np.ctypeslib.as_array(ctypes.cast(t.data_ptr(), ctypes.POINTER(
+            ctypes.c_int64 if t.dtype == torch.int64 else ctypes.c_float)), shape=(t.numel(),))
+
+    ai, af = host_arr(hx_i), host_arr(hx_f)
+
+    def e2e_step():
+        m1 = U.upir_data_map(ctx, ai, U.MAP_TO)
+        m2 = U.upir_data_map(ctx, af, U.MAP_TO)
+        mr = U.upir_data_map(ctx, hres, U.MAP_FROM)
+        rp, _, _ = U.upir_data_device_ptr(mr)
+        s = U.upir_spmd_launch(ctx, U.spmd_desc(teams, units))
+        loop_e = U.loop_desc(0, e2e_n, policy=pol, chunk=chunk)
+        U.upir_loop_exec(s, loop_e, U.body(U.BODY_REDUCE, U.I64, in0=m1),
+                         [U.reduction(U.OP_SUM, U.I64, rp + 0), U.reduction(U.OP_MAX, U.I64, rp + 8)])
+        U.upir_loop_exec(s, loop_e, U.body(U.BODY_REDUCE, U.F32, in0=m2),
+                         [U.reduction(U.OP_SUM, U.F32, rp + 16), U.reduction(U.OP_MAX, U.F32, rp + 24)])
+        if world > 1:
+            for k, (op, dt) in enumerate(((U.OP_SUM, U.I64), (U.OP_MAX, U.I64), (U.OP_SUM, U.F32),
+                                          (U.OP_MAX, U.F32))):
+                U.upir_reduce(ctx, op, dt, rp + 8 * k, 1, rp + 32 + 8 * k, U.SCOPE_WORLD)
+        U.upir_spmd_end(s)
+        U.upir_data_unmap(ctx, mr)
+        U.upir_data_unmap(ctx, m2)
+        U.upir_data_unmap(ctx, m1)
+        U.upir_sync(ctx)
+
+    e2e_step()   # warm-up (pins the host ranges once)
+    barrier()
+    te0 = time.perf_counter()
+    for _ in range(args.e2e_steps):
+        e2e_step()
+    barrier()
+    e2e_ms = (time.perf_counter() - te0) * 1e3 / args.e2e_steps
+    # the e2e path is timed by the host clock around synchronous steps (each
+    # step ends in upir_sync), max over ranks below
+
+    bytes_rank = n * 8 + n * 4
+    ki, kf = statistics.mean(k_i), statistics.mean(k_f)
+    ach_i = n * 8 / (ki / 1e3) / 1e9
+    ach_f = n * 4 / (kf / 1e3) / 1e9
+    peak = float(peaks["hbm_gbs"])
+    return {
+        "metric": "GB/s per upir.loop reduction (int64+fp32 sum/max, n=2^30 per GPU)",
+        "value": None, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "i64+f32", "data": "synthetic",
+        "config": {"workload": "C2: int64 and fp32 sum/max reduction, n=2^30 per GPU, teams x units "
+                               f"{teams}x{units}, schedule {args.sched}, map to/from",
+                   "n_per_gpu": n, "teams": teams, "units": units, "schedule": args.sched,
+                   "l2": "inputs 12 GiB per GPU >> 126 MB L2 (no flush needed)",
+                   "parallelism": f"dp{world}"},
+        "roofline": {"bound": "hbm", "achieved": ach_i, "peak": peak, "unit": "GB/s",
+                     "frac": ach_i / peak, "traffic": ncu_traffic("reduce_i64"),
+                     "kernel": "stream_loop_kernel<RED_I64,2>", "peak_source": peak_src,
+                     "other_kernels": {"reduce_f32": {"achieved": ach_f, "frac": ach_f / peak,
+                                                      "traffic": ncu_traffic("reduce_f32")}}},
+        "kernel_ms": {"reduce_i64": ki, "reduce_f32": kf},
+        "clocks": clocks,
+        "gpu_launches": launches,
+        "e2e": {"value": None, "unit": "GB/s", "h2d_bytes_per_step": bytes_rank, "d2h_bytes_per_step": 32},
+        "bytes_all_ranks": bytes_rank * world, "e2e_ms": e2e_ms,
+    }
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+        return
+    run_upir(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,130 @@
+// k_misc.cu -- dispatch of the streaming bodies, the ordered rank combine of
+// upir_reduce(WORLD), and the device-side synthetic input generator.
+#include <math_constants.h>
+
+#include "upir_internal.h"
+
+namespace upir {
+
+cudaError_t launch_stream_i64(int, int, int, int, bool, int, int, size_t, const StreamArgs &, cudaStream_t);
+cudaError_t launch_stream_f32(int, int, int, int, bool, int, int, size_t, const StreamArgs &, cudaStream_t);
+cudaError_t launch_stream_axpy(int, int, int, int, bool, int, int, size_t, const StreamArgs &, cudaStream_t);
+size_t staged_bytes_i64(int, int, int);
+size_t staged_bytes_f32(int, int, int);
+size_t staged_bytes_axpy(int, int, int);
+
+cudaError_t launch_stream_loop(int body, int path, int segv, int nst, bool trace, int teams, int units,
+                               size_t smem, const StreamArgs &a, cudaStream_t s) {
+  switch (body) {
+    case SB_RED_I64: return launch_stream_i64(a.nred, path, segv, nst, trace, teams, units, smem, a, s);
+    case SB_RED_F32: return launch_stream_f32(a.nred, path, segv, nst, trace, teams, units, smem, a, s);
+    case SB_AXPY: return launch_stream_axpy(a.nred, path, segv, nst, trace, teams, units, smem, a, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+size_t staged_smem_bytes(int body, int units, int segv, int nst) {
+  switch (body) {
+    case SB_RED_I64: return staged_bytes_i64(units, segv, nst);
+    case SB_RED_F32: return staged_bytes_f32(units, segv, nst);
+    case SB_AXPY: return staged_bytes_axpy(units, segv, nst);
+  }
+  return 0;
+}
+
+// ---- upir_reduce(WORLD): ordered combine of gathered per-rank values --------
+// gathered: [nranks][count]; out[e] = g[0][e] (+) g[1][e] (+) ... in ascending
+// rank order (reading c10; oracle o8).  fp32 values are combined in fp64 and
+// rounded once.
+__global__ void rank_combine_kernel(int op, int dtype, const void *gathered, int64_t count, int nranks,
+                                    void *out) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    if (dtype == UPIR_I64) {
+      const long long *g = reinterpret_cast<const long long *>(gathered);
+      unsigned long long acc = (unsigned long long)g[e];
+      for (int r = 1; r < nranks; ++r) {
+        const long long v = g[(int64_t)r * count + e];
+        if (op == UPIR_OP_SUM) acc += (unsigned long long)v;
+        else if (op == UPIR_OP_MAX) acc = ((long long)acc > v) ? acc : (unsigned long long)v;
+        else acc = ((long long)acc < v) ? acc : (unsigned long long)v;
+      }
+      reinterpret_cast<long long *>(out)[e] = (long long)acc;
+    } else {
+      const float *g = reinterpret_cast<const float *>(gathered);
+      double acc = g[e];
+      for (int r = 1; r < nranks; ++r) {
+        const double v = g[(int64_t)r * count + e];
+        if (op == UPIR_OP_SUM) acc += v;
+        else if (op == UPIR_OP_MAX) acc = fmax(acc, v);
+        else acc = fmin(acc, v);
+      }
+      reinterpret_cast<float *>(out)[e] = (float)acc;
+    }
+  }
+}
+
+cudaError_t launch_rank_combine(int op, int dtype, const void *gathered, int64_t count, int nranks,
+                                void *out, cudaStream_t s) {
+  const int threads = 256;
+  int64_t blocks = (count + threads - 1) / threads;
+  if (blocks > 1184) blocks = 1184;
+  if (blocks < 1) blocks = 1;
+  rank_combine_kernel<<<(int)blocks, threads, 0, s>>>(op, dtype, gathered, count, nranks, out);
+  return cudaGetLastError();
+}
+
+// ---- synthetic inputs: counter-based splitmix64 -
+// An implementation of the recipe independent of synth/ (host numpy).
+__device__ __forceinline__ unsigned long long sm_mix(unsigned long long z) {
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+__global__ void synth_fill_kernel(int dist, unsigned long long seed, void *dst, int64_t n, int64_t index0,
+                                  int64_t n_rows, int64_t n_cols) {
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const unsigned long long gi = (unsigned long long)(index0 + e);
+    const unsigned long long x = sm_mix(seed + (gi + 1ull) * 0x9E3779B97F4A7C15ull);
+    switch (dist) {
+      case 0:  // f32 U[0,1) on the 2^-24 grid
+        reinterpret_cast<float *>(dst)[e] = (float)(x >> 40) * 0x1.0p-24f;
+        break;
+      case 1:  // f32 U[-1,1)
+        reinterpret_cast<float *>(dst)[e] = 2.0f * ((float)(x >> 40) * 0x1.0p-24f) - 1.0f;
+        break;
+      case 2:  // i64 U[-2^28, 2^28)
+        reinterpret_cast<long long *>(dst)[e] = (long long)(x >> 35) - (1ll << 28);
+        break;
+      case 3: {  // bf16 U[-1,1) on the 2^-6 grid (exact)
+        const float f = ((float)(x >> 57) * 0x1.0p-7f) * 2.0f - 1.0f;
+        const unsigned int bits = __float_as_uint(f);
+        reinterpret_cast<unsigned short *>(dst)[e] = (unsigned short)(bits >> 16);
+        break;
+      }
+      case 4: {  // Jacobi initial grid: interior U[0,1), top row 1, other boundary 0
+        const int64_t i = (int64_t)gi / n_cols, j = (int64_t)gi % n_cols;
+        float v = (float)(x >> 40) * 0x1.0p-24f;
+        if (i == 0) v = 1.0f;
+        else if (i == n_rows - 1 || j == 0 || j == n_cols - 1) v = 0.0f;
+        reinterpret_cast<float *>(dst)[e] = v;
+        break;
+      }
+    }
+  }
+}
+
+cudaError_t launch_synth_fill(int dist, uint64_t stream, void *dst, int64_t n, int64_t index0, int64_t n_rows,
+                              int64_t n_cols, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const unsigned long long seed = (2209ull << 16) | (unsigned long long)stream;
+  const int threads = 256;
+  int64_t blocks = (n + threads - 1) / threads;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  synth_fill_kernel<<<(int)blocks, threads, 0, s>>>(dist, seed, dst, n, index0, n_rows, n_cols);
+  return cudaGetLastError();
+}
+
+}  // namespace upir

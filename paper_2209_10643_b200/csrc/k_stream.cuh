@@ -1,0 +1,550 @@
+// k_stream.cuh -- 1-D streaming loop kernels of upir_loop_exec:
+//   AXPY   : y[i] = y[i] + a * x[i]            (Fig. 9,
+//                                               1180-1186 Fig. 11)
+//   REDUCE : private partial p_u = (+)_{i in chunks(u)} x[i]  (Fig. 7 sync
+//            'reduction'; [REM] 929-948 mode all-unit)
+// run under the device schedule engine (sched.cuh) with the upir.sync
+// reduction fused into the loop kernel's end (reduction +
+// barrier fusion): warp butterfly -> team -> per-team slot -> last team
+// combines the slots in a fixed order and applies init (readings c9, c10).
+//
+// Two memory paths:
+//  DIRECT : every unit loads its own elements.  Used when a unit's chunk is
+//           at most one 16-B vector: adjacent units own adjacent chunks, so a
+//           warp's loads are coalesced (chunked static / dynamic, small c).
+//  STAGED : chunks longer than a vector (static block, large c): adjacent
+//           units are far apart, so per-unit loads would touch 32 lines per
+//           warp instruction.  Instead the warp stages, for each of its 32
+//           units, the unit's next 128-B (or 64-B) segment into shared
+//           memory with cp.async (8 lanes per segment: 4 full lines per
+//           instruction), NST stages deep; each unit then executes the body
+//           on ITS OWN iterations from its shared-memory row.  AXPY results
+//           go back through the row and are stored cooperatively, element-
+//           exact at unit boundaries.
+#pragma once
+#include <cuda_runtime.h>
+#include <math_constants.h>
+#include <stdint.h>
+
+#include <type_traits>
+
+#include "sched.cuh"
+
+namespace upir {
+
+static constexpr unsigned FULL = 0xffffffffu;
+
+// ---------------------------------------------------------------- combine ops
+__device__ __forceinline__ long long comb_i64(int op, long long a, long long b) {
+  if (op == UPIR_OP_SUM) return (long long)((unsigned long long)a + (unsigned long long)b);
+  if (op == UPIR_OP_MAX) return a > b ? a : b;
+  return a < b ? a : b;
+}
+__device__ __forceinline__ double comb_f(int op, double a, double b) {
+  if (op == UPIR_OP_SUM) return a + b;
+  if (op == UPIR_OP_MAX) return fmax(a, b);
+  return fmin(a, b);
+}
+__device__ __forceinline__ long long ident_i64(int op) {
+  return op == UPIR_OP_SUM ? 0LL : (op == UPIR_OP_MAX ? (long long)INT64_MIN : (long long)INT64_MAX);
+}
+__device__ __forceinline__ double ident_f(int op) {
+  return op == UPIR_OP_SUM ? 0.0 : (op == UPIR_OP_MAX ? -CUDART_INF : CUDART_INF);
+}
+__device__ __forceinline__ float ident_f32(int op) {
+  return op == UPIR_OP_SUM ? 0.0f : (op == UPIR_OP_MAX ? -CUDART_INF_F : CUDART_INF_F);
+}
+
+// Private reduction copies of one unit.  int64 data: exact int64 words.
+// fp32 data: fp64 words (reading c11: the private partial of a unit is kept
+// in double; each 16-B vector is first combined pairwise in fp32).
+template <int BODY, int NRED>
+struct Acc {
+  using W = typename std::conditional<BODY == SB_RED_I64, long long, double>::type;
+  W v[NRED > 0 ? NRED : 1];
+  int op[NRED > 0 ? NRED : 1];
+  __device__ __forceinline__ void init(const StreamArgs &a) {
+#pragma unroll
+    for (int r = 0; r < NRED; ++r) {
+      op[r] = a.red[r].op;
+      if constexpr (BODY == SB_RED_I64) v[r] = ident_i64(op[r]);
+      else v[r] = ident_f(op[r]);
+    }
+  }
+};
+
+// ---------------------------------------------------------------- memory ops
+__device__ __forceinline__ void cp_async16(void *smem, const void *gmem) {
+  const unsigned s = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(s), "l"(gmem) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <bool TRACE>
+__device__ __forceinline__ void trace_rec(const StreamArgs &a, int64_t e, int team, int unit) {
+  if constexpr (TRACE) {
+    const int64_t k = (e - a.lb) / a.step;   // normalised iteration of element e
+    a.trace[k] = team;
+    a.trace[a.T + k] = unit;
+    atomicAdd(a.trace + 2 * a.T + k, 1);
+  }
+}
+
+// Body on one element (scalar form).
+template <int BODY, int NRED, bool TRACE>
+__device__ __forceinline__ void body_scalar(const StreamArgs &a, int64_t e, Acc<BODY, NRED> &acc,
+                                            int team, int unit) {
+  if constexpr (BODY == SB_RED_I64) {
+    const long long v = __ldcs(reinterpret_cast<const long long *>(a.in0) + e);
+#pragma unroll
+    for (int r = 0; r < NRED; ++r) acc.v[r] = comb_i64(acc.op[r], acc.v[r], v);
+  } else if constexpr (BODY == SB_RED_F32) {
+    const float v = __ldcs(reinterpret_cast<const float *>(a.in0) + e);
+#pragma unroll
+    for (int r = 0; r < NRED; ++r) acc.v[r] = comb_f(acc.op[r], acc.v[r], (double)v);
+  } else {
+    const float x = __ldcs(reinterpret_cast<const float *>(a.in0) + e);
+    float *yp = reinterpret_cast<float *>(a.out) + e;
+    const float y = __ldcs(yp);
+    const float yn = __fmaf_rn(a.alpha, x, y);
+    __stcs(yp, yn);
+#pragma unroll
+    for (int r = 0; r < NRED; ++r) acc.v[r] = comb_f(acc.op[r], acc.v[r], (double)yn);
+  }
+  trace_rec<TRACE>(a, e, team, unit);
+}
+
+// Combine a 4-wide fp32 vector into the fp64 partials, masked lanes replaced
+// by the identity (pairwise in fp32 first).
+template <int BODY, int NRED>
+__device__ __forceinline__ void acc_f4(Acc<BODY, NRED> &acc, float4 v, bool m0, bool m1, bool m2,
+                                       bool m3) {
+#pragma unroll
+  for (int r = 0; r < NRED; ++r) {
+    const int op = acc.op[r];
+    const float id = ident_f32(op);
+    const float a0 = m0 ? v.x : id, a1 = m1 ? v.y : id, a2 = m2 ? v.z : id, a3 = m3 ? v.w : id;
+    float s;
+    if (op == UPIR_OP_SUM) s = __fadd_rn(__fadd_rn(a0, a1), __fadd_rn(a2, a3));
+    else if (op == UPIR_OP_MAX) s = fmaxf(fmaxf(a0, a1), fmaxf(a2, a3));
+    else s = fminf(fminf(a0, a1), fminf(a2, a3));
+    acc.v[r] = comb_f(op, acc.v[r], (double)s);
+  }
+}
+
+template <int BODY, int NRED>
+__device__ __forceinline__ void acc_l2(Acc<BODY, NRED> &acc, longlong2 v, bool m0, bool m1) {
+#pragma unroll
+  for (int r = 0; r < NRED; ++r) {
+    const int op = acc.op[r];
+    if (m0) acc.v[r] = comb_i64(op, acc.v[r], v.x);
+    if (m1) acc.v[r] = comb_i64(op, acc.v[r], v.y);
+  }
+}
+
+// ================================================================ DIRECT path
+template <int BODY, int NRED, bool TRACE>
+__device__ __forceinline__ void direct_vec(const StreamArgs &a, int64_t e, Acc<BODY, NRED> &acc,
+                                           int team, int unit) {
+  // one aligned, full 16-B vector starting at element e
+  if constexpr (BODY == SB_RED_I64) {
+    const longlong2 v = __ldcs(reinterpret_cast<const longlong2 *>(reinterpret_cast<const long long *>(a.in0) + e));
+    acc_l2(acc, v, true, true);
+  } else if constexpr (BODY == SB_RED_F32) {
+    const float4 v = __ldcs(reinterpret_cast<const float4 *>(reinterpret_cast<const float *>(a.in0) + e));
+    acc_f4(acc, v, true, true, true, true);
+  } else {
+    const float4 x = __ldcs(reinterpret_cast<const float4 *>(reinterpret_cast<const float *>(a.in0) + e));
+    float4 *yp = reinterpret_cast<float4 *>(reinterpret_cast<float *>(a.out) + e);
+    float4 y = __ldcs(yp);
+    y.x = __fmaf_rn(a.alpha, x.x, y.x);
+    y.y = __fmaf_rn(a.alpha, x.y, y.y);
+    y.z = __fmaf_rn(a.alpha, x.z, y.z);
+    y.w = __fmaf_rn(a.alpha, x.w, y.w);
+    __stcs(yp, y);
+    acc_f4(acc, y, true, true, true, true);
+  }
+  if constexpr (TRACE) {
+    constexpr int VEC = BODY == SB_RED_I64 ? 2 : 4;
+#pragma unroll
+    for (int q = 0; q < VEC; ++q) trace_rec<TRACE>(a, e + q, team, unit);
+  }
+}
+
+template <int BODY, int NRED, bool TRACE>
+__device__ void direct_run(const StreamArgs &a, const LaneWork &w, Acc<BODY, NRED> &acc, int team,
+                           int unit) {
+  if (w.nk == 0) return;
+  constexpr int VEC = BODY == SB_RED_I64 ? 2 : 4;
+  int64_t j = 0;
+  if (a.step == 1 && w.c == VEC && w.nk > 1 && ((a.lb + w.lo0) % VEC) == 0 &&
+      (w.kstride % VEC) == 0) {
+    // chunks that are one full, aligned vector inside the safe range
+    const int64_t lim = min(a.T, a.safe_hi - a.lb);   // need klo + VEC <= lim
+    int64_t nfull = 0;
+    if (lim - VEC - w.lo0 >= 0) nfull = min(w.nk, (lim - VEC - w.lo0) / w.kstride + 1);
+    const int64_t e0 = a.lb + w.lo0;
+    for (; j + 4 <= nfull; j += 4) {
+      if constexpr (BODY == SB_AXPY || TRACE) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) direct_vec<BODY, NRED, TRACE>(a, e0 + (j + q) * w.kstride, acc, team, unit);
+      } else if constexpr (BODY == SB_RED_I64) {
+        longlong2 v[4];
+        const long long *p = reinterpret_cast<const long long *>(a.in0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = __ldcs(reinterpret_cast<const longlong2 *>(p + e0 + (j + q) * w.kstride));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc_l2(acc, v[q], true, true);
+      } else {
+        float4 v[4];
+        const float *p = reinterpret_cast<const float *>(a.in0);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) v[q] = __ldcs(reinterpret_cast<const float4 *>(p + e0 + (j + q) * w.kstride));
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc_f4(acc, v[q], true, true, true, true);
+      }
+    }
+    for (; j < nfull; ++j) direct_vec<BODY, NRED, TRACE>(a, e0 + j * w.kstride, acc, team, unit);
+  }
+  // generic remainder: element by element
+  for (; j < w.nk; ++j) {
+    int64_t klo, khi;
+    chunk_bounds(w, j, a.T, klo, khi);
+    for (int64_t k = klo; k < khi; ++k) body_scalar<BODY, NRED, TRACE>(a, a.lb + k * a.step, acc, team, unit);
+  }
+}
+
+// ================================================================ STAGED path
+template <int BODY, int SEGV, int NST>
+struct StagedLayout {
+  static constexpr int ROW = SEGV * 16 + 16;                 // padded row: conflict-free
+  static constexpr int NBUF = BODY == SB_AXPY ? 2 : 1;
+  static constexpr int STAGE = 32 * ROW * NBUF;
+  static constexpr int META = 32 * 16;                        // longlong2 per lane
+  static constexpr int WARP_BYTES = NST * (STAGE + META);
+};
+
+template <int BODY, int NRED, bool TRACE, int SEGV, int NST>
+__device__ void staged_run(const StreamArgs &a, const LaneWork &w, Acc<BODY, NRED> &acc, int team,
+                           int unit, char *wsm) {
+  using L = StagedLayout<BODY, SEGV, NST>;
+  constexpr int VEC = BODY == SB_RED_I64 ? 2 : 4;
+  constexpr int ESZ = 16 / VEC;
+  constexpr int UPI = 32 / SEGV;   // units covered by one cooperative instruction
+  const int lane = threadIdx.x & 31;
+  char *rows = wsm;
+  longlong2 *meta = reinterpret_cast<longlong2 *>(wsm + NST * L::STAGE);
+  const char *gx = reinterpret_cast<const char *>(a.in0);
+  char *gy = reinterpret_cast<char *>(a.out);
+  const int64_t vec_hi = (a.safe_hi / VEC) * VEC;
+
+  int64_t j = 0, e_cur = 0, e_end = 0;
+
+  auto next_interval = [&]() -> bool {
+    while (e_cur >= e_end) {
+      if (j >= w.nk) return false;
+      int64_t klo, khi, elo, ehi;
+      chunk_bounds(w, j, a.T, klo, khi);
+      ++j;
+      elem_bounds(a.lb, a.step, klo, khi, elo, ehi);
+      const int64_t stg_hi = min(ehi, vec_hi);
+      for (int64_t e = max(elo, stg_hi); e < ehi; ++e) body_scalar<BODY, NRED, TRACE>(a, e, acc, team, unit);
+      e_cur = elo;
+      e_end = stg_hi;
+    }
+    return true;
+  };
+
+  auto issue = [&](int64_t s) -> bool {
+    const int st = (int)(s % NST);
+    longlong2 m = make_longlong2(0, 0);
+    if (next_interval()) {
+      const int64_t v0 = e_cur / VEC;
+      const int64_t vseg_end = (v0 / SEGV + 1) * SEGV;
+      const int64_t seg_hi = min(e_end, vseg_end * VEC);
+      m = make_longlong2(e_cur, seg_hi);
+      e_cur = seg_hi;
+    }
+    meta[st * 32 + lane] = m;
+    __syncwarp();
+    if (!__any_sync(FULL, m.y > m.x)) return false;
+    char *sb = rows + st * L::STAGE;
+#pragma unroll
+    for (int q = 0; q < SEGV; ++q) {
+      const int ju = q * UPI + lane / SEGV;
+      const int k = lane % SEGV;
+      const longlong2 mj = meta[st * 32 + ju];
+      if (mj.y > mj.x) {
+        const int64_t v0 = mj.x / VEC, v1 = (mj.y + VEC - 1) / VEC;
+        if (k < v1 - v0) {
+          cp_async16(sb + ju * L::ROW + k * 16, gx + (v0 + k) * 16);
+          if constexpr (BODY == SB_AXPY) cp_async16(sb + 32 * L::ROW + ju * L::ROW + k * 16, gy + (v0 + k) * 16);
+        }
+      }
+    }
+    return true;
+  };
+
+  auto consume = [&](int64_t s) {
+    const int st = (int)(s % NST);
+    const longlong2 m = meta[st * 32 + lane];
+    char *row = rows + st * L::STAGE + lane * L::ROW;
+    if (m.y > m.x) {
+      const int64_t v0 = m.x / VEC;
+#pragma unroll
+      for (int k = 0; k < SEGV; ++k) {
+        const int64_t vb = (v0 + k) * VEC;
+        if (vb < m.y) {
+          if constexpr (BODY == SB_RED_I64) {
+            const longlong2 v = *reinterpret_cast<const longlong2 *>(row + k * 16);
+            acc_l2(acc, v, vb >= m.x && vb < m.y, vb + 1 >= m.x && vb + 1 < m.y);
+          } else if constexpr (BODY == SB_RED_F32) {
+            const float4 v = *reinterpret_cast<const float4 *>(row + k * 16);
+            acc_f4(acc, v, vb >= m.x && vb < m.y, vb + 1 >= m.x && vb + 1 < m.y,
+                   vb + 2 >= m.x && vb + 2 < m.y, vb + 3 >= m.x && vb + 3 < m.y);
+          } else {
+            const float4 x = *reinterpret_cast<const float4 *>(row + k * 16);
+            float4 *yr = reinterpret_cast<float4 *>(row + 32 * L::ROW + k * 16);
+            float4 y = *yr;
+            y.x = __fmaf_rn(a.alpha, x.x, y.x);
+            y.y = __fmaf_rn(a.alpha, x.y, y.y);
+            y.z = __fmaf_rn(a.alpha, x.z, y.z);
+            y.w = __fmaf_rn(a.alpha, x.w, y.w);
+            *yr = y;
+            acc_f4(acc, y, vb >= m.x && vb < m.y, vb + 1 >= m.x && vb + 1 < m.y,
+                   vb + 2 >= m.x && vb + 2 < m.y, vb + 3 >= m.x && vb + 3 < m.y);
+          }
+          if constexpr (TRACE) {
+#pragma unroll
+            for (int q = 0; q < VEC; ++q)
+              if (vb + q >= m.x && vb + q < m.y) trace_rec<TRACE>(a, vb + q, team, unit);
+          }
+        }
+      }
+    }
+    if constexpr (BODY == SB_AXPY) {
+      __syncwarp();
+      const char *sb = rows + st * L::STAGE + 32 * L::ROW;
+#pragma unroll
+      for (int q = 0; q < SEGV; ++q) {
+        const int ju = q * UPI + lane / SEGV;
+        const int k = lane % SEGV;
+        const longlong2 mj = meta[st * 32 + ju];
+        if (mj.y > mj.x) {
+          const int64_t v0 = mj.x / VEC, v1 = (mj.y + VEC - 1) / VEC;
+          if (k < v1 - v0) {
+            const int64_t vb = (v0 + k) * VEC;
+            const float4 y = *reinterpret_cast<const float4 *>(sb + ju * L::ROW + k * 16);
+            float *dst = reinterpret_cast<float *>(gy) + vb;
+            if (vb >= mj.x && vb + VEC <= mj.y) {
+              __stcs(reinterpret_cast<float4 *>(dst), y);
+            } else {   // partial vector at a unit boundary: element-exact stores
+              const float yy[4] = {y.x, y.y, y.z, y.w};
+#pragma unroll
+              for (int qq = 0; qq < 4; ++qq)
+                if (vb + qq >= mj.x && vb + qq < mj.y) dst[qq] = yy[qq];
+            }
+          }
+        }
+      }
+    }
+  };
+
+  int64_t s_issue = 0, s_cons = 0;
+  bool more = true;
+#pragma unroll
+  for (int q = 0; q < NST - 1; ++q) {
+    if (more) {
+      more = issue(s_issue);
+      if (more) ++s_issue;
+    }
+    cp_async_commit();
+  }
+  while (s_cons < s_issue) {
+    if (more) {
+      more = issue(s_issue);
+      if (more) ++s_issue;
+    }
+    cp_async_commit();
+    cp_async_wait<NST - 1>();
+    __syncwarp();
+    consume(s_cons);
+    ++s_cons;
+    __syncwarp();
+  }
+  (void)ESZ;
+}
+
+// ================================================================ epilogue
+// Team tree then last-team combine (reading c10).  Words are 8 bytes.
+template <int BODY, int NRED>
+__device__ void reduce_epilogue(const StreamArgs &a, Acc<BODY, NRED> &acc, bool need_ticket) {
+  __shared__ unsigned long long s_part[32][2];
+  __shared__ int s_last;
+  using W = typename Acc<BODY, NRED>::W;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = (blockDim.x + 31) >> 5;
+  auto comb = [](int op, W x, W y) -> W {
+    if constexpr (BODY == SB_RED_I64) return comb_i64(op, x, y);
+    else return comb_f(op, x, y);
+  };
+  auto ident = [](int op) -> W {
+    if constexpr (BODY == SB_RED_I64) return ident_i64(op);
+    else return ident_f(op);
+  };
+  auto to_bits = [](W x) -> unsigned long long {
+    if constexpr (BODY == SB_RED_I64) return (unsigned long long)x;
+    else return (unsigned long long)__double_as_longlong(x);
+  };
+  auto from_bits = [](unsigned long long b) -> W {
+    if constexpr (BODY == SB_RED_I64) return (W)(long long)b;
+    else return __longlong_as_double((long long)b);
+  };
+  auto block_tree = [&](W (&v)[NRED > 0 ? NRED : 1]) {
+#pragma unroll
+    for (int r = 0; r < NRED; ++r) {
+#pragma unroll
+      for (int m = 16; m >= 1; m >>= 1) {
+        const W o = from_bits(__shfl_xor_sync(FULL, to_bits(v[r]), m));
+        v[r] = comb(a.red[r].op, v[r], o);
+      }
+      if (lane == 0) s_part[warp][r] = to_bits(v[r]);
+    }
+    __syncthreads();
+    if (warp == 0) {
+#pragma unroll
+      for (int r = 0; r < NRED; ++r) {
+        W x = lane < nwarps ? from_bits(s_part[lane][r]) : ident(a.red[r].op);
+#pragma unroll
+        for (int m = 16; m >= 1; m >>= 1) x = comb(a.red[r].op, x, from_bits(__shfl_xor_sync(FULL, to_bits(x), m)));
+        v[r] = x;
+      }
+    }
+    __syncthreads();
+  };
+
+  if constexpr (NRED > 0) {
+    block_tree(acc.v);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int r = 0; r < NRED; ++r) a.slots[(size_t)blockIdx.x * 2 + r] = to_bits(acc.v[r]);
+    }
+  }
+  if (!need_ticket) return;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    const unsigned t = atomicAdd(a.done, 1u);
+    s_last = (t == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if constexpr (NRED > 0) {
+    W v[NRED];
+#pragma unroll
+    for (int r = 0; r < NRED; ++r) {
+      W x = ident(a.red[r].op);
+      for (unsigned b = threadIdx.x; b < gridDim.x; b += blockDim.x)
+        x = comb(a.red[r].op, x, from_bits(__ldcg(a.slots + (size_t)b * 2 + r)));
+      v[r] = x;
+    }
+    block_tree(v);
+    if (threadIdx.x == 0) {
+#pragma unroll
+      for (int r = 0; r < NRED; ++r) {
+        const RedSpec &rs = a.red[r];
+        if constexpr (BODY == SB_RED_I64) {
+          const long long res = comb_i64(rs.op, (long long)rs.init_bits, v[r]);
+          *reinterpret_cast<long long *>(rs.result) = res;
+        } else {
+          const double res = comb_f(rs.op, __longlong_as_double((long long)rs.init_bits), v[r]);
+          *reinterpret_cast<float *>(rs.result) = (float)res;
+        }
+      }
+    }
+  }
+  if (threadIdx.x == 0) {
+    *a.done = 0u;                                      // self-reset for the next launch
+    if (a.dyn_counter) *a.dyn_counter = 0ull;
+  }
+}
+
+// ================================================================ kernel
+template <int BODY, int NRED, bool TRACE, int PATH, int SEGV, int NST>
+__global__ void __launch_bounds__(1024) stream_loop_kernel(const __grid_constant__ StreamArgs a) {
+  extern __shared__ __align__(128) char dyn_smem[];
+  const UnitIds u = unit_ids(a.distribute);
+  const int team = blockIdx.x, unit = threadIdx.x;
+  Acc<BODY, NRED> acc;
+  acc.init(a);
+  char *wsm = nullptr;
+  if constexpr (PATH == PATH_STAGED) wsm = dyn_smem + (threadIdx.x >> 5) * StagedLayout<BODY, SEGV, NST>::WARP_BYTES;
+
+  auto run = [&](const LaneWork &w) {
+    if constexpr (PATH == PATH_STAGED) staged_run<BODY, NRED, TRACE, SEGV, NST>(a, w, acc, team, unit, wsm);
+    else direct_run<BODY, NRED, TRACE>(a, w, acc, team, unit);
+  };
+
+  if (a.sched == SK_DYNAMIC) {
+    __shared__ long long s_base;
+    const int64_t nchunks = (a.T + a.chunk - 1) / a.chunk;
+    const unsigned long long tu = (unsigned long long)u.p_team * (unsigned long long)a.ticket_m;
+    for (;;) {
+      if (threadIdx.x == 0) s_base = (long long)atomicAdd(a.dyn_counter, tu);
+      __syncthreads();
+      const int64_t b = s_base;
+      __syncthreads();
+      if (b >= nchunks) break;
+      run(ticket_work(b, a.ticket_m, a.T, a.chunk, u));
+    }
+  } else {
+    run(static_work(a.sched, a.T, a.chunk, u));
+  }
+  reduce_epilogue<BODY, NRED>(a, acc, NRED > 0 || a.sched == SK_DYNAMIC);
+}
+
+// Host-side dispatch over (NRED, TRACE, PATH config) for one body.
+template <int BODY>
+cudaError_t launch_stream_body(int nred, int path, int segv, int nst, bool trace, int teams,
+                               int units, size_t smem, const StreamArgs &a, cudaStream_t s) {
+  void (*k)(StreamArgs) = nullptr;
+#define UPIR_PICK(NR, TR)                                                                  \
+  if (path == PATH_DIRECT) k = stream_loop_kernel<BODY, NR, TR, PATH_DIRECT, 0, 0>;        \
+  else if (segv == 8 && nst == 4) k = stream_loop_kernel<BODY, NR, TR, PATH_STAGED, 8, 4>; \
+  else if (segv == 8 && nst == 3) k = stream_loop_kernel<BODY, NR, TR, PATH_STAGED, 8, 3>; \
+  else if (segv == 8 && nst == 2) k = stream_loop_kernel<BODY, NR, TR, PATH_STAGED, 8, 2>; \
+  else if (segv == 4 && nst == 3) k = stream_loop_kernel<BODY, NR, TR, PATH_STAGED, 4, 3>; \
+  else if (segv == 4 && nst == 2) k = stream_loop_kernel<BODY, NR, TR, PATH_STAGED, 4, 2>;
+  if (nred == 0) {
+    if (trace) { UPIR_PICK(0, true) } else { UPIR_PICK(0, false) }
+  } else if (nred == 1) {
+    if (trace) { UPIR_PICK(1, true) } else { UPIR_PICK(1, false) }
+  } else {
+    if (trace) { UPIR_PICK(2, true) } else { UPIR_PICK(2, false) }
+  }
+#undef UPIR_PICK
+  if (!k) return cudaErrorInvalidValue;
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k<<<teams, units, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
+template <int BODY>
+size_t staged_bytes_body(int units, int segv, int nst) {
+  const int warps = (units + 31) / 32;
+  size_t per = 0;
+  if (segv == 8 && nst == 4) per = StagedLayout<BODY, 8, 4>::WARP_BYTES;
+  else if (segv == 8 && nst == 3) per = StagedLayout<BODY, 8, 3>::WARP_BYTES;
+  else if (segv == 8 && nst == 2) per = StagedLayout<BODY, 8, 2>::WARP_BYTES;
+  else if (segv == 4 && nst == 3) per = StagedLayout<BODY, 4, 3>::WARP_BYTES;
+  else if (segv == 4 && nst == 2) per = StagedLayout<BODY, 4, 2>::WARP_BYTES;
+  return per * warps;
+}
+
+}  // namespace upir

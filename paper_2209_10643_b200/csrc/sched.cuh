@@ -1,0 +1,116 @@
+// sched.cuh -- device schedule engine of upir.loop_parallel worksharing
+// (Fig. 3; readings c3-c8 of DESIGN.md).
+//
+// A unit's share of the normalised iteration space [0, T) is described as a
+// strided sequence of chunks:
+//     chunk j = [lo0 + j*kstride, min(lo0 + j*kstride + c, T)),  j in [0, nk)
+// static block  : one chunk [g*q + min(g,r), +q + (g<r))
+// static chunk c: chunks k = g, g+p, ...   -> lo0 = g*c, kstride = p*c
+// dynamic c     : a team claims a ticket of p_team*m consecutive chunks with one
+//                 atomicAdd; unit u of the team takes chunks b + u + j*p_team
+//                 (j < m): chunk boundaries are exact, each unit's chunks are
+//                 increasing, the unit assignment is decided at run time (c8).
+#pragma once
+#include <stdint.h>
+
+#include "upir_internal.h"
+
+namespace upir {
+
+struct LaneWork {
+  int64_t lo0, kstride, nk, c;
+};
+
+struct UnitIds {
+  int64_t g;       // schedule unit id (meaningful when active)
+  int64_t p;       // number of schedule units
+  int p_team;      // active units in this team (dynamic tickets)
+  int u_team;      // index of this unit among the team's active units
+  bool active;
+};
+
+// distribute (readings c5-c7):
+//   TEAMS_UNITS: flat g = team*units + unit, p = teams*units
+//   TEAMS      : p = teams, unit 0 of each team executes
+//   UNITS      : p = units (a single team)
+__device__ __forceinline__ UnitIds unit_ids(int distribute) {
+  UnitIds u;
+  if (distribute == UPIR_DIST_TEAMS) {
+    u.g = blockIdx.x;
+    u.p = gridDim.x;
+    u.p_team = 1;
+    u.u_team = 0;
+    u.active = threadIdx.x == 0;
+  } else if (distribute == UPIR_DIST_UNITS) {
+    u.g = threadIdx.x;
+    u.p = blockDim.x;
+    u.p_team = blockDim.x;
+    u.u_team = threadIdx.x;
+    u.active = true;
+  } else {
+    u.g = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    u.p = (int64_t)gridDim.x * blockDim.x;
+    u.p_team = blockDim.x;
+    u.u_team = threadIdx.x;
+    u.active = true;
+  }
+  return u;
+}
+
+__device__ __forceinline__ LaneWork static_work(int sched, int64_t T, int64_t c, const UnitIds &u) {
+  LaneWork w{0, 0, 0, 1};
+  if (!u.active || T <= 0) return w;
+  if (sched == SK_STATIC_BLOCK) {
+    const int64_t q = T / u.p, r = T % u.p;
+    const int64_t start = u.g * q + (u.g < r ? u.g : r);
+    const int64_t len = q + (u.g < r ? 1 : 0);
+    w.lo0 = start;
+    w.c = len > 0 ? len : 1;
+    w.nk = len > 0 ? 1 : 0;
+    return w;
+  }
+  // static, chunk c
+  const int64_t nchunks = (T + c - 1) / c;
+  w.c = c;
+  w.lo0 = u.g * c;
+  w.kstride = u.p * c;
+  w.nk = u.g < nchunks ? (nchunks - 1 - u.g) / u.p + 1 : 0;
+  return w;
+}
+
+// Unit's chunks of a dynamic ticket starting at chunk b (m chunks per unit).
+__device__ __forceinline__ LaneWork ticket_work(int64_t b, int64_t m, int64_t T, int64_t c,
+                                                const UnitIds &u) {
+  LaneWork w{0, 0, 0, c};
+  if (!u.active) return w;
+  const int64_t nchunks = (T + c - 1) / c;
+  const int64_t first = b + u.u_team;
+  if (first >= nchunks) return w;
+  const int64_t cnt = (nchunks - 1 - first) / u.p_team + 1;
+  w.nk = cnt < m ? cnt : m;
+  w.lo0 = first * c;
+  w.kstride = (int64_t)u.p_team * c;
+  return w;
+}
+
+// Chunk j of a lane's work, in the normalised space.
+__device__ __forceinline__ void chunk_bounds(const LaneWork &w, int64_t j, int64_t T, int64_t &klo,
+                                             int64_t &khi) {
+  klo = w.lo0 + j * w.kstride;
+  khi = klo + w.c;
+  if (khi > T) khi = T;
+}
+
+// Element interval [elo, ehi) covered by normalised [klo, khi) when |step| == 1.
+__device__ __forceinline__ void elem_bounds(int64_t lb, int64_t step, int64_t klo, int64_t khi,
+                                            int64_t &elo, int64_t &ehi) {
+  if (step == 1) {
+    elo = lb + klo;
+    ehi = lb + khi;
+  } else {  // step == -1: i = lb - k
+    elo = lb - khi + 1;
+    ehi = lb - klo + 1;
+  }
+}
+
+}  // namespace upir

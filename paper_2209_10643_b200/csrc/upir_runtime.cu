@@ -1,0 +1,1027 @@
+// upir_runtime.cu -- host runtime behind include/upir.h.
+//
+// Context (streams, workspace, NCCL communicator), the upir.data present
+// table (Figs. 5-6; reading c18), descriptor validation and
+// normalisation of upir.spmd / upir.loop / loop_parallel (Figs. 1, 3), launch
+// dispatch to the sm_100a kernels, upir.sync (Fig. 7) and CUDA-graph capture.
+// No C++ exception crosses the ABI; every entry point returns upir_status.
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <nccl.h>
+#include <stdarg.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+#include <algorithm>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "upir_internal.h"
+
+using namespace upir;
+
+// ------------------------------------------------------------------ errors
+static thread_local std::string g_err;
+
+static upir_status fail(upir_status s, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return s;
+}
+
+#define CUDA_TRY(expr)                                                                      \
+  do {                                                                                      \
+    cudaError_t _e = (expr);                                                                \
+    if (_e != cudaSuccess)                                                                  \
+      return fail(UPIR_E_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(_e), __FILE__, __LINE__); \
+  } while (0)
+
+#define NCCL_TRY(expr)                                                                      \
+  do {                                                                                      \
+    ncclResult_t _r = (expr);                                                               \
+    if (_r != ncclSuccess)                                                                  \
+      return fail(UPIR_E_NCCL, "%s failed: %s", #expr, ncclGetErrorString(_r));             \
+  } while (0)
+
+extern "C" const char *upir_last_error(void) { return g_err.c_str(); }
+extern "C" const char *upir_version(void) { return "upir-b200 0.1 (sm_100a)"; }
+
+// ------------------------------------------------------------------ objects
+struct upir_map_s {
+  upir_ctx ctx;
+  void *host;
+  size_t bytes;          // global bytes of the host array (or adopted bytes)
+  int kind;
+  void *dev;             // local device buffer
+  size_t dev_bytes;      // local bytes
+  bool owned;            // dev allocated by us
+  int refcount;
+  // distribution
+  upir_dist dist;
+  int64_t row_lo, row_hi;        // owned rows
+  int64_t loc_row_lo, loc_row_hi;  // rows held locally (halo included)
+  int64_t elems_local;           // local elements (rows*row_elems)
+  int64_t elem_offset;           // global element index of local element 0
+  int64_t elem_bytes;
+};
+
+struct upir_event_s {
+  cudaEvent_t ev;
+};
+
+struct upir_graph_s {
+  cudaGraph_t graph;
+  cudaGraphExec_t exec;
+};
+
+struct upir_spmd_s {
+  upir_ctx ctx;
+  upir_spmd_desc d;
+};
+
+struct upir_ctx_s {
+  int device = 0;
+  int rank = 0, nranks = 1;
+  int num_sms = 148;
+  cudaStream_t compute = nullptr, copy = nullptr;
+  bool own_compute = false, own_copy = false;
+  ncclComm_t comm = nullptr;
+  // workspace
+  unsigned long long *slots = nullptr;
+  size_t slots_teams = 0;
+  unsigned int *done = nullptr;
+  unsigned long long *dyn = nullptr;
+  void *scratch = nullptr;      // world-reduce gather buffer
+  size_t scratch_bytes = 0;
+  void *one = nullptr;          // 1-element buffer for the world barrier
+  // present table: host pointer -> map
+  std::map<void *, upir_map> present;
+  std::vector<upir_map> adopted;
+  std::vector<std::pair<void *, size_t>> registered;   // host ranges we pinned
+  std::vector<upir_spmd> regions;
+  cudaError_t sticky = cudaSuccess;
+  bool capturing = false;
+  // statistics
+  int64_t h2d_bytes = 0, d2h_bytes = 0, launches = 0;
+};
+
+static upir_status sticky_check(upir_ctx c) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess && c->sticky == cudaSuccess) c->sticky = e;
+  if (c->sticky != cudaSuccess)
+    return fail(UPIR_E_CUDA, "asynchronous CUDA error: %s", cudaGetErrorString(c->sticky));
+  return UPIR_OK;
+}
+
+static upir_status ensure_slots(upir_ctx c, size_t teams) {
+  if (teams <= c->slots_teams) return UPIR_OK;
+  if (c->capturing) return fail(UPIR_E_INVALID, "workspace must grow (teams=%zu) but a graph is being captured", teams);
+  CUDA_TRY(cudaStreamSynchronize(c->compute));
+  if (c->slots) CUDA_TRY(cudaFree(c->slots));
+  size_t n = std::max(teams, (size_t)1 << 16);
+  CUDA_TRY(cudaMalloc(&c->slots, n * 2 * sizeof(unsigned long long)));
+  c->slots_teams = n;
+  return UPIR_OK;
+}
+
+// ------------------------------------------------------------------ lifecycle
+extern "C" upir_status upir_init(int cuda_device, const upir_world *world, upir_ctx *out) {
+  if (!out) return fail(UPIR_E_INVALID, "out is NULL");
+  int ndev = 0;
+  cudaError_t e = cudaGetDeviceCount(&ndev);
+  if (e != cudaSuccess || ndev == 0)
+    return fail(UPIR_E_CUDA, "no CUDA device available (%s); this runtime has no CPU fallback",
+                cudaGetErrorString(e));
+  if (cuda_device < 0 || cuda_device >= ndev) return fail(UPIR_E_INVALID, "device %d out of range", cuda_device);
+  cudaDeviceProp prop;
+  CUDA_TRY(cudaGetDeviceProperties(&prop, cuda_device));
+  if (prop.major != 10)
+    return fail(UPIR_E_UNSUPPORTED, "device %d is sm_%d%d; this build targets sm_100a only", cuda_device,
+                prop.major, prop.minor);
+  if (world && (world->nranks < 1 || world->rank < 0 || world->rank >= world->nranks))
+    return fail(UPIR_E_INVALID, "bad world rank %d / nranks %d", world->rank, world->nranks);
+  if (world && world->nranks > 1 && !world->nccl_id) return fail(UPIR_E_INVALID, "nranks > 1 needs an nccl_id");
+  CUDA_TRY(cudaSetDevice(cuda_device));
+  upir_ctx c = new upir_ctx_s();
+  c->device = cuda_device;
+  c->num_sms = prop.multiProcessorCount;
+  if (world) {
+    c->rank = world->rank;
+    c->nranks = world->nranks;
+    c->compute = (cudaStream_t)world->compute_stream;
+    c->copy = (cudaStream_t)world->copy_stream;
+  }
+  auto cleanup = [&](upir_status s) { delete c; return s; };
+  if (!c->compute) {
+    if (cudaStreamCreateWithFlags(&c->compute, cudaStreamNonBlocking) != cudaSuccess)
+      return cleanup(fail(UPIR_E_CUDA, "stream create failed"));
+    c->own_compute = true;
+  }
+  if (!c->copy) {
+    if (cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking) != cudaSuccess)
+      return cleanup(fail(UPIR_E_CUDA, "stream create failed"));
+    c->own_copy = true;
+  }
+  if (cudaMalloc(&c->done, 256) != cudaSuccess || cudaMemset(c->done, 0, 256) != cudaSuccess)
+    return cleanup(fail(UPIR_E_OOM, "workspace allocation failed"));
+  c->dyn = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(c->done) + 64);
+  if (cudaMalloc(&c->one, 64) != cudaSuccess) return cleanup(fail(UPIR_E_OOM, "workspace allocation failed"));
+  if (ensure_slots(c, (size_t)1 << 16) != UPIR_OK) return cleanup(UPIR_E_OOM);
+  if (c->nranks > 1) {
+    ncclUniqueId id;
+    memcpy(&id, world->nccl_id, sizeof id);
+    ncclResult_t r = ncclCommInitRank(&c->comm, c->nranks, id, c->rank);
+    if (r != ncclSuccess) return cleanup(fail(UPIR_E_NCCL, "ncclCommInitRank: %s", ncclGetErrorString(r)));
+  }
+  *out = c;
+  return UPIR_OK;
+}
+
+extern "C" upir_status upir_comm_unique_id(void *out128) {
+  if (!out128) return fail(UPIR_E_INVALID, "out is NULL");
+  static_assert(sizeof(ncclUniqueId) == 128, "ncclUniqueId is 128 bytes");
+  ncclUniqueId id;
+  NCCL_TRY(ncclGetUniqueId(&id));
+  memcpy(out128, &id, sizeof id);
+  return UPIR_OK;
+}
+
+extern "C" upir_status upir_ctx_stream(upir_ctx c, int which, uintptr_t *out) {
+  if (!c || !out || (which != 0 && which != 1)) return fail(UPIR_E_INVALID, "bad argument");
+  *out = (uintptr_t)(which == 0 ? c->compute : c->copy);
+  return UPIR_OK;
+}
+
+extern "C" upir_status upir_ctx_stats(upir_ctx c, int64_t out[4]) {
+  if (!c || !out) return fail(UPIR_E_INVALID, "bad argument");
+  out[0] = c->h2d_bytes;
+  out[1] = c->d2h_bytes;
+  out[2] = (int64_t)(c->present.size() + c->adopted.size());
+  out[3] = c->launches;
+  return UPIR_OK;
+}
+
+extern "C" upir_status upir_finalize(upir_ctx c) {
+  if (!c) return fail(UPIR_E_INVALID, "ctx is NULL");
+  cudaSetDevice(c->device);
+  cudaStreamSynchronize(c->compute);
+  cudaStreamSynchronize(c->copy);
+  if (!c->present.empty() || !c->adopted.empty())
+    return fail(UPIR_E_LEAK, "finalize with %zu live maps", c->present.size() + c->adopted.size());
+  upir_status st = sticky_check(c);
+  for (auto &r : c->registered) cudaHostUnregister(r.first);
+  for (auto s : c->regions) delete s;
+  if (c->comm) ncclCommDestroy(c->comm);
+  cudaFree(c->slots);
+  cudaFree(c->done);
+  cudaFree(c->one);
+  if (c->scratch) cudaFree(c->scratch);
+  if (c->own_compute) cudaStreamDestroy(c->compute);
+  if (c->own_copy) cudaStreamDestroy(c->copy);
+  delete c;
+  return st;
+}
+
+// ------------------------------------------------------------------ distribution
+extern "C" upir_status upir_dist_owned_rows(int64_t n_rows, int32_t rank, int32_t nranks, int64_t *lo,
+                                            int64_t *hi) {
+  if (!lo || !hi || nranks < 1 || rank < 0 || rank >= nranks || n_rows < 0)
+    return fail(UPIR_E_INVALID, "bad distribution arguments");
+  // reading c20: the static block rule over ranks
+  const int64_t q = n_rows / nranks, r = n_rows % nranks;
+  *lo = rank * q + std::min<int64_t>(rank, r);
+  *hi = *lo + q + (rank < r ? 1 : 0);
+  return UPIR_OK;
+}
+
+static upir_status layout_map(upir_ctx c, upir_map m, size_t bytes, const upir_dist *dist) {
+  if (dist && dist->pattern == UPIR_PATTERN_BLOCK) {
+    if (dist->n_rows < 1 || dist->row_elems < 1 || dist->elem_bytes < 1 || dist->halo_rows < 0)
+      return fail(UPIR_E_INVALID, "bad upir_dist");
+    if ((size_t)(dist->n_rows * dist->row_elems * dist->elem_bytes) != bytes)
+      return fail(UPIR_E_INVALID, "upir_dist extent (%lld rows x %lld x %lld B) != bytes %zu",
+                  (long long)dist->n_rows, (long long)dist->row_elems, (long long)dist->elem_bytes, bytes);
+    m->dist = *dist;
+    upir_dist_owned_rows(dist->n_rows, c->rank, c->nranks, &m->row_lo, &m->row_hi);
+    m->loc_row_lo = std::max<int64_t>(0, m->row_lo - dist->halo_rows);
+    m->loc_row_hi = std::min<int64_t>(dist->n_rows, m->row_hi + dist->halo_rows);
+    m->elem_bytes = dist->elem_bytes;
+    m->elems_local = (m->loc_row_hi - m->loc_row_lo) * dist->row_elems;
+    m->elem_offset = m->loc_row_lo * dist->row_elems;
+    m->dev_bytes = (size_t)(m->elems_local * dist->elem_bytes);
+  } else {
+    if (dist && dist->pattern != UPIR_PATTERN_NONE) return fail(UPIR_E_INVALID, "unknown pattern");
+    memset(&m->dist, 0, sizeof m->dist);
+    m->elem_bytes = 1;
+    m->row_lo = m->loc_row_lo = 0;
+    m->row_hi = m->loc_row_hi = (int64_t)bytes;
+    m->elems_local = (int64_t)bytes;
+    m->elem_offset = 0;
+    m->dev_bytes = bytes;
+  }
+  return UPIR_OK;
+}
+
+// bytes of host / device ranges moved by a map: local rows (halo included) on
+// enter; owned rows on exit.
+static void map_range(upir_map m, bool owned_only, size_t &host_off, size_t &dev_off, size_t &len) {
+  if (m->dist.pattern == UPIR_PATTERN_BLOCK) {
+    const int64_t rb = m->dist.row_elems * m->dist.elem_bytes;
+    const int64_t r0 = owned_only ? m->row_lo : m->loc_row_lo;
+    const int64_t r1 = owned_only ? m->row_hi : m->loc_row_hi;
+    host_off = (size_t)(r0 * rb);
+    dev_off = (size_t)((r0 - m->loc_row_lo) * rb);
+    len = (size_t)((r1 - r0) * rb);
+  } else {
+    host_off = dev_off = 0;
+    len = m->bytes;
+  }
+}
+
+static upir_status pin_host(upir_ctx c, void *host, size_t bytes) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, host) == cudaSuccess &&
+      (at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeManaged))
+    return UPIR_OK;
+  cudaGetLastError();
+  for (auto &r : c->registered)
+    if ((char *)host >= (char *)r.first && (char *)host + bytes <= (char *)r.first + r.second) return UPIR_OK;
+  cudaError_t e = cudaHostRegister(host, bytes, cudaHostRegisterDefault);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return UPIR_OK;   // pageable copies still work (synchronously staged by the driver)
+  }
+  c->registered.push_back({host, bytes});
+  return UPIR_OK;
+}
+
+// compute stream waits for everything enqueued on the copy stream so far
+static upir_status copy_to_compute(upir_ctx c) {
+  cudaEvent_t ev;
+  CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(ev, c->copy));
+  CUDA_TRY(cudaStreamWaitEvent(c->compute, ev, 0));
+  CUDA_TRY(cudaEventDestroy(ev));
+  return UPIR_OK;
+}
+static upir_status compute_to_copy(upir_ctx c) {
+  cudaEvent_t ev;
+  CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CUDA_TRY(cudaEventRecord(ev, c->compute));
+  CUDA_TRY(cudaStreamWaitEvent(c->copy, ev, 0));
+  CUDA_TRY(cudaEventDestroy(ev));
+  return UPIR_OK;
+}
+
+extern "C" upir_status upir_data_map(upir_ctx c, void *host, size_t bytes, upir_map_kind kind,
+                                     const upir_dist *dist, upir_map *out) {
+  if (!c || !host || !out) return fail(UPIR_E_INVALID, "NULL argument");
+  if (kind < UPIR_MAP_TO || kind > UPIR_MAP_ALLOC) return fail(UPIR_E_INVALID, "bad map kind %d", (int)kind);
+  if (bytes == 0) return fail(UPIR_E_INVALID, "zero-byte map");
+  auto it = c->present.find(host);
+  if (it != c->present.end()) {   // present: refcount only (reading c18)
+    if (it->second->bytes != bytes) return fail(UPIR_E_INVALID, "host pointer already mapped with %zu bytes", it->second->bytes);
+    it->second->refcount++;
+    *out = it->second;
+    return UPIR_OK;
+  }
+  upir_map m = new upir_map_s();
+  m->ctx = c;
+  m->host = host;
+  m->bytes = bytes;
+  m->kind = kind;
+  m->owned = true;
+  m->refcount = 1;
+  upir_status st = layout_map(c, m, bytes, dist);
+  if (st != UPIR_OK) { delete m; return st; }
+  cudaSetDevice(c->device);
+  // mm_allocator (Fig. 6): stream-ordered allocation, rounded to 256 B so
+  // vector paths may read the last partial vector's bytes safely.
+  size_t alloc = (m->dev_bytes + 255) & ~(size_t)255;
+  cudaError_t e = cudaMallocAsync(&m->dev, alloc, c->copy);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    delete m;
+    return fail(UPIR_E_OOM, "device allocation of %zu bytes failed: %s", alloc, cudaGetErrorString(e));
+  }
+  if (kind == UPIR_MAP_TO || kind == UPIR_MAP_TOFROM) {   // data_movement forward
+    pin_host(c, host, bytes);
+    size_t ho, dof, len;
+    map_range(m, false, ho, dof, len);
+    e = cudaMemcpyAsync((char *)m->dev + dof, (char *)host + ho, len, cudaMemcpyHostToDevice, c->copy);
+    if (e != cudaSuccess) {
+      cudaFreeAsync(m->dev, c->copy);
+      delete m;
+      return fail(UPIR_E_CUDA, "H2D copy failed: %s", cudaGetErrorString(e));
+    }
+    c->h2d_bytes += (int64_t)len;
+  } else if (kind == UPIR_MAP_FROM || kind == UPIR_MAP_TOFROM) {
+    pin_host(c, host, bytes);
+  }
+  st = copy_to_compute(c);
+  if (st != UPIR_OK) return st;
+  c->present[host] = m;
+  *out = m;
+  return UPIR_OK;
+}
+
+extern "C" upir_status upir_data_adopt(upir_ctx c, void *dev_ptr, size_t bytes, const upir_dist *dist,
+                                       upir_map *out) {
+  if (!c || !dev_ptr || !out || bytes == 0) return fail(UPIR_E_INVALID, "bad argument");
+  upir_map m = new upir_map_s();
+  m->ctx = c;
+  m->host = nullptr;
+  m->bytes = bytes;
+  m->kind = 0;
+  m->owned = false;
+  m->refcount = 1;
+  m->dev = dev_ptr;
+  // an adopted buffer holds this rank's local rows of a distributed array
+  upir_status st = layout_map(c, m, dist ? (size_t)(dist->n_rows * dist->row_elems * dist->elem_bytes) : bytes, dist);
+  if (st != UPIR_OK) { delete m; return st; }
+  if (dist && dist->pattern == UPIR_PATTERN_BLOCK && (size_t)m->dev_bytes > bytes) {
+    delete m;
+    return fail(UPIR_E_INVALID, "adopted buffer (%zu B) smaller than the local block (%zu B)", bytes, m->dev_bytes);
+  }
+  if (!dist || dist->pattern != UPIR_PATTERN_BLOCK) m->dev_bytes = bytes;
+  c->adopted.push_back(m);
+  *out = m;
+  return UPIR_OK;
+}
+
+extern "C" upir_status upir_data_unmap(upir_ctx c, upir_map m) {
+  if (!c || !m || m->ctx != c) return fail(UPIR_E_INVALID, "bad map");
+  if (!m->owned) {
+    auto it = std::find(c->adopted.begin(), c->adopted.end(), m);
+    if (it == c->adopted.end()) return fail(UPIR_E_INVALID, "map not live");
+    c->adopted.erase(it);
+    delete m;
+    return sticky_check(c);
+  }
+  auto it = c->present.find(m->host);
+  if (it == c->present.end() || it->second != m) return fail(UPIR_E_INVALID, "map not live");
+  if (--m->refcount > 0) return UPIR_OK;
+  upir_status st = compute_to_copy(c);
+  if (st != UPIR_OK) return st;
+  if (m->kind == UPIR_MAP_FROM || m->kind == UPIR_MAP_TOFROM) {   // data_movement backward
+    size_t ho, dof, len;
+    map_range(m, true, ho, dof, len);
+    CUDA_TRY(cudaMemcpyAsync((char *)m->host + ho, (char *)m->dev + dof, len, cudaMemcpyDeviceToHost, c->copy));
+    c->d2h_bytes += (int64_t)len;
+  }
+  CUDA_TRY(cudaFreeAsync(m->dev, c->copy));   // mm_deallocator
+  c->present.erase(it);
+  delete m;
+  return sticky_check(c);
+}
+
+extern "C" upir_status upir_data_update(upir_ctx c, upir_map m, int direction) {
+  if (!c || !m || m->ctx != c || !m->owned || !m->host) return fail(UPIR_E_INVALID, "bad map");
+  if (direction != 0 && direction != 1) return fail(UPIR_E_INVALID, "direction must be 0 or 1");
+  upir_status st = compute_to_copy(c);
+  if (st != UPIR_OK) return st;
+  size_t ho, dof, len;
+  if (direction == 0) {
+    map_range(m, false, ho, dof, len);
+    pin_host(c, m->host, m->bytes);
+    CUDA_TRY(cudaMemcpyAsync((char *)m->dev + dof, (char *)m->host + ho, len, cudaMemcpyHostToDevice, c->copy));
+    c->h2d_bytes += (int64_t)len;
+  } else {
+    map_range(m, true, ho, dof, len);
+    pin_host(c, m->host, m->bytes);
+    CUDA_TRY(cudaMemcpyAsync((char *)m->host + ho, (char *)m->dev + dof, len, cudaMemcpyDeviceToHost, c->copy));
+    c->d2h_bytes += (int64_t)len;
+  }
+  return copy_to_compute(c);
+}
+
+extern "C" upir_status upir_data_device_ptr(upir_map m, void **dptr, int64_t *local_elems, int64_t *global_offset) {
+  if (!m) return fail(UPIR_E_INVALID, "map is NULL");
+  if (dptr) *dptr = m->dev;
+  if (local_elems) *local_elems = m->elems_local;
+  if (global_offset) *global_offset = m->elem_offset;
+  return UPIR_OK;
+}
+
+// ------------------------------------------------------------------ spmd
+static upir_status validate_spmd(const upir_spmd_desc *d) {
+  if (!d) return fail(UPIR_E_INVALID, "spmd descriptor is NULL");
+  // lesson of PAPER.md:1578-1587: honour the requested geometry or reject it
+  if (d->num_units < 1 || d->num_units > 1024)
+    return fail(UPIR_E_INVALID, "num_units=%d outside [1,1024] (geometry is never clamped)", d->num_units);
+  if (d->num_teams < 1) return fail(UPIR_E_INVALID, "num_teams=%d < 1", d->num_teams);
+  if (d->target != UPIR_TARGET_GPU && d->target != UPIR_TARGET_CLUSTER)
+    return fail(UPIR_E_INVALID, "target must be GPU or CLUSTER");
+  return UPIR_OK;
+}
+
+extern "C" upir_status upir_spmd_launch(upir_ctx c, const upir_spmd_desc *d, upir_spmd *out) {
+  if (!c || !out) return fail(UPIR_E_INVALID, "NULL argument");
+  upir_status st = validate_spmd(d);
+  if (st != UPIR_OK) return st;
+  upir_spmd s = new upir_spmd_s();
+  s->ctx = c;
+  s->d = *d;
+  c->regions.push_back(s);
+  *out = s;
+  return UPIR_OK;
+}
+
+extern "C" upir_status upir_spmd_end(upir_spmd s) {
+  if (!s) return fail(UPIR_E_INVALID, "NULL region");
+  upir_ctx c = s->ctx;
+  auto it = std::find(c->regions.begin(), c->regions.end(), s);
+  if (it == c->regions.end()) return fail(UPIR_E_INVALID, "region not open");
+  c->regions.erase(it);
+  delete s;
+  return UPIR_OK;
+}
+
+// ------------------------------------------------------------------ loop normalisation
+static int64_t trip(int64_t lb, int64_t ub, int64_t step) {
+  if (step > 0) return ub <= lb ? 0 : (ub - lb + step - 1) / step;
+  return lb <= ub ? 0 : (lb - ub + (-step) - 1) / (-step);
+}
+
+extern "C" upir_status upir_loop_normalize(const upir_loop_desc *l, int64_t *T_total, int64_t T_d[3]) {
+  if (!l || !T_total) return fail(UPIR_E_INVALID, "NULL argument");
+  if (l->collapse < 1 || l->collapse > 2) return fail(UPIR_E_INVALID, "collapse=%d outside [1,2]", l->collapse);
+  int64_t T = 1, Td[3] = {1, 1, 1};
+  for (int d = 0; d < l->collapse; ++d) {
+    if (l->step[d] == 0) return fail(UPIR_E_INVALID, "step[%d] == 0", d);
+    Td[d] = trip(l->lb[d], l->ub[d], l->step[d]);
+    if (Td[d] > 0 && T > INT64_MAX / Td[d]) return fail(UPIR_E_INVALID, "iteration space overflows int64");
+    T *= Td[d];
+  }
+  *T_total = T;
+  if (T_d) for (int d = 0; d < 3; ++d) T_d[d] = Td[d];
+  return UPIR_OK;
+}
+
+// Resolve (policy, chunk) -> (SchedKind, chunk) (readings c3, c8).
+static upir_status resolve_sched(int policy, int64_t chunk, int &sk, int64_t &c) {
+  if (chunk < 0) return fail(UPIR_E_INVALID, "chunk < 0");
+  switch (policy) {
+    case UPIR_SCHED_RUNTIME:
+    case UPIR_SCHED_AUTO:
+      sk = SK_STATIC_BLOCK;
+      c = 0;
+      return UPIR_OK;
+    case UPIR_SCHED_STATIC:
+      sk = chunk > 0 ? SK_STATIC_CHUNK : SK_STATIC_BLOCK;
+      c = chunk;
+      return UPIR_OK;
+    case UPIR_SCHED_DYNAMIC:
+      sk = SK_DYNAMIC;
+      c = chunk > 0 ? chunk : 1;
+      return UPIR_OK;
+    case UPIR_SCHED_GUIDED:
+      return fail(UPIR_E_UNSUPPORTED, "schedule(guided) is not implemented in this build");
+  }
+  return fail(UPIR_E_INVALID, "unknown schedule policy %d", policy);
+}
+
+extern "C" upir_status upir_schedule_chunks(int32_t policy, int64_t chunk, int64_t T, int64_t p, int64_t u,
+                                            int64_t *lo, int64_t *hi, int64_t cap, int64_t *count) {
+  if (!count || p < 1 || u < 0 || u >= p || T < 0 || cap < 0 || (cap > 0 && (!lo || !hi)))
+    return fail(UPIR_E_INVALID, "bad argument");
+  int sk;
+  int64_t c;
+  upir_status st = resolve_sched(policy, chunk, sk, c);
+  if (st != UPIR_OK) return st;
+  if (sk == SK_DYNAMIC) return fail(UPIR_E_INVALID, "dynamic assignment is decided at run time");
+  int64_t n = 0;
+  if (sk == SK_STATIC_BLOCK) {
+    const int64_t q = T / p, r = T % p;
+    const int64_t len = q + (u < r ? 1 : 0);
+    if (len > 0) {
+      if (cap > 0) { lo[0] = u * q + std::min(u, r); hi[0] = lo[0] + len; }
+      n = 1;
+    }
+  } else {
+    const int64_t nc = (T + c - 1) / c;
+    for (int64_t k = u; k < nc; k += p, ++n)
+      if (n < cap) { lo[n] = k * c; hi[n] = std::min((k + 1) * c, T); }
+  }
+  *count = n;
+  return UPIR_OK;
+}
+
+static int body_dtype_ok(int kind, int dtype) {
+  switch (kind) {
+    case UPIR_BODY_AXPY: return dtype == UPIR_F32;
+    case UPIR_BODY_REDUCE: return dtype == UPIR_I64 || dtype == UPIR_F32;
+    case UPIR_BODY_JACOBI5: return dtype == UPIR_F32;
+    case UPIR_BODY_MATMUL: return dtype == UPIR_BF16 || dtype == UPIR_F32;
+  }
+  return 0;
+}
+
+static upir_status validate_loop(const upir_spmd_desc *sd, const upir_loop_desc *l, int kind, int dtype,
+                                 const upir_reduction *reds, int n_reds) {
+  upir_status st = validate_spmd(sd);
+  if (st != UPIR_OK) return st;
+  if (!l) return fail(UPIR_E_INVALID, "loop descriptor is NULL");
+  int64_t T;
+  st = upir_loop_normalize(l, &T, nullptr);
+  if (st != UPIR_OK) return st;
+  int sk;
+  int64_t c;
+  st = resolve_sched(l->policy, l->chunk, sk, c);
+  if (st != UPIR_OK) return st;
+  if (l->distribute != UPIR_DIST_TEAMS && l->distribute != UPIR_DIST_UNITS && l->distribute != UPIR_DIST_TEAMS_UNITS)
+    return fail(UPIR_E_INVALID, "distribute must be TEAMS, UNITS or TEAMS_UNITS");
+  const bool tiled = l->collapse == 2 && (l->tile[0] > 0 || l->tile[1] > 0);
+  if (l->distribute == UPIR_DIST_UNITS && sd->num_teams > 1 && !tiled)
+    return fail(UPIR_E_INVALID, "distribute(units) with num_teams > 1 would replicate the loop per team (reading c7)");
+  if (kind < UPIR_BODY_AXPY || kind > UPIR_BODY_MATMUL) return fail(UPIR_E_INVALID, "unknown body kind %d", kind);
+  if (dtype >= 0 && !body_dtype_ok(kind, dtype)) return fail(UPIR_E_INVALID, "dtype %d not valid for body %d", dtype, kind);
+  if (n_reds < 0 || n_reds > 2) return fail(UPIR_E_INVALID, "n_reds=%d outside [0,2]", n_reds);
+  if (n_reds > 0 && !reds) return fail(UPIR_E_INVALID, "reds is NULL");
+  if (kind == UPIR_BODY_REDUCE && n_reds == 0) return fail(UPIR_E_INVALID, "REDUCE body needs a reduction");
+  if ((kind == UPIR_BODY_JACOBI5 || kind == UPIR_BODY_MATMUL) && n_reds > 0)
+    return fail(UPIR_E_INVALID, "reductions are not defined for this body");
+  for (int r = 0; r < n_reds; ++r) {
+    if (reds[r].op < UPIR_OP_SUM || reds[r].op > UPIR_OP_MIN) return fail(UPIR_E_INVALID, "bad reduction op");
+    if (reds[r].dtype != UPIR_I64 && reds[r].dtype != UPIR_F32) return fail(UPIR_E_INVALID, "reduction dtype must be I64 or F32");
+    if (dtype >= 0 && reds[r].dtype != (kind == UPIR_BODY_AXPY ? UPIR_F32 : dtype))
+      return fail(UPIR_E_INVALID, "reduction dtype does not match the body's element type");
+  }
+  if (kind == UPIR_BODY_AXPY || kind == UPIR_BODY_REDUCE) {
+    if (l->collapse != 1) return fail(UPIR_E_INVALID, "AXPY/REDUCE loops have collapse 1");
+  } else {
+    if (l->collapse != 2) return fail(UPIR_E_INVALID, "JACOBI5/MATMUL loops are collapse(2) nests");
+    for (int d = 0; d < 2; ++d)
+      if (l->step[d] != 1) return fail(UPIR_E_INVALID, "JACOBI5/MATMUL levels need step 1");
+  }
+  if (kind == UPIR_BODY_JACOBI5) {
+    if (l->tile[0] <= 0 || l->tile[1] <= 0) return fail(UPIR_E_INVALID, "JACOBI5 needs tile[0], tile[1] > 0");
+    if (l->distribute != UPIR_DIST_TEAMS) return fail(UPIR_E_INVALID, "the tile loop of a tiled nest is distributed over teams");
+    if (l->inner_policy != UPIR_SCHED_STATIC || l->inner_chunk < 1)
+      return fail(UPIR_E_UNSUPPORTED, "intra-tile loop supports schedule(static, c>=1) over units");
+  }
+  return UPIR_OK;
+}
+
+extern "C" upir_status upir_loop_validate(const upir_spmd_desc *sd, const upir_loop_desc *l, int32_t body_kind,
+                                         const upir_reduction *reds, int32_t n_reds) {
+  return validate_loop(sd, l, body_kind, -1, reds, n_reds);
+}
+
+// ------------------------------------------------------------------ stream loops
+static upir_status check_map(upir_ctx c, upir_map m, const char *what) {
+  if (!m) return fail(UPIR_E_NOT_MAPPED, "%s is not mapped (NULL)", what);
+  if (m->ctx != c) return fail(UPIR_E_NOT_MAPPED, "%s belongs to another context", what);
+  if (m->owned) {
+    auto it = c->present.find(m->host);
+    if (it == c->present.end() || it->second != m) return fail(UPIR_E_NOT_MAPPED, "%s is not in the present table", what);
+  } else if (std::find(c->adopted.begin(), c->adopted.end(), m) == c->adopted.end()) {
+    return fail(UPIR_E_NOT_MAPPED, "%s is not live", what);
+  }
+  return UPIR_OK;
+}
+
+// element view of a map for a body with element size esz
+struct ElemView {
+  char *base_shifted;   // element i at base_shifted + i*esz
+  int64_t lo, hi;       // valid global element indices
+  bool aligned16;
+};
+
+static upir_status elem_view(upir_map m, int64_t esz, ElemView &v) {
+  int64_t off, n;
+  if (m->dist.pattern == UPIR_PATTERN_BLOCK) {
+    if (m->elem_bytes != esz) return fail(UPIR_E_INVALID, "map element size %lld != body element size %lld",
+                                          (long long)m->elem_bytes, (long long)esz);
+    off = m->elem_offset;
+    n = m->elems_local;
+  } else {
+    off = 0;
+    n = (int64_t)(m->dev_bytes / esz);
+  }
+  v.base_shifted = (char *)m->dev - off * esz;
+  v.lo = off;
+  v.hi = off + n;
+  v.aligned16 = ((uintptr_t)v.base_shifted % 16) == 0;
+  return UPIR_OK;
+}
+
+static const char *env_path() {
+  const char *p = getenv("UPIR_PATH");
+  return p ? p : "";
+}
+
+static upir_status exec_stream(upir_spmd s, const upir_loop_desc *l, const upir_body *b, const upir_reduction *reds,
+                               int n_reds, upir_map trace) {
+  upir_ctx c = s->ctx;
+  const upir_spmd_desc &sd = s->d;
+  int64_t T;
+  upir_loop_normalize(l, &T, nullptr);
+  int sk;
+  int64_t chunk;
+  resolve_sched(l->policy, l->chunk, sk, chunk);
+  int64_t lb = l->lb[0], step = l->step[0];
+  // cluster target: block-distribute the normalised space over ranks (c20)
+  if (sd.target == UPIR_TARGET_CLUSTER && c->nranks > 1) {
+    int64_t klo, khi;
+    upir_dist_owned_rows(T, c->rank, c->nranks, &klo, &khi);
+    lb = lb + klo * step;
+    T = khi - klo;
+  }
+  const int body = b->kind == UPIR_BODY_AXPY ? SB_AXPY : (b->dtype == UPIR_I64 ? SB_RED_I64 : SB_RED_F32);
+  const int64_t esz = b->dtype == UPIR_I64 ? 8 : 4;
+  const int VEC = (int)(16 / esz);
+  upir_status st = check_map(c, b->in0, "in0");
+  if (st != UPIR_OK) return st;
+  ElemView vx, vy{};
+  if ((st = elem_view(b->in0, esz, vx)) != UPIR_OK) return st;
+  if (body == SB_AXPY) {
+    if ((st = check_map(c, b->out, "out")) != UPIR_OK) return st;
+    if ((st = elem_view(b->out, esz, vy)) != UPIR_OK) return st;
+  }
+  // every touched element must lie inside the mapped (local) buffers
+  if (T > 0) {
+    const int64_t i0 = lb, i1 = lb + (T - 1) * step;
+    const int64_t imin = std::min(i0, i1), imax = std::max(i0, i1);
+    if (imin < vx.lo || imax >= vx.hi) return fail(UPIR_E_INVALID, "iterations [%lld,%lld] outside in0's elements [%lld,%lld)",
+                                                  (long long)imin, (long long)imax, (long long)vx.lo, (long long)vx.hi);
+    if (body == SB_AXPY && (imin < vy.lo || imax >= vy.hi))
+      return fail(UPIR_E_INVALID, "iterations outside out's elements");
+  }
+  if (trace) {
+    if ((st = check_map(c, trace, "trace")) != UPIR_OK) return st;
+    if ((int64_t)trace->dev_bytes < 3 * T * 4) return fail(UPIR_E_INVALID, "trace map needs 3*T int32");
+  }
+  StreamArgs a;
+  memset(&a, 0, sizeof a);
+  a.T = T;
+  a.lb = lb;
+  a.step = step;
+  a.sched = sk;
+  a.distribute = l->distribute;
+  a.chunk = sk == SK_STATIC_BLOCK ? 1 : chunk;
+  a.in0 = vx.base_shifted;
+  a.out = body == SB_AXPY ? vy.base_shifted : nullptr;
+  a.alpha = (float)b->alpha;
+  a.safe_hi = body == SB_AXPY ? std::min(vx.hi, vy.hi) : vx.hi;
+  a.safe_lo = body == SB_AXPY ? std::max(vx.lo, vy.lo) : vx.lo;
+  a.nred = n_reds;
+  for (int r = 0; r < n_reds; ++r) {
+    a.red[r].op = reds[r].op;
+    a.red[r].dtype = reds[r].dtype;
+    a.red[r].result = reds[r].dev_result;
+    if (!reds[r].dev_result) return fail(UPIR_E_INVALID, "reduction %d has no dev_result", r);
+    if (reds[r].dtype == UPIR_I64) {
+      int64_t v = reds[r].op == UPIR_OP_SUM ? 0 : (reds[r].op == UPIR_OP_MAX ? INT64_MIN : INT64_MAX);
+      if (reds[r].init) memcpy(&v, reds[r].init, 8);
+      a.red[r].init_bits = (uint64_t)v;
+    } else {
+      double v = reds[r].op == UPIR_OP_SUM ? 0.0 : (reds[r].op == UPIR_OP_MAX ? -HUGE_VAL : HUGE_VAL);
+      if (reds[r].init) { float f; memcpy(&f, reds[r].init, 4); v = f; }
+      memcpy(&a.red[r].init_bits, &v, 8);
+    }
+  }
+  a.trace = trace ? (int32_t *)trace->dev : nullptr;
+  // dynamic tickets: m chunks per unit so a ticket covers >= ~256 KiB
+  const int p_team = l->distribute == UPIR_DIST_TEAMS ? 1 : sd.num_units;
+  if (sk == SK_DYNAMIC) {
+    const int64_t want = (256 * 1024) / esz;
+    a.ticket_m = std::max<int64_t>(1, (want + (int64_t)p_team * chunk - 1) / ((int64_t)p_team * chunk));
+    a.dyn_counter = c->dyn;
+  }
+  a.slots = c->slots;
+  a.done = c->done;
+  st = ensure_slots(c, (size_t)sd.num_teams);
+  if (st != UPIR_OK) return st;
+  a.slots = c->slots;
+  // memory path: per-unit chunk longer than one vector -> staged
+  const int64_t p = l->distribute == UPIR_DIST_TEAMS ? sd.num_teams
+                   : l->distribute == UPIR_DIST_UNITS ? sd.num_units
+                   : (int64_t)sd.num_teams * sd.num_units;
+  int64_t unit_chunk = sk == SK_STATIC_BLOCK ? (T + p - 1) / p : chunk;
+  bool staged = unit_chunk > VEC && (step == 1 || step == -1) && vx.aligned16 && (body != SB_AXPY || vy.aligned16);
+  const char *ep = env_path();
+  if (!strcmp(ep, "direct")) staged = false;
+  if (!strcmp(ep, "staged") && (step == 1 || step == -1) && vx.aligned16 && (body != SB_AXPY || vy.aligned16)) staged = true;
+  int segv = 0, nst = 0;
+  size_t smem = 0;
+  if (staged) {
+    // pick (SEGV, NST) maximising bytes in flight per SM under the smem budget
+    const int cfg[5][2] = {{8, 4}, {8, 3}, {8, 2}, {4, 3}, {4, 2}};
+    double best = -1;
+    const int warps = (sd.num_units + 31) / 32;
+    for (auto &cf : cfg) {
+      size_t sm = staged_smem_bytes(body, sd.num_units, cf[0], cf[1]);
+      if (sm > 227 * 1024) continue;
+      int ctas = std::min<int>(std::min<int>((int)((227 * 1024) / std::max<size_t>(sm, 1)), 2048 / (warps * 32)), 32);
+      ctas = std::min<int64_t>(ctas, (sd.num_teams + c->num_sms - 1) / c->num_sms);
+      if (ctas < 1) ctas = 1;
+      double inflight = std::min(128.0 * 1024, (double)ctas * warps * (cf[1] - 1) * cf[0] * 16 * 32);
+      if (inflight > best + 1e-9) { best = inflight; segv = cf[0]; nst = cf[1]; smem = sm; }
+    }
+    if (best < 0) staged = false;
+  }
+  if (!staged) { segv = 0; nst = 0; smem = 0; }
+  cudaError_t e = launch_stream_loop(body, staged ? PATH_STAGED : PATH_DIRECT, segv, nst, trace != nullptr,
+                                     sd.num_teams, sd.num_units, smem, a, c->compute);
+  if (e != cudaSuccess) return fail(UPIR_E_CUDA, "loop kernel launch failed: %s", cudaGetErrorString(e));
+  c->launches++;
+  return UPIR_OK;
+}
+
+static upir_status exec_jacobi(upir_spmd s, const upir_loop_desc *l, const upir_body *b, upir_map trace);
+static upir_status exec_matmul(upir_spmd s, const upir_loop_desc *l, const upir_body *b, upir_map trace);
+
+extern "C" upir_status upir_loop_exec(upir_spmd s, const upir_loop_desc *l, const upir_body *b,
+                                      const upir_reduction *reds, int32_t n_reds, upir_map trace) {
+  if (!s || !b) return fail(UPIR_E_INVALID, "NULL argument");
+  upir_ctx c = s->ctx;
+  if (std::find(c->regions.begin(), c->regions.end(), s) == c->regions.end())
+    return fail(UPIR_E_INVALID, "region is not open");
+  upir_status st = validate_loop(&s->d, l, b->kind, b->dtype, reds, n_reds);
+  if (st != UPIR_OK) return st;
+  if (c->sticky != cudaSuccess) return sticky_check(c);
+  cudaSetDevice(c->device);
+  switch (b->kind) {
+    case UPIR_BODY_AXPY:
+    case UPIR_BODY_REDUCE: st = exec_stream(s, l, b, reds, n_reds, trace); break;
+    case UPIR_BODY_JACOBI5: st = exec_jacobi(s, l, b, trace); break;
+    case UPIR_BODY_MATMUL: st = exec_matmul(s, l, b, trace); break;
+  }
+  if (st != UPIR_OK) return st;
+  // implicit barrier at the end of a worksharing loop: stream
+  // order makes every later operation wait; the host waits only at upir_sync.
+  return UPIR_OK;
+}
+
+// ------------------------------------------------------------------ jacobi / matmul
+static upir_status exec_jacobi(upir_spmd, const upir_loop_desc *, const upir_body *, upir_map) {
+  return fail(UPIR_E_UNSUPPORTED, "JACOBI5 body not built yet");
+}
+static upir_status exec_matmul(upir_spmd, const upir_loop_desc *, const upir_body *, upir_map) {
+  return fail(UPIR_E_UNSUPPORTED, "MATMUL body not built yet");
+}
+
+// ------------------------------------------------------------------ upir.sync
+extern "C" upir_status upir_reduce(upir_ctx c, int32_t op, int32_t dtype, const void *dev_in, int64_t count,
+                                   void *dev_out, int32_t scope) {
+  if (!c || !dev_in || !dev_out || count < 1) return fail(UPIR_E_INVALID, "bad argument");
+  if (op < UPIR_OP_SUM || op > UPIR_OP_MIN) return fail(UPIR_E_INVALID, "bad op");
+  if (dtype != UPIR_I64 && dtype != UPIR_F32) return fail(UPIR_E_INVALID, "dtype must be I64 or F32");
+  cudaSetDevice(c->device);
+  const size_t esz = dtype == UPIR_I64 ? 8 : 4;
+  if (scope == UPIR_SCOPE_DEVICE) {
+    StreamArgs a;
+    memset(&a, 0, sizeof a);
+    const int VEC = (int)(16 / esz);
+    a.T = count;
+    a.lb = 0;
+    a.step = 1;
+    a.sched = SK_STATIC_CHUNK;
+    a.chunk = ((uintptr_t)dev_in % 16 == 0) ? VEC : 1;
+    a.distribute = UPIR_DIST_TEAMS_UNITS;
+    a.in0 = dev_in;
+    a.safe_lo = 0;
+    a.safe_hi = count;
+    a.nred = 1;
+    a.red[0].op = op;
+    a.red[0].dtype = dtype;
+    a.red[0].result = dev_out;
+    if (dtype == UPIR_I64) {
+      int64_t v = op == UPIR_OP_SUM ? 0 : (op == UPIR_OP_MAX ? INT64_MIN : INT64_MAX);
+      a.red[0].init_bits = (uint64_t)v;
+    } else {
+      double v = op == UPIR_OP_SUM ? 0.0 : (op == UPIR_OP_MAX ? -HUGE_VAL : HUGE_VAL);
+      memcpy(&a.red[0].init_bits, &v, 8);
+    }
+    int teams = (int)std::min<int64_t>((int64_t)c->num_sms * 4, std::max<int64_t>(1, (count + 1023) / 1024));
+    upir_status st = ensure_slots(c, (size_t)teams);
+    if (st != UPIR_OK) return st;
+    a.slots = c->slots;
+    a.done = c->done;
+    cudaError_t e = launch_stream_loop(dtype == UPIR_I64 ? SB_RED_I64 : SB_RED_F32, PATH_DIRECT, 0, 0, false, teams,
+                                       256, 0, a, c->compute);
+    if (e != cudaSuccess) return fail(UPIR_E_CUDA, "reduce launch failed: %s", cudaGetErrorString(e));
+    c->launches++;
+    return UPIR_OK;
+  }
+  if (scope != UPIR_SCOPE_WORLD) return fail(UPIR_E_INVALID, "bad scope");
+  // allreduce over ranks (Fig. 7): all-gather of the partials, then the
+  // combine in ascending rank order on every rank (deterministic, c10).
+  const size_t need = esz * (size_t)count * (size_t)c->nranks;
+  if (need > c->scratch_bytes) {
+    if (c->capturing) return fail(UPIR_E_INVALID, "scratch must grow during capture");
+    CUDA_TRY(cudaStreamSynchronize(c->compute));
+    if (c->scratch) CUDA_TRY(cudaFree(c->scratch));
+    CUDA_TRY(cudaMalloc(&c->scratch, need));
+    c->scratch_bytes = need;
+  }
+  if (c->nranks > 1) {
+    NCCL_TRY(ncclAllGather(dev_in, c->scratch, (size_t)count, dtype == UPIR_I64 ? ncclInt64 : ncclFloat32, c->comm,
+                           c->compute));
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(c->scratch, dev_in, esz * count, cudaMemcpyDeviceToDevice, c->compute));
+  }
+  cudaError_t e = launch_rank_combine(op, dtype, c->scratch, count, c->nranks, dev_out, c->compute);
+  if (e != cudaSuccess) return fail(UPIR_E_CUDA, "combine launch failed: %s", cudaGetErrorString(e));
+  c->launches++;
+  return UPIR_OK;
+}
+
+static upir_status halo_exchange(upir_ctx c, upir_map m) {
+  if (m->dist.pattern != UPIR_PATTERN_BLOCK || m->dist.halo_rows < 1)
+    return fail(UPIR_E_INVALID, "HALO needs a BLOCK-distributed map with halo_rows >= 1");
+  if (c->nranks == 1) return UPIR_OK;
+  const int64_t rb = m->dist.row_elems * m->dist.elem_bytes;
+  const int64_t h = m->dist.halo_rows;
+  char *base = (char *)m->dev;
+  const int up = c->rank - 1, dn = c->rank + 1;
+  // Fig. 7 send/recv with rank units: my first owned rows -> up's bottom halo,
+  // my last owned rows -> dn's top halo; receive the mirror images.
+  NCCL_TRY(ncclGroupStart());
+  if (up >= 0) {
+    const int64_t nh = std::min(h, m->row_lo - m->loc_row_lo);
+    NCCL_TRY(ncclSend(base + (m->row_lo - m->loc_row_lo) * rb, (size_t)(nh * rb), ncclChar, up, c->comm, c->compute));
+    NCCL_TRY(ncclRecv(base + (m->row_lo - nh - m->loc_row_lo) * rb, (size_t)(nh * rb), ncclChar, up, c->comm, c->compute));
+  }
+  if (dn < c->nranks) {
+    const int64_t nh = std::min(h, m->loc_row_hi - m->row_hi);
+    NCCL_TRY(ncclSend(base + (m->row_hi - nh - m->loc_row_lo) * rb, (size_t)(nh * rb), ncclChar, dn, c->comm, c->compute));
+    NCCL_TRY(ncclRecv(base + (m->row_hi - m->loc_row_lo) * rb, (size_t)(nh * rb), ncclChar, dn, c->comm, c->compute));
+  }
+  NCCL_TRY(ncclGroupEnd());
+  return UPIR_OK;
+}
+
+extern "C" upir_status upir_sync(upir_ctx c, int32_t kind, upir_map halo_map, upir_event *token) {
+  if (!c) return fail(UPIR_E_INVALID, "ctx is NULL");
+  cudaSetDevice(c->device);
+  switch (kind) {
+    case UPIR_SYNC_BARRIER: {
+      cudaError_t e1 = cudaStreamSynchronize(c->compute);
+      cudaError_t e2 = cudaStreamSynchronize(c->copy);
+      if (e1 != cudaSuccess && c->sticky == cudaSuccess) c->sticky = e1;
+      if (e2 != cudaSuccess && c->sticky == cudaSuccess) c->sticky = e2;
+      if (c->comm) {
+        ncclResult_t ar;
+        if (ncclCommGetAsyncError(c->comm, &ar) == ncclSuccess && ar != ncclSuccess)
+          return fail(UPIR_E_NCCL, "NCCL asynchronous error: %s", ncclGetErrorString(ar));
+      }
+      return sticky_check(c);
+    }
+    case UPIR_SYNC_WORLD_BARRIER: {
+      upir_status st = upir_sync(c, UPIR_SYNC_BARRIER, nullptr, nullptr);
+      if (st != UPIR_OK) return st;
+      if (c->nranks > 1) {
+        NCCL_TRY(ncclAllReduce(c->one, c->one, 1, ncclInt32, ncclSum, c->comm, c->compute));
+        CUDA_TRY(cudaStreamSynchronize(c->compute));
+      }
+      return UPIR_OK;
+    }
+    case UPIR_SYNC_ARRIVE: {
+      if (!token) return fail(UPIR_E_INVALID, "ARRIVE needs a token out-param");
+      upir_event ev = new upir_event_s();
+      if (cudaEventCreateWithFlags(&ev->ev, cudaEventDisableTiming) != cudaSuccess) {
+        delete ev;
+        return fail(UPIR_E_CUDA, "event create failed");
+      }
+      upir_status st = copy_to_compute(c);
+      if (st != UPIR_OK) { cudaEventDestroy(ev->ev); delete ev; return st; }
+      CUDA_TRY(cudaEventRecord(ev->ev, c->compute));
+      *token = ev;
+      return UPIR_OK;
+    }
+    case UPIR_SYNC_WAIT: {
+      if (!token || !*token) return fail(UPIR_E_SYNC, "WAIT without a matching ARRIVE token");
+      upir_event ev = *token;
+      cudaError_t e = cudaEventSynchronize(ev->ev);
+      cudaEventDestroy(ev->ev);
+      delete ev;
+      *token = nullptr;
+      if (e != cudaSuccess) return fail(UPIR_E_CUDA, "wait failed: %s", cudaGetErrorString(e));
+      return sticky_check(c);
+    }
+    case UPIR_SYNC_HALO: {
+      if (!halo_map) return fail(UPIR_E_INVALID, "HALO needs a map");
+      upir_status st = check_map(c, halo_map, "halo map");
+      if (st != UPIR_OK) return st;
+      return halo_exchange(c, halo_map);
+    }
+  }
+  return fail(UPIR_E_INVALID, "unknown sync kind %d", kind);
+}
+
+// ------------------------------------------------------------------ graphs
+extern "C" upir_status upir_graph_begin(upir_ctx c) {
+  if (!c) return fail(UPIR_E_INVALID, "ctx is NULL");
+  if (c->capturing) return fail(UPIR_E_INVALID, "already capturing");
+  cudaSetDevice(c->device);
+  CUDA_TRY(cudaStreamBeginCapture(c->compute, cudaStreamCaptureModeRelaxed));
+  c->capturing = true;
+  return UPIR_OK;
+}
+
+extern "C" upir_status upir_graph_end(upir_ctx c, upir_graph *out) {
+  if (!c || !out) return fail(UPIR_E_INVALID, "bad argument");
+  if (!c->capturing) return fail(UPIR_E_INVALID, "not capturing");
+  c->capturing = false;
+  upir_graph g = new upir_graph_s();
+  cudaError_t e = cudaStreamEndCapture(c->compute, &g->graph);
+  if (e != cudaSuccess) { delete g; return fail(UPIR_E_CUDA, "end capture: %s", cudaGetErrorString(e)); }
+  e = cudaGraphInstantiate(&g->exec, g->graph, 0);
+  if (e != cudaSuccess) {
+    cudaGraphDestroy(g->graph);
+    delete g;
+    return fail(UPIR_E_CUDA, "instantiate: %s", cudaGetErrorString(e));
+  }
+  *out = g;
+  return UPIR_OK;
+}
+
+extern "C" upir_status upir_graph_launch(upir_ctx c, upir_graph g) {
+  if (!c || !g) return fail(UPIR_E_INVALID, "bad argument");
+  cudaSetDevice(c->device);
+  CUDA_TRY(cudaGraphLaunch(g->exec, c->compute));
+  c->launches++;
+  return UPIR_OK;
+}
+
+extern "C" upir_status upir_graph_destroy(upir_graph g) {
+  if (!g) return fail(UPIR_E_INVALID, "graph is NULL");
+  cudaGraphExecDestroy(g->exec);
+  cudaGraphDestroy(g->graph);
+  delete g;
+  return UPIR_OK;
+}
+
+// ------------------------------------------------------------------ synthetic inputs
+extern "C" upir_status upir_synth_fill(upir_ctx c, upir_map m, int32_t dist, uint64_t stream, int64_t index_base,
+                                       int64_t n_rows, int64_t n_cols) {
+  if (!c || !m) return fail(UPIR_E_INVALID, "bad argument");
+  upir_status st = check_map(c, m, "map");
+  if (st != UPIR_OK) return st;
+  if (dist < 0 || dist > 4) return fail(UPIR_E_INVALID, "bad dist");
+  const int64_t esz = dist == 2 ? 8 : (dist == 3 ? 2 : 4);
+  if (dist == 4 && (n_rows < 1 || n_cols < 1)) return fail(UPIR_E_INVALID, "Jacobi fill needs n_rows, n_cols");
+  int64_t n, off;
+  if (m->dist.pattern == UPIR_PATTERN_BLOCK) {
+    if (m->elem_bytes != esz) return fail(UPIR_E_INVALID, "element size mismatch");
+    n = m->elems_local;
+    off = m->elem_offset;
+  } else {
+    n = (int64_t)(m->dev_bytes / esz);
+    off = 0;
+  }
+  cudaSetDevice(c->device);
+  cudaError_t e = launch_synth_fill(dist, stream, m->dev, n, off + index_base, n_rows, n_cols, c->compute);
+  if (e != cudaSuccess) return fail(UPIR_E_CUDA, "fill launch failed: %s", cudaGetErrorString(e));
+  c->launches++;
+  return UPIR_OK;
+}

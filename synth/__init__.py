@@ -16,5 +16,5 @@ bit for bit.  See DESIGN.md "Input recipe".
 """
 from .splitmix import (  # noqa: F401
     STREAMS, raw, f32_unit, f32_sym, i64_sym, bf16_sym_as_f32, jacobi_init,
-    jacobi_init_rows, GOLDEN,
+    jacobi_init_rows, GOLDEN, c_f32_unit, c_i64_sym, c_raw, build_c,
 )

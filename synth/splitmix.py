@@ -82,3 +82,47 @@ def jacobi_init_rows(ny, nx, r0, r1, stream=STREAMS["jacobi"]):
 
 def jacobi_init(ny, nx, stream=STREAMS["jacobi"]):
     return jacobi_init_rows(ny, nx, 0, ny, stream)
+
+
+# ---- C twin for large inputs (same recipe; tests pin it against the above) ----
+import ctypes as _ct
+import os as _os
+import subprocess as _sp
+
+_CSRC = _os.path.join(_os.path.dirname(_os.path.abspath(__file__)), "splitmix.c")
+_CLIB = _os.path.join(_os.path.dirname(_os.path.abspath(__file__)), "libsynth.so")
+_clib = None
+
+
+def build_c(force=False):
+    if force or not _os.path.exists(_CLIB) or _os.path.getmtime(_CLIB) < _os.path.getmtime(_CSRC):
+        _sp.check_call(["gcc", "-O2", "-std=c11", "-fPIC", "-shared", "-o", _CLIB, _CSRC])
+    return _CLIB
+
+
+def _c():
+    global _clib
+    if _clib is None:
+        _clib = _ct.CDLL(build_c())
+        for n in ("synth_raw", "synth_f32_unit", "synth_i64_sym"):
+            getattr(_clib, n).argtypes = [_ct.c_uint64, _ct.c_int64, _ct.c_int64, _ct.c_void_p]
+            getattr(_clib, n).restype = None
+    return _clib
+
+
+def c_f32_unit(stream, start, n):
+    out = np.empty(n, dtype=np.float32)
+    _c().synth_f32_unit(stream, start, n, out.ctypes.data)
+    return out
+
+
+def c_i64_sym(stream, start, n):
+    out = np.empty(n, dtype=np.int64)
+    _c().synth_i64_sym(stream, start, n, out.ctypes.data)
+    return out
+
+
+def c_raw(stream, start, n):
+    out = np.empty(n, dtype=np.uint64)
+    _c().synth_raw(stream, start, n, out.ctypes.data)
+    return out
