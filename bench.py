@@ -235,8 +235,9 @@ def bench_reduce(args, U, ctx, stream, barrier, rank, world, peaks, peak_src):
     import torch
     n = 1 << args.n_log2
     teams, units = 148 * 4, 256
-    pol, chunk = {"static": (U.SCHED_STATIC, 0), "static1": (U.SCHED_STATIC, 2),
-                  "dynamic": (U.SCHED_DYNAMIC, 2)}[args.sched]
+    # static1 / dynamic: chunk = one 16-B vector per unit (2 int64 / 4 fp32)
+    pol = {"static": U.SCHED_STATIC, "static1": U.SCHED_STATIC, "dynamic": U.SCHED_DYNAMIC}[args.sched]
+    ci, cf = (0, 0) if args.sched == "static" else (2, 4)
     # device-resident inputs: map(alloc) + on-device synthetic fill (rank r
     # holds global elements [r*n, (r+1)*n) of each stream)
     hi = np.empty(1, np.int64)          # host key objects for the alloc maps
@@ -253,7 +254,8 @@ def bench_reduce(args, U, ctx, stream, barrier, rank, world, peaks, peak_src):
     base = res_t.data_ptr()
     reds_i = [U.reduction(U.OP_SUM, U.I64, base + 0), U.reduction(U.OP_MAX, U.I64, base + 8)]
     reds_f = [U.reduction(U.OP_SUM, U.F32, base + 16), U.reduction(U.OP_MAX, U.F32, base + 24)]
-    loop = U.loop_desc(0, n, policy=pol, chunk=chunk)
+    loop_i = U.loop_desc(0, n, policy=pol, chunk=ci)
+    loop_f = U.loop_desc(0, n, policy=pol, chunk=cf)
     spmd = U.upir_spmd_launch(ctx, U.spmd_desc(teams, units))
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
 
@@ -261,10 +263,10 @@ def bench_reduce(args, U, ctx, stream, barrier, rank, world, peaks, peak_src):
         e = timed_events
         if e:
             e[0].record(stream)
-        U.upir_loop_exec(spmd, loop, U.body(U.BODY_REDUCE, U.I64, in0=mi), reds_i)
+        U.upir_loop_exec(spmd, loop_i, U.body(U.BODY_REDUCE, U.I64, in0=mi), reds_i)
         if e:
             e[1].record(stream)
-        U.upir_loop_exec(spmd, loop, U.body(U.BODY_REDUCE, U.F32, in0=mf), reds_f)
+        U.upir_loop_exec(spmd, loop_f, U.body(U.BODY_REDUCE, U.F32, in0=mf), reds_f)
         if e:
             e[2].record(stream)
         if world > 1:
@@ -298,7 +300,7 @@ def bench_reduce(args, U, ctx, stream, barrier, rank, world, peaks, peak_src):
 
     # ---- e2e: host buffers through the C-ABI ------------------------------------
     import ctypes
-    e2e_n = n
+    e2e_n = n if args.e2e_steps > 0 else 1
     hx_i = torch.empty(e2e_n, dtype=torch.int64, pin_memory=True)
     hx_f = torch.empty(e2e_n, dtype=torch.float32, pin_memory=True)
     hx_i.copy_(xi_t[:e2e_n])
@@ -322,10 +324,9 @@ def bench_reduce(args, U, ctx, stream, barrier, rank, world, peaks, peak_src):
         mr = U.upir_data_map(ctx, hres, U.MAP_FROM)
         rp, _, _ = U.upir_data_device_ptr(mr)
         s = U.upir_spmd_launch(ctx, U.spmd_desc(teams, units))
-        loop_e = U.loop_desc(0, e2e_n, policy=pol, chunk=chunk)
-        U.upir_loop_exec(s, loop_e, U.body(U.BODY_REDUCE, U.I64, in0=m1),
+        U.upir_loop_exec(s, U.loop_desc(0, e2e_n, policy=pol, chunk=ci), U.body(U.BODY_REDUCE, U.I64, in0=m1),
                          [U.reduction(U.OP_SUM, U.I64, rp + 0), U.reduction(U.OP_MAX, U.I64, rp + 8)])
-        U.upir_loop_exec(s, loop_e, U.body(U.BODY_REDUCE, U.F32, in0=m2),
+        U.upir_loop_exec(s, U.loop_desc(0, e2e_n, policy=pol, chunk=cf), U.body(U.BODY_REDUCE, U.F32, in0=m2),
                          [U.reduction(U.OP_SUM, U.F32, rp + 16), U.reduction(U.OP_MAX, U.F32, rp + 24)])
         if world > 1:
             for k, (op, dt) in enumerate(((U.OP_SUM, U.I64), (U.OP_MAX, U.I64), (U.OP_SUM, U.F32),
@@ -337,13 +338,15 @@ def bench_reduce(args, U, ctx, stream, barrier, rank, world, peaks, peak_src):
         U.upir_data_unmap(ctx, m1)
         U.upir_sync(ctx)
 
-    e2e_step()   # warm-up (pins the host ranges once)
-    barrier()
-    te0 = time.perf_counter()
-    for _ in range(args.e2e_steps):
-        e2e_step()
-    barrier()
-    e2e_ms = (time.perf_counter() - te0) * 1e3 / args.e2e_steps
+    e2e_ms = float("nan")
+    if args.e2e_steps > 0:
+        e2e_step()   # warm-up (pins the host ranges once)
+        barrier()
+        te0 = time.perf_counter()
+        for _ in range(args.e2e_steps):
+            e2e_step()
+        barrier()
+        e2e_ms = (time.perf_counter() - te0) * 1e3 / args.e2e_steps
     # the e2e path is timed by the host clock around synchronous steps (each
     # step ends in upir_sync), max over ranks below
 

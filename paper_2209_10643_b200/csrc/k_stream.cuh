@@ -210,6 +210,44 @@ __device__ void direct_run(const StreamArgs &a, const LaneWork &w, Acc<BODY, NRE
     }
     for (; j < nfull; ++j) direct_vec<BODY, NRED, TRACE>(a, e0 + j * w.kstride, acc, team, unit);
   }
+  // long contiguous chunks (static block / large c) with step 1: per-unit
+  // 16-B vectors, 4 in flight (adjacent units are far apart: uncoalesced,
+  // relies on L1 sector reuse -- the STAGED path is the coalesced variant)
+  if (a.step == 1 && w.c > VEC) {
+    const int64_t vec_hi = (a.safe_hi / VEC) * VEC;
+    for (; j < w.nk; ++j) {
+      int64_t klo, khi;
+      chunk_bounds(w, j, a.T, klo, khi);
+      const int64_t elo = a.lb + klo, ehi = a.lb + khi;
+      int64_t e = elo;
+      const int64_t ea = min(ehi, ((elo + VEC - 1) / VEC) * VEC);
+      for (; e < ea; ++e) body_scalar<BODY, NRED, TRACE>(a, e, acc, team, unit);
+      const int64_t eb = max(e, min(ehi, vec_hi) / VEC * VEC);
+      for (; e + 4 * VEC <= eb; e += 4 * VEC) {
+        if constexpr (BODY == SB_RED_I64 && !TRACE) {
+          longlong2 v[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            v[q] = __ldcs(reinterpret_cast<const longlong2 *>(reinterpret_cast<const long long *>(a.in0) + e + q * VEC));
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc_l2(acc, v[q], true, true);
+        } else if constexpr (BODY == SB_RED_F32 && !TRACE) {
+          float4 v[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            v[q] = __ldcs(reinterpret_cast<const float4 *>(reinterpret_cast<const float *>(a.in0) + e + q * VEC));
+#pragma unroll
+          for (int q = 0; q < 4; ++q) acc_f4(acc, v[q], true, true, true, true);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) direct_vec<BODY, NRED, TRACE>(a, e + q * VEC, acc, team, unit);
+        }
+      }
+      for (; e + VEC <= eb; e += VEC) direct_vec<BODY, NRED, TRACE>(a, e, acc, team, unit);
+      for (; e < ehi; ++e) body_scalar<BODY, NRED, TRACE>(a, e, acc, team, unit);
+    }
+    return;
+  }
   // generic remainder: element by element
   for (; j < w.nk; ++j) {
     int64_t klo, khi;
@@ -224,7 +262,7 @@ struct StagedLayout {
   static constexpr int ROW = SEGV * 16 + 16;                 // padded row: conflict-free
   static constexpr int NBUF = BODY == SB_AXPY ? 2 : 1;
   static constexpr int STAGE = 32 * ROW * NBUF;
-  static constexpr int META = 32 * 16;                        // longlong2 per lane
+  static constexpr int META = 32 * 32;                        // 2 x longlong2 per lane
   static constexpr int WARP_BYTES = NST * (STAGE + META);
 };
 
@@ -259,95 +297,104 @@ __device__ void staged_run(const StreamArgs &a, const LaneWork &w, Acc<BODY, NRE
     return true;
   };
 
+  // meta[st][lane]  = {elo, ehi}  : the lane's element interval of stage st
+  // meta2[st][lane] = {v0, nv}     : its 16-B vectors [v0, v0 + nv)
+  longlong2 *meta2 = meta + NST * 32;
+  constexpr int LOGV = VEC == 2 ? 1 : 2;
+
   auto issue = [&](int64_t s) -> bool {
     const int st = (int)(s % NST);
-    longlong2 m = make_longlong2(0, 0);
+    longlong2 m = make_longlong2(0, 0), m2 = make_longlong2(0, 0);
     if (next_interval()) {
-      const int64_t v0 = e_cur / VEC;
-      const int64_t vseg_end = (v0 / SEGV + 1) * SEGV;
-      const int64_t seg_hi = min(e_end, vseg_end * VEC);
+      const int64_t v0 = (int64_t)((uint64_t)e_cur >> LOGV);
+      const int64_t vseg_end = (v0 & ~(int64_t)(SEGV - 1)) + SEGV;   // segments end on SEGV boundaries
+      const int64_t seg_hi = min(e_end, vseg_end << LOGV);
+      const int64_t v1 = (int64_t)(((uint64_t)seg_hi + VEC - 1) >> LOGV);
       m = make_longlong2(e_cur, seg_hi);
+      m2 = make_longlong2(v0, v1 - v0);
       e_cur = seg_hi;
     }
     meta[st * 32 + lane] = m;
+    meta2[st * 32 + lane] = m2;
     __syncwarp();
-    if (!__any_sync(FULL, m.y > m.x)) return false;
+    if (!__any_sync(FULL, m2.y > 0)) return false;
     char *sb = rows + st * L::STAGE;
+    const int k = lane % SEGV;
 #pragma unroll
     for (int q = 0; q < SEGV; ++q) {
       const int ju = q * UPI + lane / SEGV;
-      const int k = lane % SEGV;
-      const longlong2 mj = meta[st * 32 + ju];
-      if (mj.y > mj.x) {
-        const int64_t v0 = mj.x / VEC, v1 = (mj.y + VEC - 1) / VEC;
-        if (k < v1 - v0) {
-          cp_async16(sb + ju * L::ROW + k * 16, gx + (v0 + k) * 16);
-          if constexpr (BODY == SB_AXPY) cp_async16(sb + 32 * L::ROW + ju * L::ROW + k * 16, gy + (v0 + k) * 16);
-        }
+      const longlong2 mj = meta2[st * 32 + ju];
+      if (k < mj.y) {
+        cp_async16(sb + ju * L::ROW + k * 16, gx + (mj.x + k) * 16);
+        if constexpr (BODY == SB_AXPY) cp_async16(sb + 32 * L::ROW + ju * L::ROW + k * 16, gy + (mj.x + k) * 16);
       }
     }
     return true;
   };
 
+  auto consume_vec = [&](char *row, int k, int64_t vb, bool full, const longlong2 &m) {
+    if constexpr (BODY == SB_RED_I64) {
+      const longlong2 v = *reinterpret_cast<const longlong2 *>(row + k * 16);
+      if (full) acc_l2(acc, v, true, true);
+      else acc_l2(acc, v, vb >= m.x && vb < m.y, vb + 1 >= m.x && vb + 1 < m.y);
+    } else if constexpr (BODY == SB_RED_F32) {
+      const float4 v = *reinterpret_cast<const float4 *>(row + k * 16);
+      if (full) acc_f4(acc, v, true, true, true, true);
+      else acc_f4(acc, v, vb >= m.x && vb < m.y, vb + 1 >= m.x && vb + 1 < m.y, vb + 2 >= m.x && vb + 2 < m.y,
+                  vb + 3 >= m.x && vb + 3 < m.y);
+    } else {
+      const float4 x = *reinterpret_cast<const float4 *>(row + k * 16);
+      float4 *yr = reinterpret_cast<float4 *>(row + 32 * L::ROW + k * 16);
+      float4 y = *yr;
+      y.x = __fmaf_rn(a.alpha, x.x, y.x);
+      y.y = __fmaf_rn(a.alpha, x.y, y.y);
+      y.z = __fmaf_rn(a.alpha, x.z, y.z);
+      y.w = __fmaf_rn(a.alpha, x.w, y.w);
+      *yr = y;
+      if (full) acc_f4(acc, y, true, true, true, true);
+      else acc_f4(acc, y, vb >= m.x && vb < m.y, vb + 1 >= m.x && vb + 1 < m.y, vb + 2 >= m.x && vb + 2 < m.y,
+                  vb + 3 >= m.x && vb + 3 < m.y);
+    }
+    if constexpr (TRACE) {
+#pragma unroll
+      for (int q = 0; q < VEC; ++q)
+        if (vb + q >= m.x && vb + q < m.y) trace_rec<TRACE>(a, vb + q, team, unit);
+    }
+  };
+
   auto consume = [&](int64_t s) {
     const int st = (int)(s % NST);
     const longlong2 m = meta[st * 32 + lane];
+    const longlong2 m2 = meta2[st * 32 + lane];
     char *row = rows + st * L::STAGE + lane * L::ROW;
-    if (m.y > m.x) {
-      const int64_t v0 = m.x / VEC;
+    if (m2.y == SEGV && m.x == (m2.x << LOGV) && m.y == ((m2.x + SEGV) << LOGV)) {
 #pragma unroll
-      for (int k = 0; k < SEGV; ++k) {
-        const int64_t vb = (v0 + k) * VEC;
-        if (vb < m.y) {
-          if constexpr (BODY == SB_RED_I64) {
-            const longlong2 v = *reinterpret_cast<const longlong2 *>(row + k * 16);
-            acc_l2(acc, v, vb >= m.x && vb < m.y, vb + 1 >= m.x && vb + 1 < m.y);
-          } else if constexpr (BODY == SB_RED_F32) {
-            const float4 v = *reinterpret_cast<const float4 *>(row + k * 16);
-            acc_f4(acc, v, vb >= m.x && vb < m.y, vb + 1 >= m.x && vb + 1 < m.y,
-                   vb + 2 >= m.x && vb + 2 < m.y, vb + 3 >= m.x && vb + 3 < m.y);
-          } else {
-            const float4 x = *reinterpret_cast<const float4 *>(row + k * 16);
-            float4 *yr = reinterpret_cast<float4 *>(row + 32 * L::ROW + k * 16);
-            float4 y = *yr;
-            y.x = __fmaf_rn(a.alpha, x.x, y.x);
-            y.y = __fmaf_rn(a.alpha, x.y, y.y);
-            y.z = __fmaf_rn(a.alpha, x.z, y.z);
-            y.w = __fmaf_rn(a.alpha, x.w, y.w);
-            *yr = y;
-            acc_f4(acc, y, vb >= m.x && vb < m.y, vb + 1 >= m.x && vb + 1 < m.y,
-                   vb + 2 >= m.x && vb + 2 < m.y, vb + 3 >= m.x && vb + 3 < m.y);
-          }
-          if constexpr (TRACE) {
+      for (int k = 0; k < SEGV; ++k) consume_vec(row, k, (m2.x + k) << LOGV, true, m);
+    } else {
 #pragma unroll
-            for (int q = 0; q < VEC; ++q)
-              if (vb + q >= m.x && vb + q < m.y) trace_rec<TRACE>(a, vb + q, team, unit);
-          }
-        }
-      }
+      for (int k = 0; k < SEGV; ++k)
+        if (k < m2.y) consume_vec(row, k, (m2.x + k) << LOGV, false, m);
     }
     if constexpr (BODY == SB_AXPY) {
       __syncwarp();
       const char *sb = rows + st * L::STAGE + 32 * L::ROW;
+      const int k = lane % SEGV;
 #pragma unroll
       for (int q = 0; q < SEGV; ++q) {
         const int ju = q * UPI + lane / SEGV;
-        const int k = lane % SEGV;
-        const longlong2 mj = meta[st * 32 + ju];
-        if (mj.y > mj.x) {
-          const int64_t v0 = mj.x / VEC, v1 = (mj.y + VEC - 1) / VEC;
-          if (k < v1 - v0) {
-            const int64_t vb = (v0 + k) * VEC;
-            const float4 y = *reinterpret_cast<const float4 *>(sb + ju * L::ROW + k * 16);
-            float *dst = reinterpret_cast<float *>(gy) + vb;
-            if (vb >= mj.x && vb + VEC <= mj.y) {
-              __stcs(reinterpret_cast<float4 *>(dst), y);
-            } else {   // partial vector at a unit boundary: element-exact stores
-              const float yy[4] = {y.x, y.y, y.z, y.w};
+        const longlong2 mj2 = meta2[st * 32 + ju];
+        if (k < mj2.y) {
+          const longlong2 mj = meta[st * 32 + ju];
+          const int64_t vb = (mj2.x + k) << LOGV;
+          const float4 y = *reinterpret_cast<const float4 *>(sb + ju * L::ROW + k * 16);
+          float *dst = reinterpret_cast<float *>(gy) + vb;
+          if (vb >= mj.x && vb + VEC <= mj.y) {
+            __stcs(reinterpret_cast<float4 *>(dst), y);
+          } else {   // partial vector at a unit boundary: element-exact stores
+            const float yy[4] = {y.x, y.y, y.z, y.w};
 #pragma unroll
-              for (int qq = 0; qq < 4; ++qq)
-                if (vb + qq >= mj.x && vb + qq < mj.y) dst[qq] = yy[qq];
-            }
+            for (int qq = 0; qq < 4; ++qq)
+              if (vb + qq >= mj.x && vb + qq < mj.y) dst[qq] = yy[qq];
           }
         }
       }
@@ -403,14 +450,30 @@ __device__ void reduce_epilogue(const StreamArgs &a, Acc<BODY, NRED> &acc, bool 
     if constexpr (BODY == SB_RED_I64) return (W)(long long)b;
     else return __longlong_as_double((long long)b);
   };
+  // Warp combine over the wl lanes that exist (a team's last warp may be
+  // partial when num_units % 32 != 0): butterfly for full warps, ordered
+  // gather to lane 0 otherwise.  Fixed order either way (reading c10).
+  auto warp_comb = [&](int op, W x, int wl) -> W {
+    if (wl == 32) {
+#pragma unroll
+      for (int m = 16; m >= 1; m >>= 1) x = comb(op, x, from_bits(__shfl_xor_sync(FULL, to_bits(x), m)));
+      return x;
+    }
+    const unsigned mask = (1u << wl) - 1u;
+    W acc = x;
+    for (int l = 1; l < wl; ++l) {
+      const W o = from_bits(__shfl_sync(mask, to_bits(x), l));
+      acc = comb(op, acc, o);
+    }
+    return acc;   // valid in lane 0
+  };
+  const int rem = (int)(blockDim.x & 31u);
+  const int my_wl = (warp == nwarps - 1 && rem) ? rem : 32;
+  const int w0_wl = blockDim.x >= 32 ? 32 : (int)blockDim.x;
   auto block_tree = [&](W (&v)[NRED > 0 ? NRED : 1]) {
 #pragma unroll
     for (int r = 0; r < NRED; ++r) {
-#pragma unroll
-      for (int m = 16; m >= 1; m >>= 1) {
-        const W o = from_bits(__shfl_xor_sync(FULL, to_bits(v[r]), m));
-        v[r] = comb(a.red[r].op, v[r], o);
-      }
+      v[r] = warp_comb(a.red[r].op, v[r], my_wl);
       if (lane == 0) s_part[warp][r] = to_bits(v[r]);
     }
     __syncthreads();
@@ -418,9 +481,7 @@ __device__ void reduce_epilogue(const StreamArgs &a, Acc<BODY, NRED> &acc, bool 
 #pragma unroll
       for (int r = 0; r < NRED; ++r) {
         W x = lane < nwarps ? from_bits(s_part[lane][r]) : ident(a.red[r].op);
-#pragma unroll
-        for (int m = 16; m >= 1; m >>= 1) x = comb(a.red[r].op, x, from_bits(__shfl_xor_sync(FULL, to_bits(x), m)));
-        v[r] = x;
+        v[r] = warp_comb(a.red[r].op, x, w0_wl);
       }
     }
     __syncthreads();

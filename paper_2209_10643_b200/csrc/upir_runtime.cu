@@ -70,6 +70,7 @@ struct upir_map_s {
   int64_t elems_local;           // local elements (rows*row_elems)
   int64_t elem_offset;           // global element index of local element 0
   int64_t elem_bytes;
+  bool pinned = false;     // took a user count on a registration
 };
 
 struct upir_event_s {
@@ -104,7 +105,9 @@ struct upir_ctx_s {
   // present table: host pointer -> map
   std::map<void *, upir_map> present;
   std::vector<upir_map> adopted;
-  std::vector<std::pair<void *, size_t>> registered;   // host ranges we pinned
+  // host ranges this context pinned with cudaHostRegister: {ptr, bytes, live maps}
+  struct Reg { void *ptr; size_t bytes; int users; };
+  std::vector<Reg> registered;
   std::vector<upir_spmd> regions;
   cudaError_t sticky = cudaSuccess;
   bool capturing = false;
@@ -216,7 +219,7 @@ extern "C" upir_status upir_finalize(upir_ctx c) {
   if (!c->present.empty() || !c->adopted.empty())
     return fail(UPIR_E_LEAK, "finalize with %zu live maps", c->present.size() + c->adopted.size());
   upir_status st = sticky_check(c);
-  for (auto &r : c->registered) cudaHostUnregister(r.first);
+  for (auto &r : c->registered) cudaHostUnregister(r.ptr);
   for (auto s : c->regions) delete s;
   if (c->comm) ncclCommDestroy(c->comm);
   cudaFree(c->slots);
@@ -285,21 +288,48 @@ static void map_range(upir_map m, bool owned_only, size_t &host_off, size_t &dev
   }
 }
 
-static upir_status pin_host(upir_ctx c, void *host, size_t bytes) {
+// Pin a caller host range for async DMA.  Memory the caller already pinned
+// (cudaHostAlloc / torch pin_memory) is used as is.  Ranges we register are
+// released at the first upir_sync (or finalize) after their last map is gone
+// -- the contract keeps host buffers valid until that sync.
+static void pin_host(upir_ctx c, void *host, size_t bytes) {
+  for (auto &r : c->registered)
+    if ((char *)host >= (char *)r.ptr && (char *)host + bytes <= (char *)r.ptr + r.bytes) {
+      r.users++;
+      return;
+    }
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, host) == cudaSuccess &&
       (at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeManaged))
-    return UPIR_OK;
+    return;
   cudaGetLastError();
-  for (auto &r : c->registered)
-    if ((char *)host >= (char *)r.first && (char *)host + bytes <= (char *)r.first + r.second) return UPIR_OK;
   cudaError_t e = cudaHostRegister(host, bytes, cudaHostRegisterDefault);
   if (e != cudaSuccess) {
     cudaGetLastError();
-    return UPIR_OK;   // pageable copies still work (synchronously staged by the driver)
+    return;   // pageable copies still work (staged by the driver)
   }
-  c->registered.push_back({host, bytes});
-  return UPIR_OK;
+  c->registered.push_back({host, bytes, 1});
+}
+
+static void unpin_host(upir_ctx c, void *host) {
+  for (auto &r : c->registered)
+    if ((char *)host >= (char *)r.ptr && (char *)host < (char *)r.ptr + r.bytes) {
+      r.users--;
+      return;
+    }
+}
+
+// after all copies completed: drop registrations without live maps
+static void release_pins(upir_ctx c) {
+  for (size_t i = 0; i < c->registered.size();) {
+    if (c->registered[i].users <= 0) {
+      cudaHostUnregister(c->registered[i].ptr);
+      cudaGetLastError();
+      c->registered.erase(c->registered.begin() + i);
+    } else {
+      ++i;
+    }
+  }
 }
 
 // compute stream waits for everything enqueued on the copy stream so far
@@ -351,8 +381,11 @@ extern "C" upir_status upir_data_map(upir_ctx c, void *host, size_t bytes, upir_
     delete m;
     return fail(UPIR_E_OOM, "device allocation of %zu bytes failed: %s", alloc, cudaGetErrorString(e));
   }
-  if (kind == UPIR_MAP_TO || kind == UPIR_MAP_TOFROM) {   // data_movement forward
+  if (kind != UPIR_MAP_ALLOC) {
     pin_host(c, host, bytes);
+    m->pinned = true;
+  }
+  if (kind == UPIR_MAP_TO || kind == UPIR_MAP_TOFROM) {   // data_movement forward
     size_t ho, dof, len;
     map_range(m, false, ho, dof, len);
     e = cudaMemcpyAsync((char *)m->dev + dof, (char *)host + ho, len, cudaMemcpyHostToDevice, c->copy);
@@ -362,8 +395,6 @@ extern "C" upir_status upir_data_map(upir_ctx c, void *host, size_t bytes, upir_
       return fail(UPIR_E_CUDA, "H2D copy failed: %s", cudaGetErrorString(e));
     }
     c->h2d_bytes += (int64_t)len;
-  } else if (kind == UPIR_MAP_FROM || kind == UPIR_MAP_TOFROM) {
-    pin_host(c, host, bytes);
   }
   st = copy_to_compute(c);
   if (st != UPIR_OK) return st;
@@ -417,6 +448,7 @@ extern "C" upir_status upir_data_unmap(upir_ctx c, upir_map m) {
     c->d2h_bytes += (int64_t)len;
   }
   CUDA_TRY(cudaFreeAsync(m->dev, c->copy));   // mm_deallocator
+  if (m->pinned) unpin_host(c, m->host);
   c->present.erase(it);
   delete m;
   return sticky_check(c);
@@ -430,12 +462,10 @@ extern "C" upir_status upir_data_update(upir_ctx c, upir_map m, int direction) {
   size_t ho, dof, len;
   if (direction == 0) {
     map_range(m, false, ho, dof, len);
-    pin_host(c, m->host, m->bytes);
     CUDA_TRY(cudaMemcpyAsync((char *)m->dev + dof, (char *)m->host + ho, len, cudaMemcpyHostToDevice, c->copy));
     c->h2d_bytes += (int64_t)len;
   } else {
     map_range(m, true, ho, dof, len);
-    pin_host(c, m->host, m->bytes);
     CUDA_TRY(cudaMemcpyAsync((char *)m->host + ho, (char *)m->dev + dof, len, cudaMemcpyDeviceToHost, c->copy));
     c->d2h_bytes += (int64_t)len;
   }
@@ -746,10 +776,13 @@ static upir_status exec_stream(upir_spmd s, const upir_loop_desc *l, const upir_
                    : l->distribute == UPIR_DIST_UNITS ? sd.num_units
                    : (int64_t)sd.num_teams * sd.num_units;
   int64_t unit_chunk = sk == SK_STATIC_BLOCK ? (T + p - 1) / p : chunk;
-  bool staged = unit_chunk > VEC && (step == 1 || step == -1) && vx.aligned16 && (body != SB_AXPY || vy.aligned16);
+  // the staged path is warp-cooperative: it needs whole warps
+  const bool can_stage = (step == 1 || step == -1) && vx.aligned16 && (body != SB_AXPY || vy.aligned16) &&
+                         sd.num_units % 32 == 0;
+  bool staged = can_stage && unit_chunk > VEC;
   const char *ep = env_path();
   if (!strcmp(ep, "direct")) staged = false;
-  if (!strcmp(ep, "staged") && (step == 1 || step == -1) && vx.aligned16 && (body != SB_AXPY || vy.aligned16)) staged = true;
+  if (!strcmp(ep, "staged") && can_stage) staged = true;
   int segv = 0, nst = 0;
   size_t smem = 0;
   if (staged) {
@@ -767,6 +800,13 @@ static upir_status exec_stream(upir_spmd s, const upir_loop_desc *l, const upir_
       if (inflight > best + 1e-9) { best = inflight; segv = cf[0]; nst = cf[1]; smem = sm; }
     }
     if (best < 0) staged = false;
+    // experiment hook: UPIR_STAGE=segv,nst forces a configuration
+    const char *fc = getenv("UPIR_STAGE");
+    int fs = 0, fn = 0;
+    if (fc && sscanf(fc, "%d,%d", &fs, &fn) == 2) {
+      size_t sm = staged_smem_bytes(body, sd.num_units, fs, fn);
+      if (sm > 0 && sm <= 227 * 1024) { segv = fs; nst = fn; smem = sm; staged = true; }
+    }
   }
   if (!staged) { segv = 0; nst = 0; smem = 0; }
   cudaError_t e = launch_stream_loop(body, staged ? PATH_STAGED : PATH_DIRECT, segv, nst, trace != nullptr,
@@ -909,6 +949,7 @@ extern "C" upir_status upir_sync(upir_ctx c, int32_t kind, upir_map halo_map, up
       cudaError_t e2 = cudaStreamSynchronize(c->copy);
       if (e1 != cudaSuccess && c->sticky == cudaSuccess) c->sticky = e1;
       if (e2 != cudaSuccess && c->sticky == cudaSuccess) c->sticky = e2;
+      if (e1 == cudaSuccess && e2 == cudaSuccess) release_pins(c);
       if (c->comm) {
         ncclResult_t ar;
         if (ncclCommGetAsyncError(c->comm, &ar) == ncclSuccess && ar != ncclSuccess)
