@@ -13,14 +13,12 @@
 //           at most one 16-B vector: adjacent units own adjacent chunks, so a
 //           warp's loads are coalesced (chunked static / dynamic, small c).
 //  STAGED : chunks longer than a vector (static block, large c): adjacent
-//           units are far apart, so per-unit loads would touch 32 lines per
-//           warp instruction.  Instead the warp stages, for each of its 32
-//           units, the unit's next 128-B (or 64-B) segment into shared
-//           memory with cp.async (8 lanes per segment: 4 full lines per
-//           instruction), NST stages deep; each unit then executes the body
-//           on ITS OWN iterations from its shared-memory row.  AXPY results
-//           go back through the row and are stored cooperatively, element-
-//           exact at unit boundaries.
+//           units are far apart, so per-unit vector loads would touch 32
+//           lines per warp instruction.  Instead every unit moves its own
+//           next 64-256 B segment into a private shared-memory row with one
+//           TMA bulk copy (NST stages deep, mbarrier-tracked) and executes
+//           the body on ITS OWN iterations from that row.  AXPY results go
+//           back by bulk store, element-exact at unit boundaries.
 #pragma once
 #include <cuda_runtime.h>
 #include <math_constants.h>
@@ -175,6 +173,93 @@ __device__ __forceinline__ void direct_vec(const StreamArgs &a, int64_t e, Acc<B
   }
 }
 
+// One unit's contiguous element range [elo, ehi) of a reduction body: NV
+// 16-B vectors per load (NV = 2: 256-bit LDG with a 256-B L2 prefetch), U
+// loads in flight.  Scalar head / tail.
+template <int BODY, int NRED, int NV, int U>
+__device__ __forceinline__ void direct_long(const StreamArgs &a, int64_t elo, int64_t ehi, int64_t vec_hi,
+                                            Acc<BODY, NRED> &acc) {
+  constexpr int VEC = BODY == SB_RED_I64 ? 2 : 4;
+  constexpr int STEP = VEC * NV;   // elements per load
+  int64_t e = elo;
+  const int64_t ea = min(ehi, ((elo + STEP - 1) / STEP) * STEP);
+  for (; e < ea; ++e) body_scalar<BODY, NRED, false>(a, e, acc, 0, 0);
+  const int64_t eb = max(e, min(ehi, vec_hi) / STEP * STEP);
+  for (; e + U * STEP <= eb; e += U * STEP) {
+    if constexpr (BODY == SB_RED_I64) {
+      const long long *p = reinterpret_cast<const long long *>(a.in0) + e;
+      longlong2 v[U * NV];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        if constexpr (NV == 2)
+          asm("ld.global.cs.L2::256B.v4.s64 {%0,%1,%2,%3}, [%4];"
+              : "=l"(v[2 * q].x), "=l"(v[2 * q].y), "=l"(v[2 * q + 1].x), "=l"(v[2 * q + 1].y)
+              : "l"(p + q * STEP));
+        else
+          v[q] = __ldcs(reinterpret_cast<const longlong2 *>(p + q * STEP));
+      }
+#pragma unroll
+      for (int q = 0; q < U * NV; ++q) acc_l2(acc, v[q], true, true);
+    } else if constexpr (BODY == SB_AXPY) {
+      const float *px = reinterpret_cast<const float *>(a.in0) + e;
+      float *py = reinterpret_cast<float *>(a.out) + e;
+      float4 x[U * NV], y[U * NV];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        if constexpr (NV == 2) {
+          asm("ld.global.cs.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+              : "=f"(x[2 * q].x), "=f"(x[2 * q].y), "=f"(x[2 * q].z), "=f"(x[2 * q].w), "=f"(x[2 * q + 1].x),
+                "=f"(x[2 * q + 1].y), "=f"(x[2 * q + 1].z), "=f"(x[2 * q + 1].w)
+              : "l"(px + q * STEP));
+          asm volatile("ld.global.cs.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=f"(y[2 * q].x), "=f"(y[2 * q].y), "=f"(y[2 * q].z), "=f"(y[2 * q].w), "=f"(y[2 * q + 1].x),
+                         "=f"(y[2 * q + 1].y), "=f"(y[2 * q + 1].z), "=f"(y[2 * q + 1].w)
+                       : "l"(py + q * STEP)
+                       : "memory");
+        } else {
+          x[q] = __ldcs(reinterpret_cast<const float4 *>(px + q * STEP));
+          y[q] = __ldcs(reinterpret_cast<const float4 *>(py + q * STEP));
+        }
+      }
+#pragma unroll
+      for (int q = 0; q < U * NV; ++q) {
+        y[q].x = __fmaf_rn(a.alpha, x[q].x, y[q].x);
+        y[q].y = __fmaf_rn(a.alpha, x[q].y, y[q].y);
+        y[q].z = __fmaf_rn(a.alpha, x[q].z, y[q].z);
+        y[q].w = __fmaf_rn(a.alpha, x[q].w, y[q].w);
+        acc_f4(acc, y[q], true, true, true, true);
+      }
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        if constexpr (NV == 2)
+          asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(py + q * STEP), "f"(y[2 * q].x),
+                       "f"(y[2 * q].y), "f"(y[2 * q].z), "f"(y[2 * q].w), "f"(y[2 * q + 1].x), "f"(y[2 * q + 1].y),
+                       "f"(y[2 * q + 1].z), "f"(y[2 * q + 1].w)
+                       : "memory");
+        else
+          __stcs(reinterpret_cast<float4 *>(py + q * STEP), y[q]);
+      }
+    } else {
+      const float *p = reinterpret_cast<const float *>(a.in0) + e;
+      float4 v[U * NV];
+#pragma unroll
+      for (int q = 0; q < U; ++q) {
+        if constexpr (NV == 2)
+          asm("ld.global.cs.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+              : "=f"(v[2 * q].x), "=f"(v[2 * q].y), "=f"(v[2 * q].z), "=f"(v[2 * q].w), "=f"(v[2 * q + 1].x),
+                "=f"(v[2 * q + 1].y), "=f"(v[2 * q + 1].z), "=f"(v[2 * q + 1].w)
+              : "l"(p + q * STEP));
+        else
+          v[q] = __ldcs(reinterpret_cast<const float4 *>(p + q * STEP));
+      }
+#pragma unroll
+      for (int q = 0; q < U * NV; ++q) acc_f4(acc, v[q], true, true, true, true);
+    }
+  }
+  for (; e + VEC <= eb; e += VEC) direct_vec<BODY, NRED, false>(a, e, acc, 0, 0);
+  for (; e < ehi; ++e) body_scalar<BODY, NRED, false>(a, e, acc, 0, 0);
+}
+
 template <int BODY, int NRED, bool TRACE>
 __device__ void direct_run(const StreamArgs &a, const LaneWork &w, Acc<BODY, NRED> &acc, int team,
                            int unit) {
@@ -210,38 +295,32 @@ __device__ void direct_run(const StreamArgs &a, const LaneWork &w, Acc<BODY, NRE
     }
     for (; j < nfull; ++j) direct_vec<BODY, NRED, TRACE>(a, e0 + j * w.kstride, acc, team, unit);
   }
-  // long contiguous chunks (static block / large c) with step 1: per-unit
-  // 16-B vectors, 4 in flight (adjacent units are far apart: uncoalesced,
-  // relies on L1 sector reuse -- the STAGED path is the coalesced variant)
+  // long contiguous chunks (static block / large c) with step 1: every unit
+  // streams its own range with wide vector loads, several in flight
+  // (adjacent units are far apart, so a warp instruction touches 32 lines;
+  // each line is then consumed from L1 by the following loads of the lane).
   if (a.step == 1 && w.c > VEC) {
     const int64_t vec_hi = (a.safe_hi / VEC) * VEC;
     for (; j < w.nk; ++j) {
       int64_t klo, khi;
       chunk_bounds(w, j, a.T, klo, khi);
       const int64_t elo = a.lb + klo, ehi = a.lb + khi;
+      if constexpr (!TRACE) {
+        switch (a.dvar) {
+          case 1: direct_long<BODY, NRED, 2, 4>(a, elo, ehi, vec_hi, acc); break;
+          case 2: direct_long<BODY, NRED, 2, 2>(a, elo, ehi, vec_hi, acc); break;
+          case 3: direct_long<BODY, NRED, 1, 8>(a, elo, ehi, vec_hi, acc); break;
+          default: direct_long<BODY, NRED, 1, 4>(a, elo, ehi, vec_hi, acc); break;
+        }
+        continue;
+      }
       int64_t e = elo;
       const int64_t ea = min(ehi, ((elo + VEC - 1) / VEC) * VEC);
       for (; e < ea; ++e) body_scalar<BODY, NRED, TRACE>(a, e, acc, team, unit);
       const int64_t eb = max(e, min(ehi, vec_hi) / VEC * VEC);
       for (; e + 4 * VEC <= eb; e += 4 * VEC) {
-        if constexpr (BODY == SB_RED_I64 && !TRACE) {
-          longlong2 v[4];
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            v[q] = __ldcs(reinterpret_cast<const longlong2 *>(reinterpret_cast<const long long *>(a.in0) + e + q * VEC));
-#pragma unroll
-          for (int q = 0; q < 4; ++q) acc_l2(acc, v[q], true, true);
-        } else if constexpr (BODY == SB_RED_F32 && !TRACE) {
-          float4 v[4];
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            v[q] = __ldcs(reinterpret_cast<const float4 *>(reinterpret_cast<const float *>(a.in0) + e + q * VEC));
-#pragma unroll
-          for (int q = 0; q < 4; ++q) acc_f4(acc, v[q], true, true, true, true);
-        } else {
-#pragma unroll
-          for (int q = 0; q < 4; ++q) direct_vec<BODY, NRED, TRACE>(a, e + q * VEC, acc, team, unit);
-        }
+        for (int q = 0; q < 4; ++q) direct_vec<BODY, NRED, TRACE>(a, e + q * VEC, acc, team, unit);
       }
       for (; e + VEC <= eb; e += VEC) direct_vec<BODY, NRED, TRACE>(a, e, acc, team, unit);
       for (; e < ehi; ++e) body_scalar<BODY, NRED, TRACE>(a, e, acc, team, unit);
@@ -257,31 +336,82 @@ __device__ void direct_run(const StreamArgs &a, const LaneWork &w, Acc<BODY, NRE
 }
 
 // ================================================================ STAGED path
+// Per-unit bulk staging: every unit (lane) streams ITS OWN iterations through
+// a private shared-memory row with one TMA bulk copy (cp.async.bulk) per
+// segment of up to SEGV 16-B vectors, NST stages deep, completion tracked by
+// one mbarrier per warp and stage (32 arrivals + transaction bytes).  Rows
+// are padded by 16 B so the lanes' LDS.128 reads are bank-conflict free.
+// AXPY results are written back from the row with a bulk store (full
+// vectors) and element-exact scalar stores at unit boundaries.
 template <int BODY, int SEGV, int NST>
 struct StagedLayout {
-  static constexpr int ROW = SEGV * 16 + 16;                 // padded row: conflict-free
+  static constexpr int ROW = SEGV * 16 + 16;
   static constexpr int NBUF = BODY == SB_AXPY ? 2 : 1;
   static constexpr int STAGE = 32 * ROW * NBUF;
-  static constexpr int META = 32 * 32;                        // 2 x longlong2 per lane
-  static constexpr int WARP_BYTES = NST * (STAGE + META);
+  static constexpr int META = 32 * 16;
+  static constexpr int WARP_BYTES = ((NST * (STAGE + META) + 8 * NST + 127) / 128) * 128;
 };
 
+__device__ __forceinline__ unsigned smem_u32(const void *p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(unsigned long long *bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(unsigned long long *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(unsigned long long *bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *bar, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, unsigned bytes, unsigned long long *bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void *dst, const void *src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;\n" ::"l"(dst), "r"(smem_u32(src)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
+template <int BODY, int SEGV, int NST>
+__device__ __forceinline__ void staged_init(char *wsm) {
+  using L = StagedLayout<BODY, SEGV, NST>;
+  unsigned long long *bars = reinterpret_cast<unsigned long long *>(wsm + NST * (L::STAGE + L::META));
+  if ((threadIdx.x & 31) == 0)
+    for (int i = 0; i < NST; ++i) mbar_init(bars + i, 32);
+  asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  __syncwarp();
+}
+
 template <int BODY, int NRED, bool TRACE, int SEGV, int NST>
-__device__ void staged_run(const StreamArgs &a, const LaneWork &w, Acc<BODY, NRED> &acc, int team,
-                           int unit, char *wsm) {
+__device__ void staged_run(const StreamArgs &a, const LaneWork &w, Acc<BODY, NRED> &acc, int team, int unit,
+                           char *wsm, int64_t &sglob) {
   using L = StagedLayout<BODY, SEGV, NST>;
   constexpr int VEC = BODY == SB_RED_I64 ? 2 : 4;
-  constexpr int ESZ = 16 / VEC;
-  constexpr int UPI = 32 / SEGV;   // units covered by one cooperative instruction
+  constexpr int LOGV = VEC == 2 ? 1 : 2;
   const int lane = threadIdx.x & 31;
   char *rows = wsm;
   longlong2 *meta = reinterpret_cast<longlong2 *>(wsm + NST * L::STAGE);
+  unsigned long long *bars = reinterpret_cast<unsigned long long *>(wsm + NST * (L::STAGE + L::META));
   const char *gx = reinterpret_cast<const char *>(a.in0);
   char *gy = reinterpret_cast<char *>(a.out);
   const int64_t vec_hi = (a.safe_hi / VEC) * VEC;
 
   int64_t j = 0, e_cur = 0, e_end = 0;
-
   auto next_interval = [&]() -> bool {
     while (e_cur >= e_end) {
       if (j >= w.nk) return false;
@@ -297,42 +427,34 @@ __device__ void staged_run(const StreamArgs &a, const LaneWork &w, Acc<BODY, NRE
     return true;
   };
 
-  // meta[st][lane]  = {elo, ehi}  : the lane's element interval of stage st
-  // meta2[st][lane] = {v0, nv}     : its 16-B vectors [v0, v0 + nv)
-  longlong2 *meta2 = meta + NST * 32;
-  constexpr int LOGV = VEC == 2 ? 1 : 2;
-
+  // stage s -> slot s % NST, mbarrier phase parity (s / NST) & 1
   auto issue = [&](int64_t s) -> bool {
-    const int st = (int)(s % NST);
-    longlong2 m = make_longlong2(0, 0), m2 = make_longlong2(0, 0);
+    const int slot = (int)(s % NST);
+    longlong2 m = make_longlong2(0, 0);
+    int64_t v0 = 0, nv = 0;
     if (next_interval()) {
-      const int64_t v0 = (int64_t)((uint64_t)e_cur >> LOGV);
-      const int64_t vseg_end = (v0 & ~(int64_t)(SEGV - 1)) + SEGV;   // segments end on SEGV boundaries
+      v0 = (int64_t)((uint64_t)e_cur >> LOGV);
+      const int64_t vseg_end = (v0 & ~(int64_t)(SEGV - 1)) + SEGV;   // segments end on SEGV*16-B boundaries
       const int64_t seg_hi = min(e_end, vseg_end << LOGV);
-      const int64_t v1 = (int64_t)(((uint64_t)seg_hi + VEC - 1) >> LOGV);
+      nv = (int64_t)(((uint64_t)seg_hi + VEC - 1) >> LOGV) - v0;
       m = make_longlong2(e_cur, seg_hi);
-      m2 = make_longlong2(v0, v1 - v0);
       e_cur = seg_hi;
     }
-    meta[st * 32 + lane] = m;
-    meta2[st * 32 + lane] = m2;
-    __syncwarp();
-    if (!__any_sync(FULL, m2.y > 0)) return false;
-    char *sb = rows + st * L::STAGE;
-    const int k = lane % SEGV;
-#pragma unroll
-    for (int q = 0; q < SEGV; ++q) {
-      const int ju = q * UPI + lane / SEGV;
-      const longlong2 mj = meta2[st * 32 + ju];
-      if (k < mj.y) {
-        cp_async16(sb + ju * L::ROW + k * 16, gx + (mj.x + k) * 16);
-        if constexpr (BODY == SB_AXPY) cp_async16(sb + 32 * L::ROW + ju * L::ROW + k * 16, gy + (mj.x + k) * 16);
-      }
+    meta[slot * 32 + lane] = m;
+    unsigned long long *bar = bars + slot;
+    char *row = rows + slot * L::STAGE + lane * L::ROW;
+    if (nv > 0) {
+      fence_proxy_async();   // my earlier generic reads of this row precede the async write
+      mbar_arrive_tx(bar, (unsigned)(nv * 16 * L::NBUF));
+      bulk_g2s(row, gx + v0 * 16, (unsigned)(nv * 16), bar);
+      if constexpr (BODY == SB_AXPY) bulk_g2s(row + 32 * L::ROW, gy + v0 * 16, (unsigned)(nv * 16), bar);
+    } else {
+      mbar_arrive(bar);
     }
-    return true;
+    return __any_sync(FULL, nv > 0);
   };
 
-  auto consume_vec = [&](char *row, int k, int64_t vb, bool full, const longlong2 &m) {
+  auto consume_vec = [&](const char *row, int k, int64_t vb, bool full, const longlong2 &m) {
     if constexpr (BODY == SB_RED_I64) {
       const longlong2 v = *reinterpret_cast<const longlong2 *>(row + k * 16);
       if (full) acc_l2(acc, v, true, true);
@@ -344,7 +466,7 @@ __device__ void staged_run(const StreamArgs &a, const LaneWork &w, Acc<BODY, NRE
                   vb + 3 >= m.x && vb + 3 < m.y);
     } else {
       const float4 x = *reinterpret_cast<const float4 *>(row + k * 16);
-      float4 *yr = reinterpret_cast<float4 *>(row + 32 * L::ROW + k * 16);
+      float4 *yr = reinterpret_cast<float4 *>(const_cast<char *>(row) + 32 * L::ROW + k * 16);
       float4 y = *yr;
       y.x = __fmaf_rn(a.alpha, x.x, y.x);
       y.y = __fmaf_rn(a.alpha, x.y, y.y);
@@ -363,67 +485,56 @@ __device__ void staged_run(const StreamArgs &a, const LaneWork &w, Acc<BODY, NRE
   };
 
   auto consume = [&](int64_t s) {
-    const int st = (int)(s % NST);
-    const longlong2 m = meta[st * 32 + lane];
-    const longlong2 m2 = meta2[st * 32 + lane];
-    char *row = rows + st * L::STAGE + lane * L::ROW;
-    if (m2.y == SEGV && m.x == (m2.x << LOGV) && m.y == ((m2.x + SEGV) << LOGV)) {
+    const int slot = (int)(s % NST);
+    mbar_wait(bars + slot, (unsigned)((s / NST) & 1));
+    const longlong2 m = meta[slot * 32 + lane];
+    if (m.y <= m.x) return;
+    const char *row = rows + slot * L::STAGE + lane * L::ROW;
+    const int64_t v0 = (int64_t)((uint64_t)m.x >> LOGV);
+    const int nv = (int)((((uint64_t)m.y + VEC - 1) >> LOGV) - v0);
+    if (nv == SEGV && m.x == (v0 << LOGV) && m.y == ((v0 + SEGV) << LOGV)) {
 #pragma unroll
-      for (int k = 0; k < SEGV; ++k) consume_vec(row, k, (m2.x + k) << LOGV, true, m);
+      for (int k = 0; k < SEGV; ++k) consume_vec(row, k, (v0 + k) << LOGV, true, m);
     } else {
 #pragma unroll
       for (int k = 0; k < SEGV; ++k)
-        if (k < m2.y) consume_vec(row, k, (m2.x + k) << LOGV, false, m);
+        if (k < nv) consume_vec(row, k, (v0 + k) << LOGV, false, m);
     }
     if constexpr (BODY == SB_AXPY) {
-      __syncwarp();
-      const char *sb = rows + st * L::STAGE + 32 * L::ROW;
-      const int k = lane % SEGV;
-#pragma unroll
-      for (int q = 0; q < SEGV; ++q) {
-        const int ju = q * UPI + lane / SEGV;
-        const longlong2 mj2 = meta2[st * 32 + ju];
-        if (k < mj2.y) {
-          const longlong2 mj = meta[st * 32 + ju];
-          const int64_t vb = (mj2.x + k) << LOGV;
-          const float4 y = *reinterpret_cast<const float4 *>(sb + ju * L::ROW + k * 16);
-          float *dst = reinterpret_cast<float *>(gy) + vb;
-          if (vb >= mj.x && vb + VEC <= mj.y) {
-            __stcs(reinterpret_cast<float4 *>(dst), y);
-          } else {   // partial vector at a unit boundary: element-exact stores
-            const float yy[4] = {y.x, y.y, y.z, y.w};
-#pragma unroll
-            for (int qq = 0; qq < 4; ++qq)
-              if (vb + qq >= mj.x && vb + qq < mj.y) dst[qq] = yy[qq];
-          }
-        }
+      // write back y': full vectors by one bulk store, boundary vectors element-exact
+      const float *yrow = reinterpret_cast<const float *>(row + 32 * L::ROW);
+      const int64_t f0 = (m.x + VEC - 1) >> LOGV;         // first full vector
+      const int64_t f1 = m.y >> LOGV;                      // end of full vectors
+      for (int64_t e = m.x; e < min((int64_t)m.y, f0 << LOGV); ++e) reinterpret_cast<float *>(gy)[e] = yrow[e - (v0 << LOGV)];
+      if (f1 > f0) {
+        fence_proxy_async();   // generic smem writes of y' -> visible to the bulk store
+        bulk_s2g(gy + f0 * 16, row + 32 * L::ROW + (f0 - v0) * 16, (unsigned)((f1 - f0) * 16));
+        bulk_commit();
       }
+      for (int64_t e = max((int64_t)m.x, f1 << LOGV); e < m.y; ++e) reinterpret_cast<float *>(gy)[e] = yrow[e - (v0 << LOGV)];
     }
   };
 
-  int64_t s_issue = 0, s_cons = 0;
+  int64_t s_issue = sglob, s_cons = sglob;
   bool more = true;
 #pragma unroll
   for (int q = 0; q < NST - 1; ++q) {
     if (more) {
       more = issue(s_issue);
-      if (more) ++s_issue;
+      ++s_issue;
     }
-    cp_async_commit();
   }
   while (s_cons < s_issue) {
     if (more) {
+      if constexpr (BODY == SB_AXPY) bulk_wait_read0();   // the slot's last bulk store has read its row
       more = issue(s_issue);
-      if (more) ++s_issue;
+      ++s_issue;
     }
-    cp_async_commit();
-    cp_async_wait<NST - 1>();
-    __syncwarp();
     consume(s_cons);
     ++s_cons;
-    __syncwarp();
   }
-  (void)ESZ;
+  if constexpr (BODY == SB_AXPY) bulk_wait0();
+  sglob = s_issue;
 }
 
 // ================================================================ epilogue
@@ -542,10 +653,14 @@ __global__ void __launch_bounds__(1024) stream_loop_kernel(const __grid_constant
   Acc<BODY, NRED> acc;
   acc.init(a);
   char *wsm = nullptr;
-  if constexpr (PATH == PATH_STAGED) wsm = dyn_smem + (threadIdx.x >> 5) * StagedLayout<BODY, SEGV, NST>::WARP_BYTES;
+  int64_t sglob = 0;   // staged: stage counter of this warp (mbarrier phases)
+  if constexpr (PATH == PATH_STAGED) {
+    wsm = dyn_smem + (threadIdx.x >> 5) * StagedLayout<BODY, SEGV, NST>::WARP_BYTES;
+    staged_init<BODY, SEGV, NST>(wsm);
+  }
 
   auto run = [&](const LaneWork &w) {
-    if constexpr (PATH == PATH_STAGED) staged_run<BODY, NRED, TRACE, SEGV, NST>(a, w, acc, team, unit, wsm);
+    if constexpr (PATH == PATH_STAGED) staged_run<BODY, NRED, TRACE, SEGV, NST>(a, w, acc, team, unit, wsm, sglob);
     else direct_run<BODY, NRED, TRACE>(a, w, acc, team, unit);
   };
 
@@ -573,11 +688,11 @@ cudaError_t launch_stream_body(int nred, int path, int segv, int nst, bool trace
                                int units, size_t smem, const StreamArgs &a, cudaStream_t s) {
   void (*k)(StreamArgs) = nullptr;
 #define UPIR_PICK(NR, TR)                                                                  \
-  if (path == PATH_DIRECT) k = stream_loop_kernel<BODY, NR, TR, PATH_DIRECT, 0, 0>;        \
-  else if (segv == 8 && nst == 4) k = stream_loop_kernel<BODY, NR, TR, PATH_STAGED, 8, 4>; \
-  else if (segv == 8 && nst == 3) k = stream_loop_kernel<BODY, NR, TR, PATH_STAGED, 8, 3>; \
-  else if (segv == 8 && nst == 2) k = stream_loop_kernel<BODY, NR, TR, PATH_STAGED, 8, 2>; \
-  else if (segv == 4 && nst == 3) k = stream_loop_kernel<BODY, NR, TR, PATH_STAGED, 4, 3>; \
+  if (path == PATH_DIRECT) k = stream_loop_kernel<BODY, NR, TR, PATH_DIRECT, 0, 0>;          \
+  else if (segv == 16 && nst == 3) k = stream_loop_kernel<BODY, NR, TR, PATH_STAGED, 16, 3>; \
+  else if (segv == 16 && nst == 2) k = stream_loop_kernel<BODY, NR, TR, PATH_STAGED, 16, 2>; \
+  else if (segv == 8 && nst == 3) k = stream_loop_kernel<BODY, NR, TR, PATH_STAGED, 8, 3>;   \
+  else if (segv == 8 && nst == 2) k = stream_loop_kernel<BODY, NR, TR, PATH_STAGED, 8, 2>;   \
   else if (segv == 4 && nst == 2) k = stream_loop_kernel<BODY, NR, TR, PATH_STAGED, 4, 2>;
   if (nred == 0) {
     if (trace) { UPIR_PICK(0, true) } else { UPIR_PICK(0, false) }
@@ -600,10 +715,10 @@ template <int BODY>
 size_t staged_bytes_body(int units, int segv, int nst) {
   const int warps = (units + 31) / 32;
   size_t per = 0;
-  if (segv == 8 && nst == 4) per = StagedLayout<BODY, 8, 4>::WARP_BYTES;
+  if (segv == 16 && nst == 3) per = StagedLayout<BODY, 16, 3>::WARP_BYTES;
+  else if (segv == 16 && nst == 2) per = StagedLayout<BODY, 16, 2>::WARP_BYTES;
   else if (segv == 8 && nst == 3) per = StagedLayout<BODY, 8, 3>::WARP_BYTES;
   else if (segv == 8 && nst == 2) per = StagedLayout<BODY, 8, 2>::WARP_BYTES;
-  else if (segv == 4 && nst == 3) per = StagedLayout<BODY, 4, 3>::WARP_BYTES;
   else if (segv == 4 && nst == 2) per = StagedLayout<BODY, 4, 2>::WARP_BYTES;
   return per * warps;
 }

@@ -42,6 +42,7 @@ struct StreamArgs {
   void *out;            // axpy: y
   float alpha;
   int64_t safe_lo, safe_hi;  // elements [safe_lo, safe_hi) may be read as 16-B vectors
+  int32_t dvar;              // DIRECT long-chunk load variant (0: 4x16 B, 1: 4x32 B, 2: 2x32 B, 3: 8x16 B)
   // reductions
   int32_t nred;
   RedSpec red[2];
