@@ -62,6 +62,7 @@ def lib():
             "orc_jacobi5_window": (i32, [i64, i64, i64, i64, i64, i64, i64, vp, vp]),
             "orc_matmul_rows": (i32, [i64, i64, i64, vp, vp, vp, i64, vp]),
             "orc_tile_owner": (i32, [i64, i64, i64, i64, i32, i64, i64, vp]),
+            "orc_tiled_owner": (i64, [i64, i64, i64, i64, i64, i64, i32, i64, i64, i64, i64, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -116,6 +117,19 @@ def tile_owner(R, C, tm, tn, policy, chunk, p):
     owner = np.zeros(max(nt, 1), dtype=np.int64)
     _check(lib().orc_tile_owner(R, C, tm, tn, policy, chunk, p, _p(owner)), "tile_owner")
     return owner[:nt]
+
+
+def tiled_owner(lb0, ub0, lb1, ub1, BM, BN, policy, chunk, p_teams, ic, units):
+    """(team, unit) of every box position of a tiled collapse(2) nest (c24)."""
+    if ub0 <= lb0 or ub1 <= lb1:
+        return np.zeros(0, np.int64), np.zeros(0, np.int64)
+    nt = (((ub0 + BM - 1) // BM) - lb0 // BM) * (((ub1 + BN - 1) // BN) - lb1 // BN)
+    team = np.zeros(nt * BM * BN, dtype=np.int64)
+    unit = np.zeros(nt * BM * BN, dtype=np.int64)
+    r = lib().orc_tiled_owner(lb0, ub0, lb1, ub1, BM, BN, policy, chunk, p_teams, ic, units, _p(team), _p(unit))
+    if r != nt:
+        raise ValueError("tiled_owner failed")
+    return team, unit
 
 
 # ---- o4 ---------------------------------------------------------------------

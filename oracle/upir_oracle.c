@@ -389,3 +389,38 @@ int orc_tile_owner(int64_t R, int64_t Cn, int64_t tm, int64_t tn, int policy,
     int64_t ntiles = ((R + tm - 1) / tm) * ((Cn + tn - 1) / tn);
     return orc_owner_map(policy, chunk, ntiles, p, owner);
 }
+
+/* Executors of a tiled collapse(2) nest (reading c24; PAPER.md:622/666
+ * tiling before parallelisation, Fig. 3 distribute teams / units):
+ * tiles of BM x BN anchored at induction value 0 of each level cover the
+ * space [lb0,ub0) x [lb1,ub1); tile id = row-major over the tiles that touch
+ * the space; the tile loop runs over p_teams teams with (policy, chunk); the
+ * BM*BN box positions of a tile (row-major) run over `units` units with
+ * static chunk ic.  For box index t = tile*BM*BN + pos: team[t], unit[t] =
+ * executor, or -1 where the box position is not an iteration.  Returns the
+ * number of tiles, or -1. */
+int64_t orc_tiled_owner(int64_t lb0, int64_t ub0, int64_t lb1, int64_t ub1, int64_t BM, int64_t BN,
+                        int policy, int64_t chunk, int64_t p_teams, int64_t ic, int64_t units,
+                        int64_t *team, int64_t *unit)
+{
+    if (BM <= 0 || BN <= 0 || ic <= 0 || units <= 0 || p_teams <= 0) return -1;
+    if (ub0 <= lb0 || ub1 <= lb1) return 0;
+    int64_t ti0 = lb0 / BM, tj0 = lb1 / BN;
+    int64_t ntr = (ub0 + BM - 1) / BM - ti0, ntc = (ub1 + BN - 1) / BN - tj0;
+    int64_t nt = ntr * ntc, P = BM * BN;
+    int64_t *towner = (int64_t *)malloc(sizeof(int64_t) * (size_t)nt);
+    if (!towner) return -1;
+    if (orc_owner_map(policy, chunk, nt, p_teams, towner) != 0) { free(towner); return -1; }
+    for (int64_t tile = 0; tile < nt; ++tile) {
+        int64_t ti = ti0 + tile / ntc, tj = tj0 + tile % ntc;
+        for (int64_t pos = 0; pos < P; ++pos) {
+            int64_t i = ti * BM + pos / BN, j = tj * BN + pos % BN;
+            int64_t t = tile * P + pos;
+            if (i < lb0 || i >= ub0 || j < lb1 || j >= ub1) { team[t] = -1; unit[t] = -1; continue; }
+            team[t] = towner[tile];
+            unit[t] = (pos / ic) % units;          /* static, chunk ic over units */
+        }
+    }
+    free(towner);
+    return nt;
+}

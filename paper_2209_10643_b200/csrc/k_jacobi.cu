@@ -1,0 +1,247 @@
+// k_jacobi.cu -- the JACOBI5 loop body (north_star; reading c16):
+//   out[i][j] = 0.25 * ((in[i-1][j] + in[i+1][j]) + (in[i][j-1] + in[i][j+1]))
+// over a tiled collapse(2) upir.loop (tiling before
+// parallelisation; reading c24).  Tile loop over TEAMS under the loop's
+// schedule (static block / static,c / dynamic); inside a tile the BM x BN box
+// positions are scheduled static,ic over UNITS.
+//
+// B200 design: each team (CTA) walks its tiles with a 2-deep TMA pipeline:
+// while it computes tile t from shared memory, one elected thread has the
+// next tile's (BM+2) x BN centre box and two (BM+2) x 4 halo-column boxes in
+// flight (cp.async.bulk.tensor.2d, mbarrier complete_tx; out-of-range rows /
+// columns are zero-filled by the TMA unit and never written).  Results are
+// stored as coalesced 16-B vectors.  Every input element is read from HBM
+// once per sweep (neighbour tiles' halos hit L2): 8 B per lattice update.
+// fp32 arithmetic with explicit __fadd_rn/__fmul_rn: no FMA contraction, so
+// the result is independent of decomposition (1 vs N GPUs bit-identical).
+#include "dev_tma.cuh"
+#include "upir_internal.h"
+
+namespace upir {
+
+bool encode_tmap_2d(CUtensorMap *out, CUtensorMapDataType dt, const void *base, uint64_t cols, uint64_t rows,
+                    uint64_t pitch_bytes, uint32_t box_cols, uint32_t box_rows, CUtensorMapSwizzle swz,
+                    CUtensorMapL2promotion l2) {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void *p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !p)
+      return false;
+    fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {pitch_bytes};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t es[2] = {1, 1};
+  return fn(out, dt, 2, const_cast<void *>(base), dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, swz, l2,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+namespace {
+
+constexpr int align128(int x) { return (x + 127) / 128 * 128; }
+
+template <int BM, int BN>
+struct JLayout {
+  static constexpr int R = BM + 2;
+  static constexpr int CEN = align128(R * BN * 4);
+  static constexpr int HAL = align128(R * 4 * 4);
+  static constexpr int BUF = CEN + 2 * HAL;
+  static constexpr int TX = R * BN * 4 + 2 * R * 16;   // bytes per tile load
+  static constexpr int SMEM = 2 * BUF + 128;           // + mbarriers / tile ids
+};
+
+// Tile iterator of the tile loop (executed by thread 0 only).
+struct TileIter {
+  int64_t cur = 0, end = 0, k = 0;
+  bool started = false;
+};
+
+__device__ __forceinline__ int64_t next_tile(TileIter &it, const JacobiArgs &a, int64_t nt) {
+  const int64_t p = gridDim.x, t = blockIdx.x;
+  if (it.cur < it.end) return it.cur++;
+  if (a.sched == SK_STATIC_BLOCK) {
+    if (it.started) return -1;
+    it.started = true;
+    const int64_t q = nt / p, r = nt % p;
+    it.cur = t * q + (t < r ? t : r);
+    it.end = it.cur + q + (t < r ? 1 : 0);
+  } else if (a.sched == SK_STATIC_CHUNK) {
+    const int64_t kk = it.started ? it.k + p : t;
+    it.started = true;
+    it.k = kk;
+    it.cur = kk * a.chunk;
+    it.end = min(nt, it.cur + a.chunk);
+  } else {
+    const int64_t kk = (int64_t)atomicAdd(a.dyn_counter, 1ull);
+    it.cur = kk * a.chunk;
+    it.end = min(nt, it.cur + a.chunk);
+  }
+  if (it.cur >= it.end) return -1;
+  return it.cur++;
+}
+
+template <int BM, int BN, bool TRACE>
+__global__ void __launch_bounds__(1024) jacobi5_kernel(const __grid_constant__ JacobiArgs a,
+                                                       const __grid_constant__ CUtensorMap tmc,
+                                                       const __grid_constant__ CUtensorMap tmh) {
+  using L = JLayout<BM, BN>;
+  extern __shared__ __align__(128) char smem[];
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + 2 * L::BUF);
+  volatile long long *tile_s = reinterpret_cast<volatile long long *>(smem + 2 * L::BUF + 16);
+  __shared__ unsigned s_last;
+  const int64_t nt = a.ntr * a.ntc;
+  TileIter it;
+
+  auto issue = [&](int64_t tile, int buf) {
+    const int64_t ti = a.ti0 + tile / a.ntc, tj = a.tj0 + tile % a.ntc;
+    const int r0 = (int)(ti * BM - 1 - a.row0);   // local row of the box's first row
+    const int c0 = (int)(tj * BN);
+    char *b = smem + buf * L::BUF;
+    tma_fence_proxy();
+    tma_mbar_expect_tx(bars + buf, L::TX);
+    tma_load_2d(b, &tmc, c0, r0, bars + buf);
+    tma_load_2d(b + L::CEN, &tmh, c0 - 4, r0, bars + buf);
+    tma_load_2d(b + L::CEN + L::HAL, &tmh, c0 + BN, r0, bars + buf);
+  };
+
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmc);
+    tma_prefetch_desc(&tmh);
+    tma_mbar_init(bars + 0, 1);
+    tma_mbar_init(bars + 1, 1);
+    tma_fence_init();
+    const int64_t t0 = next_tile(it, a, nt);
+    tile_s[0] = t0;
+    if (t0 >= 0) issue(t0, 0);
+  }
+  __syncthreads();
+
+  const int units = blockDim.x, u = threadIdx.x;
+  const int ic = a.inner_chunk;
+  constexpr int POS = BM * BN;
+  for (int iter = 0;; ++iter) {
+    const int buf = iter & 1;
+    const int64_t tile = tile_s[buf];
+    if (tile < 0) break;
+    if (threadIdx.x == 0) {
+      const int64_t nx = next_tile(it, a, nt);
+      tile_s[buf ^ 1] = nx;
+      if (nx >= 0) issue(nx, buf ^ 1);
+    }
+    tma_mbar_wait(bars + buf, (unsigned)((iter >> 1) & 1));
+    const int64_t ti = a.ti0 + tile / a.ntc, tj = a.tj0 + tile % a.ntc;
+    const int64_t i0 = ti * BM, j0 = tj * BN;
+    const float *cen = reinterpret_cast<const float *>(smem + buf * L::BUF);
+    const float *lef = reinterpret_cast<const float *>(smem + buf * L::BUF + L::CEN);
+    const float *rig = reinterpret_cast<const float *>(smem + buf * L::BUF + L::CEN + L::HAL);
+    auto at = [&](int r, int c) -> float {   // smem row r (global row i0-1+r), tile column c in [-1, BN]
+      if (c < 0) return lef[r * 4 + 3];
+      if (c >= BN) return rig[r * 4 + (c - BN)];
+      return cen[r * BN + c];
+    };
+    if (ic == 4) {
+      // static,4 over units: chunk k = 4 consecutive columns of one row
+      for (int k = u; k * 4 < POS; k += units) {
+        const int r = (k * 4) / BN, c = (k * 4) % BN;
+        const int64_t i = i0 + r;
+        if (i < a.lb0 || i >= a.ub0) continue;
+        const int64_t j = j0 + c;
+        if (j + 3 < a.lb1 || j >= a.ub1) continue;
+        const float4 up = *reinterpret_cast<const float4 *>(cen + r * BN + c);
+        const float4 dn = *reinterpret_cast<const float4 *>(cen + (r + 2) * BN + c);
+        const float4 md = *reinterpret_cast<const float4 *>(cen + (r + 1) * BN + c);
+        const float w0 = at(r + 1, c - 1), e3 = at(r + 1, c + 4);
+        float4 o;
+        o.x = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(up.x, dn.x), __fadd_rn(w0, md.y)));
+        o.y = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(up.y, dn.y), __fadd_rn(md.x, md.z)));
+        o.z = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(up.z, dn.z), __fadd_rn(md.y, md.w)));
+        o.w = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(up.w, dn.w), __fadd_rn(md.z, e3)));
+        float *dst = a.out + (i - a.row0) * a.ld + j;
+        if (j >= a.lb1 && j + 4 <= a.ub1) {
+          __stcs(reinterpret_cast<float4 *>(dst), o);
+        } else {
+          const float ov[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (j + q >= a.lb1 && j + q < a.ub1) dst[q] = ov[q];
+        }
+        if constexpr (TRACE) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            if (j + q >= a.lb1 && j + q < a.ub1) {
+              const int64_t idx = tile * POS + r * BN + c + q;
+              a.trace[idx] = blockIdx.x;
+              a.trace[nt * POS + idx] = u;
+              atomicAdd(a.trace + 2 * nt * POS + idx, 1);
+            }
+        }
+      }
+    } else {
+      // static,ic over units, element by element
+      for (int64_t k = u; k * ic < POS; k += units) {
+        for (int pos = (int)(k * ic); pos < (int)min((int64_t)POS, (k + 1) * ic); ++pos) {
+          const int r = pos / BN, c = pos % BN;
+          const int64_t i = i0 + r, j = j0 + c;
+          if (i < a.lb0 || i >= a.ub0 || j < a.lb1 || j >= a.ub1) continue;
+          const float v = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(at(r, c), at(r + 2, c)),
+                                                     __fadd_rn(at(r + 1, c - 1), at(r + 1, c + 1))));
+          a.out[(i - a.row0) * a.ld + j] = v;
+          if constexpr (TRACE) {
+            const int64_t idx = tile * POS + pos;
+            a.trace[idx] = blockIdx.x;
+            a.trace[nt * POS + idx] = u;
+            atomicAdd(a.trace + 2 * nt * POS + idx, 1);
+          }
+        }
+      }
+    }
+    __syncthreads();   // buffer `buf` free; tile_s[buf ^ 1] visible
+  }
+  // dynamic: the last team resets the tile counter for the next launch
+  if (a.sched == SK_DYNAMIC) {
+    if (threadIdx.x == 0) {
+      __threadfence();
+      s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (s_last && threadIdx.x == 0) {
+      *a.done = 0u;
+      *a.dyn_counter = 0ull;
+    }
+  }
+}
+
+template <int BM, int BN>
+cudaError_t launch_bmbn(const JacobiArgs &a, const CUtensorMap &c, const CUtensorMap &h, int teams, int units,
+                        bool trace, cudaStream_t s) {
+  using L = JLayout<BM, BN>;
+  auto k = trace ? jacobi5_kernel<BM, BN, true> : jacobi5_kernel<BM, BN, false>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+  if (e != cudaSuccess) return e;
+  k<<<teams, units, L::SMEM, s>>>(a, c, h);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool jacobi_supported_tile(int bm, int bn) {
+  return (bm == 32 && bn == 256) || (bm == 32 && bn == 128) || (bm == 16 && bn == 256) || (bm == 64 && bn == 128) ||
+         (bm == 8 && bn == 64);
+}
+
+cudaError_t launch_jacobi_tma(const JacobiArgs &a, const void *tmc, const void *tmh, int teams, int units, int bm,
+                              int bn, bool trace, cudaStream_t s) {
+  const CUtensorMap &c = *reinterpret_cast<const CUtensorMap *>(tmc);
+  const CUtensorMap &h = *reinterpret_cast<const CUtensorMap *>(tmh);
+  if (bm == 32 && bn == 256) return launch_bmbn<32, 256>(a, c, h, teams, units, trace, s);
+  if (bm == 32 && bn == 128) return launch_bmbn<32, 128>(a, c, h, teams, units, trace, s);
+  if (bm == 16 && bn == 256) return launch_bmbn<16, 256>(a, c, h, teams, units, trace, s);
+  if (bm == 64 && bn == 128) return launch_bmbn<64, 128>(a, c, h, teams, units, trace, s);
+  if (bm == 8 && bn == 64) return launch_bmbn<8, 64>(a, c, h, teams, units, trace, s);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace upir

@@ -72,30 +72,26 @@ cudaError_t launch_synth_fill(int dist, uint64_t stream, void *dst, int64_t n, i
 
 // ---- Jacobi 5-point ----------------------------------------------------------
 struct JacobiArgs {
-  const float *in;      // element (i, j) at in[(i - row0) * ld + j]
-  float *out;
+  float *out;           // element (i, j) at out[(i - row0) * ld + j]
   int64_t ld;           // row pitch (elements)
   int64_t row0;         // global row of the first local row
-  int64_t local_rows;   // rows in the local buffer
   // iteration space (global induction values) [lb0,ub0) x [lb1,ub1), step 1
   int64_t lb0, ub0, lb1, ub1;
-  // tiles anchored at 0: tile rows [ti*BM, ti*BM+BM) ...
+  // tiles anchored at 0: tile (ti, tj) = rows [ti*BM, +BM) x cols [tj*BN, +BN)
   int64_t ti0, tj0;     // first tile indices touching the space
-  int64_t ntr, ntc;     // tile grid extent
-  int32_t sched;        // tile loop over teams
-  int64_t chunk;
-  int64_t ticket_m;
-  unsigned long long *dyn_counter;
+  int64_t ntr, ntc;     // tile grid extent; tile id = (ti-ti0)*ntc + (tj-tj0)
+  int32_t sched;        // tile loop over teams (SchedKind)
   int32_t inner_chunk;  // intra-tile static chunk over units
-  int32_t *trace;       // [team, unit, hits] x (ntiles * BM * BN) or null
-  void *tmap;           // device copy of the CUtensorMap (TMA path) or null
+  int64_t chunk;
+  unsigned long long *dyn_counter;
+  unsigned int *done;
+  int32_t *trace;       // [team | unit | hits] planes of ntiles*BM*BN int32, or null
 };
-cudaError_t launch_jacobi(const JacobiArgs &a, int teams, int units, int bm, int bn,
-                          bool trace, bool tma, cudaStream_t s);
-// Encode the TMA descriptor for a Jacobi input buffer (host).  Returns false
-// if the driver entry point is unavailable.
-bool jacobi_encode_tmap(void *tmap_out128, const float *base, int64_t rows, int64_t cols,
-                        int64_t ld, int bm, int bn);
+bool jacobi_supported_tile(int bm, int bn);
+// tmc / tmh: CUtensorMap (128 B) of the input buffer with boxes {BN, BM+2}
+// and {4, BM+2}.
+cudaError_t launch_jacobi_tma(const JacobiArgs &a, const void *tmc, const void *tmh, int teams, int units, int bm,
+                              int bn, bool trace, cudaStream_t s);
 
 // ---- matmul (tcgen05) ------------------------------------------------------------
 struct MatmulArgs {

@@ -19,6 +19,7 @@
 #include <string>
 #include <vector>
 
+#include "dev_tma.cuh"
 #include "upir_internal.h"
 
 using namespace upir;
@@ -848,8 +849,84 @@ extern "C" upir_status upir_loop_exec(upir_spmd s, const upir_loop_desc *l, cons
 }
 
 // ------------------------------------------------------------------ jacobi / matmul
-static upir_status exec_jacobi(upir_spmd, const upir_loop_desc *, const upir_body *, upir_map) {
-  return fail(UPIR_E_UNSUPPORTED, "JACOBI5 body not built yet");
+// Tile-loop schedule over teams (readings c3, c8, c24).
+static upir_status tile_sched(const upir_loop_desc *l, int &sk, int64_t &chunk) {
+  upir_status st = resolve_sched(l->policy, l->chunk, sk, chunk);
+  if (st != UPIR_OK) return st;
+  if (sk == SK_STATIC_BLOCK) chunk = 1;
+  return UPIR_OK;
+}
+
+static upir_status exec_jacobi(upir_spmd s, const upir_loop_desc *l, const upir_body *b, upir_map trace) {
+  upir_ctx c = s->ctx;
+  const upir_spmd_desc &sd = s->d;
+  upir_status st;
+  if ((st = check_map(c, b->in0, "in0")) != UPIR_OK) return st;
+  if ((st = check_map(c, b->out, "out")) != UPIR_OK) return st;
+  const int64_t ny = b->dims[0], ld = b->ld[0];
+  const int bm = (int)l->tile[0], bn = (int)l->tile[1];
+  if (!jacobi_supported_tile(bm, bn))
+    return fail(UPIR_E_UNSUPPORTED, "JACOBI5 tile %dx%d not built (32x256, 32x128, 16x256, 64x128, 8x64)", bm, bn);
+  if (ny < 3 || ld < 3) return fail(UPIR_E_INVALID, "JACOBI5 needs dims[0] (rows) >= 3 and ld[0] (row pitch) >= 3");
+  if (ld % 4 != 0) return fail(UPIR_E_UNSUPPORTED, "JACOBI5 row pitch must be a multiple of 4 elements (TMA stride)");
+  ElemView vi, vo;
+  if ((st = elem_view(b->in0, 4, vi)) != UPIR_OK) return st;
+  if ((st = elem_view(b->out, 4, vo)) != UPIR_OK) return st;
+  if (vi.lo != vo.lo || vi.hi != vo.hi) return fail(UPIR_E_INVALID, "in0 and out must have the same layout");
+  if (vi.lo % ld != 0 || vi.hi % ld != 0) return fail(UPIR_E_INVALID, "maps must hold whole rows of ld elements");
+  const int64_t row0 = vi.lo / ld, rows_local = (vi.hi - vi.lo) / ld;
+  // the 5-point stencil reads i +- 1 and j +- 1
+  int64_t lb0 = l->lb[0], ub0 = l->ub[0], lb1 = l->lb[1], ub1 = l->ub[1];
+  if (lb0 < 1 || ub0 > ny - 1 || lb1 < 1 || ub1 > ld - 1)
+    return fail(UPIR_E_INVALID, "JACOBI5 iteration space must lie in the grid interior [1,ny-1) x [1,ld-1)");
+  if (sd.target == UPIR_TARGET_CLUSTER && c->nranks > 1) {
+    upir_map m = b->in0;
+    if (m->dist.pattern != UPIR_PATTERN_BLOCK) return fail(UPIR_E_INVALID, "cluster JACOBI5 needs BLOCK-distributed maps");
+    lb0 = std::max(lb0, m->row_lo);
+    ub0 = std::min(ub0, m->row_hi);
+  }
+  if (ub0 > lb0 && (lb0 - 1 < row0 || ub0 + 1 > row0 + rows_local))
+    return fail(UPIR_E_INVALID, "rows [%lld,%lld) need halo rows outside the local buffer [%lld,%lld)", (long long)lb0,
+                (long long)ub0, (long long)row0, (long long)(row0 + rows_local));
+  JacobiArgs a;
+  memset(&a, 0, sizeof a);
+  a.out = reinterpret_cast<float *>(b->out->dev);
+  a.ld = ld;
+  a.row0 = row0;
+  a.lb0 = lb0;
+  a.ub0 = ub0;
+  a.lb1 = lb1;
+  a.ub1 = ub1;
+  if (ub0 <= lb0 || ub1 <= lb1) return UPIR_OK;   // empty iteration space
+  a.ti0 = lb0 / bm;
+  a.tj0 = lb1 / bn;
+  a.ntr = (ub0 + bm - 1) / bm - a.ti0;
+  a.ntc = (ub1 + bn - 1) / bn - a.tj0;
+  int sk;
+  int64_t chunk;
+  if ((st = tile_sched(l, sk, chunk)) != UPIR_OK) return st;
+  a.sched = sk;
+  a.chunk = chunk;
+  a.inner_chunk = (int)l->inner_chunk;
+  a.dyn_counter = c->dyn;
+  a.done = c->done;
+  if (trace) {
+    if ((st = check_map(c, trace, "trace")) != UPIR_OK) return st;
+    const int64_t need = 3 * a.ntr * a.ntc * bm * bn * 4;
+    if ((int64_t)trace->dev_bytes < need) return fail(UPIR_E_INVALID, "trace map needs %lld bytes", (long long)need);
+    a.trace = (int32_t *)trace->dev;
+  }
+  CUtensorMap tmc, tmh;
+  const void *base = b->in0->dev;
+  if (!encode_tmap_2d(&tmc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, base, (uint64_t)ld, (uint64_t)rows_local, (uint64_t)ld * 4,
+                      (uint32_t)bn, (uint32_t)(bm + 2), CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) ||
+      !encode_tmap_2d(&tmh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, base, (uint64_t)ld, (uint64_t)rows_local, (uint64_t)ld * 4, 4,
+                      (uint32_t)(bm + 2), CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B))
+    return fail(UPIR_E_CUDA, "cuTensorMapEncodeTiled failed for the JACOBI5 input");
+  cudaError_t e = launch_jacobi_tma(a, &tmc, &tmh, sd.num_teams, sd.num_units, bm, bn, trace != nullptr, c->compute);
+  if (e != cudaSuccess) return fail(UPIR_E_CUDA, "JACOBI5 launch failed: %s", cudaGetErrorString(e));
+  c->launches++;
+  return UPIR_OK;
 }
 static upir_status exec_matmul(upir_spmd, const upir_loop_desc *, const upir_body *, upir_map) {
   return fail(UPIR_E_UNSUPPORTED, "MATMUL body not built yet");

@@ -156,3 +156,23 @@ def test_tile_owner_static1_round_robin():
     own = oracle.tile_owner(10, 20, 3, 7, oracle.STATIC, 1, 4)
     ntiles = 4 * 3
     assert own.tolist() == [t % 4 for t in range(ntiles)]
+
+
+def test_tiled_owner_bruteforce():
+    # brute force from the reading: tiles anchored at 0, tile loop static,1
+    # over teams, box positions static,ic over units, out-of-space positions -1
+    lb0, ub0, lb1, ub1, BM, BN = 1, 10, 1, 13, 4, 8
+    team, unit = oracle.tiled_owner(lb0, ub0, lb1, ub1, BM, BN, oracle.STATIC, 1, 3, 4, 5)
+    tiles = [(ti, tj) for ti in range(0, 3) for tj in range(0, 2)]
+    t = 0
+    for tid, (ti, tj) in enumerate(tiles):
+        for pos in range(BM * BN):
+            i, j = ti * BM + pos // BN, tj * BN + pos % BN
+            if lb0 <= i < ub0 and lb1 <= j < ub1:
+                assert team[t] == tid % 3 and unit[t] == (pos // 4) % 5
+            else:
+                assert team[t] == -1 and unit[t] == -1
+            t += 1
+    assert t == len(team)
+    # every iteration appears exactly once
+    assert (team >= 0).sum() == (ub0 - lb0) * (ub1 - lb1)
