@@ -46,6 +46,7 @@ def parse():
     ap.add_argument("--n-log2", type=int, default=30)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-kernels", action="store_true", help="skip the axpy / Jacobi / matmul kernel lines")
     return ap.parse_args()
 
 
@@ -214,6 +215,14 @@ def run_upir(args):
         res = bench_reduce(args, U, ctx, stream, barrier, rank, world, peaks, peak_src)
     else:
         raise SystemExit(f"workload {args.workload} not built yet")
+    # the other loop bodies of the path, each timed on its own (single GPU)
+    if world == 1 and not args.no_kernels:
+        res["kernels"] = {}
+        for name, fn in (("axpy", bench_axpy), ("jacobi", bench_jacobi), ("matmul", bench_matmul)):
+            try:
+                res["kernels"][name] = fn(args, U, ctx, stream, peaks, peak_src)
+            except Exception as e:   # report, never hide
+                res["kernels"][name] = {"error": str(e)[:300]}
     # max over ranks of the timed values
     if pg:
         t = torch.tensor([res["ms_per_step"], res["e2e_ms"]], device="cuda")
@@ -376,6 +385,95 @@ def bench_reduce(args, U, ctx, stream, barrier, rank, world, peaks, peak_src):
         "e2e": {"value": None, "unit": "GB/s", "h2d_bytes_per_step": bytes_rank, "d2h_bytes_per_step": 32},
         "bytes_all_ranks": bytes_rank * world, "e2e_ms": e2e_ms,
     }
+
+
+def _time_graph(U, ctx, stream, launch, reps):
+    import torch
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    U.upir_sync(ctx)
+    e0.record(stream)
+    for _ in range(reps):
+        launch()
+    e1.record(stream)
+    U.upir_sync(ctx)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def bench_axpy(args, U, ctx, stream, peaks, peak_src):
+    """a6 axpy y = y + a*x with a fused fp32 sum (C1 body) at n = 2^28."""
+    import torch
+    n = 1 << 28
+    x = torch.empty(n, dtype=torch.float32, device="cuda")
+    y = torch.empty(n, dtype=torch.float32, device="cuda")
+    r = torch.zeros(1, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    mx, my = U.upir_data_adopt(ctx, x), U.upir_data_adopt(ctx, y)
+    U.upir_synth_fill(ctx, mx, 0, 1)
+    U.upir_synth_fill(ctx, my, 0, 2)
+    out = {}
+    s = U.upir_spmd_launch(ctx, U.spmd_desc(148 * 4, 256))
+    for label, pol, c in (("static", U.SCHED_STATIC, 0), ("static4", U.SCHED_STATIC, 4)):
+        loop = U.loop_desc(0, n, policy=pol, chunk=c)
+        body = U.body(U.BODY_AXPY, U.F32, in0=mx, out=my, alpha=2.0)
+        red = [U.reduction(U.OP_SUM, U.F32, r)]
+        for _ in range(3):
+            U.upir_loop_exec(s, loop, body, red)
+        ms = _time_graph(U, ctx, stream, lambda: U.upir_loop_exec(s, loop, body, red), 10)
+        gbs = 12 * n / (ms / 1e3) / 1e9
+        out[label] = {"ms": ms, "GB/s": gbs, "frac": gbs / float(peaks["hbm_gbs"])}
+    U.upir_spmd_end(s)
+    U.upir_data_unmap(ctx, mx)
+    U.upir_data_unmap(ctx, my)
+    U.upir_sync(ctx)
+    return {"workload": "axpy y=y+2x + fused fp32 sum, n=2^28, 592x256, 12 B/iter", "peak_source": peak_src,
+            "bound": "hbm", **out}
+
+
+def bench_jacobi(args, U, ctx, stream, peaks, peak_src, ny=8192, nx=8192, S=100):
+    """C3: 2-D Jacobi 5-point 8192^2 fp32, 100 sweeps as one CUDA graph, tiles
+    32x256 static,1 over 296 teams, intra-tile static,4 over 256 units."""
+    import torch
+    a_t = torch.empty(ny * nx, dtype=torch.float32, device="cuda")
+    b_t = torch.empty(ny * nx, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    ma, mb = U.upir_data_adopt(ctx, a_t), U.upir_data_adopt(ctx, b_t)
+    U.upir_synth_fill(ctx, ma, 4, 5, 0, ny, nx)
+    U.upir_synth_fill(ctx, mb, 4, 5, 0, ny, nx)
+    teams = int(os.environ.get("UPIR_JACOBI_TEAMS", 296))
+    loop = U.loop_desc([1, 1], [ny - 1, nx - 1], tile=[32, 256], policy=U.SCHED_STATIC, chunk=1,
+                       distribute=U.DIST_TEAMS, inner_chunk=4)
+    s = U.upir_spmd_launch(ctx, U.spmd_desc(teams, 256))
+    bodies = [U.body(U.BODY_JACOBI5, U.F32, in0=ma, out=mb, ld=(nx, 0, 0), dims=(ny, 0, 0)),
+              U.body(U.BODY_JACOBI5, U.F32, in0=mb, out=ma, ld=(nx, 0, 0), dims=(ny, 0, 0))]
+    U.upir_graph_begin(ctx)
+    for k in range(S):
+        U.upir_loop_exec(s, loop, bodies[k % 2])
+    g = U.upir_graph_end(ctx)
+    for _ in range(2):
+        U.upir_graph_launch(ctx, g)
+    reps = max(2, min(args.steps, 5))
+    ms = _time_graph(U, ctx, stream, lambda: U.upir_graph_launch(ctx, g), reps)
+    lups = (ny - 2) * (nx - 2) * S
+    glups = lups / (ms / 1e3) / 1e9
+    gbs = 8 * lups / (ms / 1e3) / 1e9
+    U.upir_graph_destroy(g)
+    U.upir_spmd_end(s)
+    U.upir_data_unmap(ctx, ma)
+    U.upir_data_unmap(ctx, mb)
+    U.upir_sync(ctx)
+    peak = float(peaks["hbm_gbs"])
+    return {"workload": f"C3: Jacobi 5-point {ny}x{nx} fp32, {S} sweeps (one CUDA graph), tiles 32x256 "
+                        f"static,1 over {teams} teams, static,4 over 256 units",
+            "ms_per_100_sweeps": ms, "GLUP/s": glups, "bound": "hbm",
+            "roofline": {"achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+                         "algorithmic_bytes_per_lup": 8, "peak_source": peak_src,
+                         "traffic": ncu_traffic("jacobi")}}
+
+
+def bench_matmul(args, U, ctx, stream, peaks, peak_src):
+    raise RuntimeError("MATMUL body not built yet")
 
 
 def main():

@@ -44,20 +44,23 @@ def jacobi_gpu(ctx, g, S, teams=8, units=256, tile=(32, 256), policy=U.SCHED_STA
         tm = U.upir_data_map(ctx, tr, U.MAP_TOFROM)
     bodies = [U.body(U.BODY_JACOBI5, U.F32, in0=ma, out=mb, ld=(nx, 0, 0), dims=(ny, 0, 0)),
               U.body(U.BODY_JACOBI5, U.F32, in0=mb, out=ma, ld=(nx, 0, 0), dims=(ny, 0, 0))]
-    if graph:
-        U.upir_graph_begin(ctx)
-    for k in range(S):
-        U.upir_loop_exec(s, loop, bodies[k % 2], trace=tm if k == 0 else None)
-    if graph:
-        gr = U.upir_graph_end(ctx)
-        U.upir_graph_launch(ctx, gr)
-    U.upir_spmd_end(s)
-    if tm is not None:
-        U.upir_data_unmap(ctx, tm)
-    U.upir_data_unmap(ctx, mb)
-    U.upir_data_unmap(ctx, ma)
-    U.upir_sync(ctx)
-    if graph:
+    gr = None
+    try:
+        if graph:
+            U.upir_graph_begin(ctx)
+        for k in range(S):
+            U.upir_loop_exec(s, loop, bodies[k % 2], trace=tm if k == 0 else None)
+        if graph:
+            gr = U.upir_graph_end(ctx)
+            U.upir_graph_launch(ctx, gr)
+    finally:
+        U.upir_spmd_end(s)
+        if tm is not None:
+            U.upir_data_unmap(ctx, tm)
+        U.upir_data_unmap(ctx, mb)
+        U.upir_data_unmap(ctx, ma)
+        U.upir_sync(ctx)
+    if gr is not None:
         U.upir_graph_destroy(gr)
     return (b if S % 2 else a), tr
 
