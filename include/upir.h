@@ -209,8 +209,11 @@ typedef struct {
  *            out = out, fp32, row pitch ld[0] elements, dims[0] = n rows.
  *  MATMUL  : C[i][j] = sum_k A[i][k] * B[k][j] over the loop's (i, j) space
  *            (collapse 2, k sequential inside the iteration); in0 = A (M x K),
- *            in1 = B (K x N), out = C (M x N fp32), row-major, dims[0] = K.
- *            dtype BF16: bf16 inputs; F32: fp32 inputs (3xTF32).
+ *            in1 = B (K x N), out = C (M x N fp32), row-major; dims = (K, M,
+ *            N), ld = (lda, ldb, ldc) in elements (multiples of 8).  dtype
+ *            BF16: bf16 inputs, fp32 accumulation on tcgen05 tensor cores;
+ *            the tile loop (128 x 256 tiles) runs over teams of exactly 256
+ *            units (other unit counts are rejected, never clamped).
  * The element index used by a body is the induction value itself (global
  * index; for distributed maps the runtime subtracts the local offset). */
 typedef enum { UPIR_BODY_AXPY = 0, UPIR_BODY_REDUCE = 1, UPIR_BODY_JACOBI5 = 2,

@@ -1,0 +1,280 @@
+// k_matmul.cu -- the MATMUL loop body on the 5th-generation tensor cores:
+//   C[i][j] = sum_k A[i][k] * B[k][j]      (north_star; c17)
+// as a collapse(2) upir.loop over (i, j) whose tile loop (128 x 256 output
+// tiles anchored at 0) is scheduled over persistent TEAMS (CTAs); inside a
+// tile the work is cooperative (reading c24).
+//
+// sm_100a design (one CTA per SM, 256 threads):
+//   warp 0      : TMA producer -- A tile 128 x 64 (K-major) and B tile 64 x 256
+//                 (N-major, four 64-column boxes), 128-B swizzle, 4-stage
+//                 mbarrier ring (full / empty).
+//   warp 1      : one elected thread issues tcgen05.mma.cta_group::1.kind::f16
+//                 (M=128, N=256, K=16) from shared-memory descriptors into a
+//                 TMEM accumulator; tcgen05.commit frees smem stages and
+//                 signals the epilogue.  Two accumulators (2 x 256 columns)
+//                 so the epilogue of tile t overlaps the MMAs of tile t+1.
+//   warp 2      : TMEM allocator (512 columns).
+//   warps 4..7  : epilogue -- tcgen05.ld 32x32b.x32 (TMEM lane = output row)
+//                 -> registers -> fp32 C with 256-bit stores (masked at ragged
+//                 edges).
+// bf16 inputs, fp32 accumulation (kind::f16).  Ragged M/N/K are handled by
+// TMA zero fill (loads) and masks (stores).
+#include "dev_tma.cuh"
+#include "upir_internal.h"
+
+namespace upir {
+namespace {
+
+constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
+constexpr int A_BYTES = BM * BK * 2;          // 16 KiB
+constexpr int B_BYTES = BK * BN * 2;          // 32 KiB (4 boxes of 64 x 64)
+constexpr int B_BOX = 64 * BK * 2;            // 8 KiB per 64-column box
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int THREADS = 256;
+constexpr uint32_t TMEM_COLS = 512;
+
+__device__ __forceinline__ uint64_t smem_desc(const void *p, uint32_t lbo, uint32_t sbo) {
+  // tcgen05 shared-memory matrix descriptor: start >> 4 [0,14), LBO >> 4
+  // [16,30), SBO >> 4 [32,46), version 1 [46,48), base offset 0, layout
+  // SWIZZLE_128B = 2 at [61,64).
+  const uint64_t a = (uint64_t)((tma_smem(p) >> 4) & 0x3FFF);
+  return a | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) | ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) |
+         (2ull << 61);
+}
+
+// instruction descriptor: D f32, A/B bf16, A K-major, B MN-major, N=256, M=128
+constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (1u << 16) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+
+__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accum));
+}
+__device__ __forceinline__ void mma_commit(uint64_t *bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(tma_smem(bar))
+               : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() { asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory"); }
+__device__ __forceinline__ void tc_fence_after() { asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+}
+
+// Tile sequence of this team under a static tile schedule (reading c24).
+struct TileSeq {
+  int64_t cur, end, k;
+  int sched;
+  int64_t chunk, nt, p, t;
+  __device__ void init(int sched_, int64_t chunk_, int64_t nt_) {
+    sched = sched_;
+    chunk = chunk_;
+    nt = nt_;
+    p = gridDim.x;
+    t = blockIdx.x;
+    if (sched == SK_STATIC_BLOCK) {
+      const int64_t q = nt / p, r = nt % p;
+      cur = t * q + (t < r ? t : r);
+      end = cur + q + (t < r ? 1 : 0);
+      k = 0;
+    } else {
+      k = t;
+      cur = k * chunk;
+      end = min(nt, cur + chunk);
+    }
+  }
+  __device__ int64_t next() {
+    while (true) {
+      if (cur < end) return cur++;
+      if (sched == SK_STATIC_BLOCK) return -1;
+      k += p;
+      cur = k * chunk;
+      if (cur >= nt) return -1;
+      end = min(nt, cur + chunk);
+    }
+  }
+};
+
+__global__ void __launch_bounds__(THREADS, 1)
+    matmul_bf16_kernel(const __grid_constant__ MatmulArgs a, const __grid_constant__ CUtensorMap tma,
+                       const __grid_constant__ CUtensorMap tmb) {
+  extern __shared__ __align__(1024) char smem_raw[];
+  char *smem = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
+  uint64_t *empty = full + STAGES;
+  uint64_t *tfull = empty + STAGES;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  const int64_t ti0 = a.lb0 / BM, tj0 = a.lb1 / BN;
+  const int64_t ntr = (a.ub0 + BM - 1) / BM - ti0, ntc = (a.ub1 + BN - 1) / BN - tj0;
+  const int64_t nt = ntr * ntc;
+  const int KB = (int)((a.K + BK - 1) / BK);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tma);
+    tma_prefetch_desc(&tmb);
+    for (int s = 0; s < STAGES; ++s) {
+      tma_mbar_init(full + s, 1);
+      tma_mbar_init(empty + s, 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      tma_mbar_init(tfull + s, 1);
+      tma_mbar_init(tempty + s, 4);
+    }
+    tma_fence_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tma_smem(tmem_holder)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  TileSeq seq;
+  seq.init(a.sched, a.chunk, nt);
+
+  if (warp == 0) {
+    if (lane == 0) {   // ---------------- TMA producer
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t tile = seq.next(); tile >= 0; tile = seq.next()) {
+        const int m0 = (int)((ti0 + tile / ntc) * BM), n0 = (int)((tj0 + tile % ntc) * BN);
+        for (int kb = 0; kb < KB; ++kb) {
+          tma_mbar_wait(empty + stage, phase ^ 1);
+          char *sa = smem + stage * STAGE_BYTES;
+          char *sb = sa + A_BYTES;
+          tma_mbar_expect_tx(full + stage, STAGE_BYTES);
+          tma_load_2d(sa, &tma, kb * BK, m0, full + stage);
+#pragma unroll
+          for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * B_BOX, &tmb, n0 + 64 * j, kb * BK, full + stage);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {   // ---------------- MMA issuer
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int64_t tile = seq.next(); tile >= 0; tile = seq.next(), ++local) {
+        const int acc = local & 1;
+        const uint32_t acc_phase = (uint32_t)((local >> 1) & 1);
+        tma_mbar_wait(tempty + acc, acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < KB; ++kb) {
+          tma_mbar_wait(full + stage, phase);
+          tc_fence_after();
+          const char *sa = smem + stage * STAGE_BYTES;
+          const char *sb = sa + A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // A K-major SW128: advance 16 elements = 32 B inside the atom; SBO = 8 rows x 128 B
+            const uint64_t ad = smem_desc(sa + k * 32, 16, 1024);
+            // B MN-major SW128: 16 k-rows = 2 x 1024 B; LBO = 64-column box stride, SBO = 8 k-rows
+            const uint64_t bd = smem_desc(sb + k * 2048, B_BOX, 1024);
+            mma_bf16(tmem_d, ad, bd, (kb | k) != 0);
+          }
+          mma_commit(empty + stage);   // smem stage free once these MMAs complete
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        mma_commit(tfull + acc);   // accumulator ready
+      }
+    }
+  } else if (warp >= 4) {   // ---------------- epilogue
+    const int ew = warp & 3;   // TMEM lanes [32*ew, 32*ew+32)
+    int local = 0;
+    for (int64_t tile = seq.next(); tile >= 0; tile = seq.next(), ++local) {
+      const int acc = local & 1;
+      const uint32_t acc_phase = (uint32_t)((local >> 1) & 1);
+      const int64_t m0 = (ti0 + tile / ntc) * BM, n0 = (tj0 + tile % ntc) * BN;
+      tma_mbar_wait(tfull + acc, acc_phase);
+      tc_fence_after();
+      const int64_t row = m0 + 32 * ew + lane;
+      const bool row_ok = row >= a.lb0 && row < a.ub0;
+      float *crow = a.C + row * a.ldc;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((uint32_t)(32 * ew) << 16) + (uint32_t)(acc * BN + c), r);
+        const int64_t col0 = n0 + c;
+        if (!row_ok) continue;
+        if (col0 >= a.lb1 && col0 + 32 <= a.ub1) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(crow + col0 + 8 * q),
+                         "r"(r[8 * q]), "r"(r[8 * q + 1]), "r"(r[8 * q + 2]), "r"(r[8 * q + 3]), "r"(r[8 * q + 4]),
+                         "r"(r[8 * q + 5]), "r"(r[8 * q + 6]), "r"(r[8 * q + 7])
+                         : "memory");
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; ++q)
+            if (col0 + q >= a.lb1 && col0 + q < a.ub1) crow[col0 + q] = __uint_as_float(r[q]);
+        }
+      }
+      if (a.trace && ew == 0 && lane == 0) {
+        a.trace[tile] = blockIdx.x;
+        a.trace[nt + tile] = 0;
+        atomicAdd(a.trace + 2 * nt + tile, 1);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) tma_mbar_arrive(tempty + acc);
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(TMEM_COLS));
+}
+
+}  // namespace
+
+int matmul_tile_m() { return BM; }
+int matmul_tile_n() { return BN; }
+int matmul_required_units() { return THREADS; }
+
+bool matmul_encode_tmaps(void *tma, void *tmb, const void *A, const void *B, int dtype, int64_t M, int64_t N,
+                         int64_t K, int64_t lda, int64_t ldb) {
+  if (dtype != UPIR_BF16) return false;
+  return encode_tmap_2d(reinterpret_cast<CUtensorMap *>(tma), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, A, (uint64_t)K,
+                        (uint64_t)M, (uint64_t)lda * 2, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B) &&
+         encode_tmap_2d(reinterpret_cast<CUtensorMap *>(tmb), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, B, (uint64_t)N,
+                        (uint64_t)K, (uint64_t)ldb * 2, 64, BK, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+}
+
+cudaError_t launch_matmul(const MatmulArgs &a, int dtype, int teams, int units, cudaStream_t s) {
+  if (dtype != UPIR_BF16 || units != THREADS) return cudaErrorInvalidValue;
+  cudaError_t e = cudaFuncSetAttribute(matmul_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+  if (e != cudaSuccess) return e;
+  matmul_bf16_kernel<<<teams, THREADS, SMEM_BYTES, s>>>(a, *reinterpret_cast<const CUtensorMap *>(a.tmap_a),
+                                                        *reinterpret_cast<const CUtensorMap *>(a.tmap_b));
+  return cudaGetLastError();
+}
+
+}  // namespace upir

@@ -928,8 +928,59 @@ static upir_status exec_jacobi(upir_spmd s, const upir_loop_desc *l, const upir_
   c->launches++;
   return UPIR_OK;
 }
-static upir_status exec_matmul(upir_spmd, const upir_loop_desc *, const upir_body *, upir_map) {
-  return fail(UPIR_E_UNSUPPORTED, "MATMUL body not built yet");
+static upir_status exec_matmul(upir_spmd s, const upir_loop_desc *l, const upir_body *b, upir_map trace) {
+  upir_ctx c = s->ctx;
+  const upir_spmd_desc &sd = s->d;
+  upir_status st;
+  if ((st = check_map(c, b->in0, "in0 (A)")) != UPIR_OK) return st;
+  if ((st = check_map(c, b->in1, "in1 (B)")) != UPIR_OK) return st;
+  if ((st = check_map(c, b->out, "out (C)")) != UPIR_OK) return st;
+  if (b->dtype != UPIR_BF16) return fail(UPIR_E_UNSUPPORTED, "MATMUL: only bf16 inputs are built (fp32 3xTF32 is next)");
+  const int64_t K = b->dims[0], M = b->dims[1], N = b->dims[2];
+  const int64_t lda = b->ld[0], ldb = b->ld[1], ldc = b->ld[2];
+  if (M < 1 || N < 1 || K < 1) return fail(UPIR_E_INVALID, "MATMUL needs dims = (K, M, N) >= 1");
+  if (lda < K || ldb < N || ldc < N) return fail(UPIR_E_INVALID, "MATMUL leading dimensions too small");
+  if (lda % 8 || ldb % 8 || ldc % 8)
+    return fail(UPIR_E_UNSUPPORTED, "MATMUL needs lda, ldb, ldc multiples of 8 elements (TMA / 32-B stores)");
+  if ((int64_t)b->in0->dev_bytes < ((M - 1) * lda + K) * 2 || (int64_t)b->in1->dev_bytes < ((K - 1) * ldb + N) * 2 ||
+      (int64_t)b->out->dev_bytes < ((M - 1) * ldc + N) * 4)
+    return fail(UPIR_E_INVALID, "MATMUL maps smaller than the matrices they hold");
+  if (l->lb[0] < 0 || l->ub[0] > M || l->lb[1] < 0 || l->ub[1] > N)
+    return fail(UPIR_E_INVALID, "MATMUL iteration space must lie in [0,M) x [0,N)");
+  if (sd.num_units != matmul_required_units())
+    return fail(UPIR_E_INVALID, "the tcgen05 MATMUL body runs %d units per team (got %d): geometry is not clamped",
+                matmul_required_units(), sd.num_units);
+  int sk;
+  int64_t chunk;
+  if ((st = tile_sched(l, sk, chunk)) != UPIR_OK) return st;
+  if (sk == SK_DYNAMIC) return fail(UPIR_E_UNSUPPORTED, "MATMUL tile loop supports static schedules");
+  MatmulArgs a;
+  memset(&a, 0, sizeof a);
+  a.A = b->in0->dev;
+  a.B = b->in1->dev;
+  a.C = (float *)b->out->dev;
+  a.M = M; a.N = N; a.K = K;
+  a.lda = lda; a.ldb = ldb; a.ldc = ldc;
+  a.lb0 = l->lb[0]; a.ub0 = l->ub[0]; a.lb1 = l->lb[1]; a.ub1 = l->ub[1];
+  if (a.ub0 <= a.lb0 || a.ub1 <= a.lb1) return UPIR_OK;
+  a.sched = sk;
+  a.chunk = chunk;
+  const int64_t bm = matmul_tile_m(), bn = matmul_tile_n();
+  const int64_t nt = ((a.ub0 + bm - 1) / bm - a.lb0 / bm) * ((a.ub1 + bn - 1) / bn - a.lb1 / bn);
+  if (trace) {
+    if ((st = check_map(c, trace, "trace")) != UPIR_OK) return st;
+    if ((int64_t)trace->dev_bytes < 3 * nt * 4) return fail(UPIR_E_INVALID, "trace map needs 3*ntiles int32");
+    a.trace = (int32_t *)trace->dev;
+  }
+  alignas(64) CUtensorMap ta, tb;
+  if (!matmul_encode_tmaps(&ta, &tb, a.A, a.B, b->dtype, M, N, K, lda, ldb))
+    return fail(UPIR_E_CUDA, "cuTensorMapEncodeTiled failed for MATMUL operands");
+  a.tmap_a = &ta;
+  a.tmap_b = &tb;
+  cudaError_t e = launch_matmul(a, b->dtype, sd.num_teams, sd.num_units, c->compute);
+  if (e != cudaSuccess) return fail(UPIR_E_CUDA, "MATMUL launch failed: %s", cudaGetErrorString(e));
+  c->launches++;
+  return UPIR_OK;
 }
 
 // ------------------------------------------------------------------ upir.sync
