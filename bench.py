@@ -472,8 +472,36 @@ def bench_jacobi(args, U, ctx, stream, peaks, peak_src, ny=8192, nx=8192, S=100)
                          "traffic": ncu_traffic("jacobi")}}
 
 
-def bench_matmul(args, U, ctx, stream, peaks, peak_src):
-    raise RuntimeError("MATMUL body not built yet")
+def bench_matmul(args, U, ctx, stream, peaks, peak_src, n=8192):
+    """C4: dense bf16 matmul 8192^3 -> fp32 as a collapse(2) upir.loop, 128x256
+    output tiles static,1 over 148 persistent teams (tcgen05 path)."""
+    import torch
+    A = torch.empty(n * n, dtype=torch.bfloat16, device="cuda")
+    B = torch.empty(n * n, dtype=torch.bfloat16, device="cuda")
+    C = torch.empty(n * n, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    ma, mb, mc = U.upir_data_adopt(ctx, A), U.upir_data_adopt(ctx, B), U.upir_data_adopt(ctx, C)
+    U.upir_synth_fill(ctx, ma, 3, 3)
+    U.upir_synth_fill(ctx, mb, 3, 4)
+    teams = int(os.environ.get("UPIR_MATMUL_TEAMS", 148))
+    s = U.upir_spmd_launch(ctx, U.spmd_desc(teams, 256))
+    loop = U.loop_desc([0, 0], [n, n], policy=U.SCHED_STATIC, chunk=1, distribute=U.DIST_TEAMS)
+    body = U.body(U.BODY_MATMUL, U.BF16, in0=ma, in1=mb, out=mc, ld=(n, n, n), dims=(n, n, n))
+    for _ in range(3):
+        U.upir_loop_exec(s, loop, body)
+    reps = max(3, min(args.steps, 10))
+    ms = _time_graph(U, ctx, stream, lambda: U.upir_loop_exec(s, loop, body), reps)
+    U.upir_spmd_end(s)
+    for m in (mc, mb, ma):
+        U.upir_data_unmap(ctx, m)
+    U.upir_sync(ctx)
+    tflops = 2.0 * n ** 3 / (ms / 1e3) / 1e12
+    peak = float(peaks.get("bf16_tflops", 1590.0))
+    return {"workload": f"C4: bf16 matmul {n}^3 -> fp32, 128x256 tiles static,1 over {teams} teams x 256 units "
+                        "(tcgen05.mma kind::f16, TMA SW128, TMEM accumulators)",
+            "ms": ms, "TFLOP/s": tflops, "bound": "tensor",
+            "roofline": {"achieved": tflops, "peak": peak, "unit": "TFLOP/s", "frac": tflops / peak,
+                         "peak_source": peak_src + " bf16 burst", "traffic": ncu_traffic("matmul")}}
 
 
 def main():

@@ -65,7 +65,7 @@ def scaled_err(C, A, B, ref):
     return (np.abs(C.astype(np.float64) - ref) / scale).max()
 
 
-@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 512, 256), (384, 256, 1024), (200, 300, 72),
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (256, 512, 256), (384, 256, 1024), (200, 312, 72),
                                    (1, 8, 8), (130, 264, 136)])
 def test_matmul_parity(ctx, M, N, K):
     A = synth.bf16_sym_as_f32(3, 0, M * K).reshape(M, K)
