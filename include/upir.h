@@ -138,6 +138,15 @@ upir_status upir_data_device_ptr(upir_map map, void **dptr, int64_t *local_elems
 upir_status upir_dist_owned_rows(int64_t n_rows, int32_t rank, int32_t nranks,
                                  int64_t *lo, int64_t *hi);
 
+/* Halo plan of a BLOCK distribution (Fig. 7 send/recv between rank-adjacent
+ * slabs, reading c20): for rank r, rows (global indices, half-open) to send
+ * to / receive from the rank above (r-1) and below (r+1):
+ *   out[0..1] send_up [lo,hi)   out[2..3] recv_up [lo,hi)
+ *   out[4..5] send_dn [lo,hi)   out[6..7] recv_dn [lo,hi)
+ * Empty ranges are [0,0).  Host-only; upir_sync(HALO) moves exactly these. */
+upir_status upir_halo_plan(int64_t n_rows, int32_t halo_rows, int32_t rank, int32_t nranks,
+                           int64_t out[8]);
+
 /* ---- upir.spmd (Fig. 1) -------------------------------------------------
  * teams x units = CUDA grid x block (Figs. 11-12): team = CTA,
  * unit = thread, flat unit id g = team * num_units + unit.

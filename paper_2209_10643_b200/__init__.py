@@ -159,6 +159,13 @@ def upir_dist_owned_rows(n_rows, rank, nranks):
     return lo.value, hi.value
 
 
+def upir_halo_plan(n_rows, halo_rows, rank, nranks):
+    out = (ctypes.c_int64 * 8)()
+    check(lib().upir_halo_plan(n_rows, halo_rows, rank, nranks, out))
+    return {"send_up": (out[0], out[1]), "recv_up": (out[2], out[3]),
+            "send_dn": (out[4], out[5]), "recv_dn": (out[6], out[7])}
+
+
 def upir_spmd_launch(ctx, desc):
     s = ctypes.c_void_p()
     check(lib().upir_spmd_launch(ctx, ctypes.byref(desc), ctypes.byref(s)))

@@ -72,6 +72,7 @@ _SIGS = {
     "upir_data_update": (i32, [vp, vp, ctypes.c_int]),
     "upir_data_device_ptr": (i32, [vp, ctypes.POINTER(vp), ctypes.POINTER(i64), ctypes.POINTER(i64)]),
     "upir_dist_owned_rows": (i32, [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
+    "upir_halo_plan": (i32, [i64, i32, i32, i32, ctypes.POINTER(i64)]),
     "upir_spmd_launch": (i32, [vp, ctypes.POINTER(SpmdDesc), ctypes.POINTER(vp)]),
     "upir_spmd_end": (i32, [vp]),
     "upir_loop_exec": (i32, [vp, ctypes.POINTER(LoopDesc), ctypes.POINTER(Body), ctypes.POINTER(Reduction),

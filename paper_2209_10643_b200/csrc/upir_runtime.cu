@@ -245,6 +245,33 @@ extern "C" upir_status upir_dist_owned_rows(int64_t n_rows, int32_t rank, int32_
   return UPIR_OK;
 }
 
+extern "C" upir_status upir_halo_plan(int64_t n_rows, int32_t halo, int32_t rank, int32_t nranks, int64_t out[8]) {
+  if (!out || halo < 0) return fail(UPIR_E_INVALID, "bad halo plan arguments");
+  int64_t lo, hi;
+  upir_status st = upir_dist_owned_rows(n_rows, rank, nranks, &lo, &hi);
+  if (st != UPIR_OK) return st;
+  for (int i = 0; i < 8; ++i) out[i] = 0;
+  if (rank > 0) {
+    int64_t ulo, uhi;
+    upir_dist_owned_rows(n_rows, rank - 1, nranks, &ulo, &uhi);
+    const int64_t s = std::min<int64_t>(halo, std::min(hi - lo, uhi - ulo));
+    if (s > 0) {
+      out[0] = lo; out[1] = lo + s;        // my first owned rows -> up's bottom halo
+      out[2] = lo - s; out[3] = lo;        // up's last owned rows -> my top halo
+    }
+  }
+  if (rank < nranks - 1) {
+    int64_t dlo, dhi;
+    upir_dist_owned_rows(n_rows, rank + 1, nranks, &dlo, &dhi);
+    const int64_t s = std::min<int64_t>(halo, std::min(hi - lo, dhi - dlo));
+    if (s > 0) {
+      out[4] = hi - s; out[5] = hi;        // my last owned rows -> down's top halo
+      out[6] = hi; out[7] = hi + s;        // down's first owned rows -> my bottom halo
+    }
+  }
+  return UPIR_OK;
+}
+
 static upir_status layout_map(upir_ctx c, upir_map m, size_t bytes, const upir_dist *dist) {
   if (dist && dist->pattern == UPIR_PATTERN_BLOCK) {
     if (dist->n_rows < 1 || dist->row_elems < 1 || dist->elem_bytes < 1 || dist->halo_rows < 0)
@@ -1053,22 +1080,21 @@ static upir_status halo_exchange(upir_ctx c, upir_map m) {
   if (m->dist.pattern != UPIR_PATTERN_BLOCK || m->dist.halo_rows < 1)
     return fail(UPIR_E_INVALID, "HALO needs a BLOCK-distributed map with halo_rows >= 1");
   if (c->nranks == 1) return UPIR_OK;
+  int64_t plan[8];
+  upir_status st = upir_halo_plan(m->dist.n_rows, m->dist.halo_rows, c->rank, c->nranks, plan);
+  if (st != UPIR_OK) return st;
   const int64_t rb = m->dist.row_elems * m->dist.elem_bytes;
-  const int64_t h = m->dist.halo_rows;
   char *base = (char *)m->dev;
-  const int up = c->rank - 1, dn = c->rank + 1;
-  // Fig. 7 send/recv with rank units: my first owned rows -> up's bottom halo,
-  // my last owned rows -> dn's top halo; receive the mirror images.
+  auto at = [&](int64_t row) { return base + (row - m->loc_row_lo) * rb; };
+  // Fig. 7 send/recv with rank units, in stream order before the next sweep
   NCCL_TRY(ncclGroupStart());
-  if (up >= 0) {
-    const int64_t nh = std::min(h, m->row_lo - m->loc_row_lo);
-    NCCL_TRY(ncclSend(base + (m->row_lo - m->loc_row_lo) * rb, (size_t)(nh * rb), ncclChar, up, c->comm, c->compute));
-    NCCL_TRY(ncclRecv(base + (m->row_lo - nh - m->loc_row_lo) * rb, (size_t)(nh * rb), ncclChar, up, c->comm, c->compute));
+  if (plan[1] > plan[0]) {
+    NCCL_TRY(ncclSend(at(plan[0]), (size_t)((plan[1] - plan[0]) * rb), ncclChar, c->rank - 1, c->comm, c->compute));
+    NCCL_TRY(ncclRecv(at(plan[2]), (size_t)((plan[3] - plan[2]) * rb), ncclChar, c->rank - 1, c->comm, c->compute));
   }
-  if (dn < c->nranks) {
-    const int64_t nh = std::min(h, m->loc_row_hi - m->row_hi);
-    NCCL_TRY(ncclSend(base + (m->row_hi - nh - m->loc_row_lo) * rb, (size_t)(nh * rb), ncclChar, dn, c->comm, c->compute));
-    NCCL_TRY(ncclRecv(base + (m->row_hi - m->loc_row_lo) * rb, (size_t)(nh * rb), ncclChar, dn, c->comm, c->compute));
+  if (plan[5] > plan[4]) {
+    NCCL_TRY(ncclSend(at(plan[4]), (size_t)((plan[5] - plan[4]) * rb), ncclChar, c->rank + 1, c->comm, c->compute));
+    NCCL_TRY(ncclRecv(at(plan[6]), (size_t)((plan[7] - plan[6]) * rb), ncclChar, c->rank + 1, c->comm, c->compute));
   }
   NCCL_TRY(ncclGroupEnd());
   return UPIR_OK;
