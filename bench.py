@@ -442,7 +442,8 @@ def bench_jacobi(args, U, ctx, stream, peaks, peak_src, ny=8192, nx=8192, S=100)
     U.upir_synth_fill(ctx, ma, 4, 5, 0, ny, nx)
     U.upir_synth_fill(ctx, mb, 4, 5, 0, ny, nx)
     teams = int(os.environ.get("UPIR_JACOBI_TEAMS", 296))
-    loop = U.loop_desc([1, 1], [ny - 1, nx - 1], tile=[32, 256], policy=U.SCHED_STATIC, chunk=1,
+    bm, bn = (int(v) for v in os.environ.get("UPIR_JACOBI_TILE", "32x256").split("x"))
+    loop = U.loop_desc([1, 1], [ny - 1, nx - 1], tile=[bm, bn], policy=U.SCHED_STATIC, chunk=1,
                        distribute=U.DIST_TEAMS, inner_chunk=4)
     s = U.upir_spmd_launch(ctx, U.spmd_desc(teams, 256))
     bodies = [U.body(U.BODY_JACOBI5, U.F32, in0=ma, out=mb, ld=(nx, 0, 0), dims=(ny, 0, 0)),
@@ -464,7 +465,7 @@ def bench_jacobi(args, U, ctx, stream, peaks, peak_src, ny=8192, nx=8192, S=100)
     U.upir_data_unmap(ctx, mb)
     U.upir_sync(ctx)
     peak = float(peaks["hbm_gbs"])
-    return {"workload": f"C3: Jacobi 5-point {ny}x{nx} fp32, {S} sweeps (one CUDA graph), tiles 32x256 "
+    return {"workload": f"C3: Jacobi 5-point {ny}x{nx} fp32, {S} sweeps (one CUDA graph), tiles {bm}x{bn} "
                         f"static,1 over {teams} teams, static,4 over 256 units",
             "ms_per_100_sweeps": ms, "GLUP/s": glups, "bound": "hbm",
             "roofline": {"achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,

@@ -220,9 +220,11 @@ typedef struct {
  *            (collapse 2, k sequential inside the iteration); in0 = A (M x K),
  *            in1 = B (K x N), out = C (M x N fp32), row-major; dims = (K, M,
  *            N), ld = (lda, ldb, ldc) in elements (multiples of 8).  dtype
- *            BF16: bf16 inputs, fp32 accumulation on tcgen05 tensor cores;
- *            the tile loop (128 x 256 tiles) runs over teams of exactly 256
- *            units (other unit counts are rejected, never clamped).
+ *            BF16: bf16 inputs, fp32 accumulation on tcgen05 tensor cores,
+ *            teams of exactly 256 units; F32: fp32 inputs via 3xTF32
+ *            (kind::tf32, hi/lo split in shared memory), teams of exactly 384
+ *            units.  The tile loop (128 x 256 tiles) runs over the teams;
+ *            other unit counts are rejected, never clamped.
  * The element index used by a body is the induction value itself (global
  * index; for distributed maps the runtime subtracts the local offset). */
 typedef enum { UPIR_BODY_AXPY = 0, UPIR_BODY_REDUCE = 1, UPIR_BODY_JACOBI5 = 2,

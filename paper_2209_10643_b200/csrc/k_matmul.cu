@@ -4,7 +4,7 @@
 // tiles anchored at 0) is scheduled over persistent TEAMS (CTAs); inside a
 // tile the work is cooperative (reading c24).
 //
-// sm_100a design (one CTA per SM, 256 threads):
+// sm_100a design (one CTA per SM, 256 threads for bf16, 384 for fp32):
 //   warp 0      : TMA producer -- A tile 128 x 64 (K-major) and B tile 64 x 256
 //                 (N-major, four 64-column boxes), 128-B swizzle, 4-stage
 //                 mbarrier ring (full / empty).
@@ -17,22 +17,50 @@
 //   warps 4..7  : epilogue -- tcgen05.ld 32x32b.x32 (TMEM lane = output row)
 //                 -> registers -> fp32 C with 256-bit stores (masked at ragged
 //                 edges).
-// bf16 inputs, fp32 accumulation (kind::f16).  Ragged M/N/K are handled by
-// TMA zero fill (loads) and masks (stores).
+// bf16 inputs, fp32 accumulation (kind::f16); fp32 inputs via 3xTF32
+// (kind::tf32, warps 8..11 split each staged tile into hi/lo in shared memory).
+// Ragged M/N/K are handled by TMA zero fill (loads) and masks (stores).
 #include "dev_tma.cuh"
 #include "upir_internal.h"
 
 namespace upir {
 namespace {
 
-constexpr int BM = 128, BN = 256, BK = 64, STAGES = 4;
-constexpr int A_BYTES = BM * BK * 2;          // 16 KiB
-constexpr int B_BYTES = BK * BN * 2;          // 32 KiB (4 boxes of 64 x 64)
-constexpr int B_BOX = 64 * BK * 2;            // 8 KiB per 64-column box
-constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
-constexpr int THREADS = 256;
+// Per-dtype configuration.  BF16: kind::f16, K = 16 per MMA, 64-deep stages.
+// F32 (3xTF32): kind::tf32, K = 8 per MMA, 32-deep stages; each fp32 operand
+// tile is split in shared memory into hi = rna_tf32(x) and lo = x - hi by 4
+// transform warps, and D += lo_a*hi_b + hi_a*lo_b + hi_a*hi_b (small terms
+// first), which keeps the fp32 result within the 1e-5 bar.
+template <int DT>
+struct Cfg;
+template <>
+struct Cfg<UPIR_BF16> {
+  static constexpr int ES = 2, BK = 64, STAGES = 4, THREADS = 256, KSTEP = 16;
+  static constexpr int NSPLIT = 1;   // operand copies per stage (hi only)
+  static constexpr uint32_t FMT = 1;  // BF16
+};
+template <>
+struct Cfg<UPIR_F32> {
+  static constexpr int ES = 4, BK = 32, STAGES = 2, THREADS = 384, KSTEP = 8;
+  static constexpr int NSPLIT = 2;   // hi and lo copies
+  static constexpr uint32_t FMT = 2;  // TF32
+};
+
+constexpr int BM = 128, BN = 256;
 constexpr uint32_t TMEM_COLS = 512;
+
+template <int DT>
+struct MLayout {
+  using C = Cfg<DT>;
+  static constexpr int A_BYTES = BM * C::BK * C::ES;              // one copy of the A tile
+  static constexpr int BOXN = 128 / C::ES;                        // N columns per 128-B swizzle atom
+  static constexpr int B_BOX = BOXN * C::BK * C::ES;              // one B box (BOXN x BK)
+  static constexpr int B_BYTES = C::BK * BN * C::ES;            // B tile (BN / BOXN boxes)
+  static constexpr int COPY = A_BYTES + B_BYTES;                  // A + B of one split copy
+  static constexpr int STAGE = COPY * C::NSPLIT;
+  static constexpr int SMEM = C::STAGES * STAGE + 1024 + 256;
+  static constexpr int TX = COPY;                                 // bytes TMA delivers per stage
+};
 
 __device__ __forceinline__ uint64_t smem_desc(const void *p, uint32_t lbo, uint32_t sbo) {
   // tcgen05 shared-memory matrix descriptor: start >> 4 [0,14), LBO >> 4
@@ -43,15 +71,25 @@ __device__ __forceinline__ uint64_t smem_desc(const void *p, uint32_t lbo, uint3
          (2ull << 61);
 }
 
-// instruction descriptor: D f32, A/B bf16, A K-major, B MN-major, N=256, M=128
-constexpr uint32_t IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (1u << 16) | ((uint32_t)(BN >> 3) << 17) |
-                           ((uint32_t)(BM >> 4) << 24);
+// instruction descriptor: D f32, A/B fmt, A K-major, B MN-major, N=256, M=128
+template <int DT>
+constexpr uint32_t idesc() {
+  return (1u << 4) | (Cfg<DT>::FMT << 7) | (Cfg<DT>::FMT << 10) | (0u << 15) | (1u << 16) |
+         ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
 
-__device__ __forceinline__ void mma_bf16(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
-  asm volatile(
-      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-      " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
-      "l"(adesc), "l"(bdesc), "r"(IDESC), "r"(accum));
+template <int DT>
+__device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+  if constexpr (DT == UPIR_BF16)
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc<DT>()), "r"(accum));
+  else
+    asm volatile(
+        "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+        " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc<DT>()), "r"(accum));
 }
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(tma_smem(bar))
@@ -106,14 +144,19 @@ struct TileSeq {
   }
 };
 
-__global__ void __launch_bounds__(THREADS, 1)
-    matmul_bf16_kernel(const __grid_constant__ MatmulArgs a, const __grid_constant__ CUtensorMap tma,
-                       const __grid_constant__ CUtensorMap tmb) {
+template <int DT>
+__global__ void __launch_bounds__(Cfg<DT>::THREADS, 1)
+    matmul_kernel(const __grid_constant__ MatmulArgs a, const __grid_constant__ CUtensorMap tma,
+                  const __grid_constant__ CUtensorMap tmb) {
+  using C = Cfg<DT>;
+  using L = MLayout<DT>;
+  constexpr int BK = C::BK, STAGES = C::STAGES;
   extern __shared__ __align__(1024) char smem_raw[];
   char *smem = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
-  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * STAGE_BYTES);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * L::STAGE);
   uint64_t *empty = full + STAGES;
-  uint64_t *tfull = empty + STAGES;
+  uint64_t *ready = empty + STAGES;          // F32: split done
+  uint64_t *tfull = ready + STAGES;
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -129,6 +172,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int s = 0; s < STAGES; ++s) {
       tma_mbar_init(full + s, 1);
       tma_mbar_init(empty + s, 1);
+      tma_mbar_init(ready + s, 4);
     }
     for (int s = 0; s < 2; ++s) {
       tma_mbar_init(tfull + s, 1);
@@ -150,19 +194,20 @@ __global__ void __launch_bounds__(THREADS, 1)
   seq.init(a.sched, a.chunk, nt);
 
   if (warp == 0) {
-    if (lane == 0) {   // ---------------- TMA producer
+    if (lane == 0) {   // ---------------- TMA producer (raw operand tiles -> copy 0)
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t tile = seq.next(); tile >= 0; tile = seq.next()) {
         const int m0 = (int)((ti0 + tile / ntc) * BM), n0 = (int)((tj0 + tile % ntc) * BN);
         for (int kb = 0; kb < KB; ++kb) {
           tma_mbar_wait(empty + stage, phase ^ 1);
-          char *sa = smem + stage * STAGE_BYTES;
-          char *sb = sa + A_BYTES;
-          tma_mbar_expect_tx(full + stage, STAGE_BYTES);
+          char *sa = smem + stage * L::STAGE;
+          char *sb = sa + L::A_BYTES;
+          tma_mbar_expect_tx(full + stage, L::TX);
           tma_load_2d(sa, &tma, kb * BK, m0, full + stage);
 #pragma unroll
-          for (int j = 0; j < BN / 64; ++j) tma_load_2d(sb + j * B_BOX, &tmb, n0 + 64 * j, kb * BK, full + stage);
+          for (int j = 0; j < BN / L::BOXN; ++j)
+            tma_load_2d(sb + j * L::B_BOX, &tmb, n0 + L::BOXN * j, kb * BK, full + stage);
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -182,17 +227,26 @@ __global__ void __launch_bounds__(THREADS, 1)
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + (uint32_t)(acc * BN);
         for (int kb = 0; kb < KB; ++kb) {
-          tma_mbar_wait(full + stage, phase);
+          if constexpr (DT == UPIR_BF16) tma_mbar_wait(full + stage, phase);
+          else tma_mbar_wait(ready + stage, phase);
           tc_fence_after();
-          const char *sa = smem + stage * STAGE_BYTES;
-          const char *sb = sa + A_BYTES;
+          const char *hi = smem + stage * L::STAGE;
 #pragma unroll
-          for (int k = 0; k < BK / 16; ++k) {
-            // A K-major SW128: advance 16 elements = 32 B inside the atom; SBO = 8 rows x 128 B
-            const uint64_t ad = smem_desc(sa + k * 32, 16, 1024);
-            // B MN-major SW128: 16 k-rows = 2 x 1024 B; LBO = 64-column box stride, SBO = 8 k-rows
-            const uint64_t bd = smem_desc(sb + k * 2048, B_BOX, 1024);
-            mma_bf16(tmem_d, ad, bd, (kb | k) != 0);
+          for (int k = 0; k < BK / C::KSTEP; ++k) {
+            // A K-major SW128: K step = 32 B inside the atom; SBO = 8 rows x 128 B.
+            // B MN-major SW128: K step = KSTEP k-rows (x 128 B); LBO = box stride, SBO = 8 k-rows.
+            const uint64_t ah = smem_desc(hi + k * 32, 16, 1024);
+            const uint64_t bh = smem_desc(hi + L::A_BYTES + k * C::KSTEP * 128, L::B_BOX, 1024);
+            if constexpr (DT == UPIR_BF16) {
+              mma<DT>(tmem_d, ah, bh, (kb | k) != 0);
+            } else {
+              const char *lo = hi + L::COPY;
+              const uint64_t al = smem_desc(lo + k * 32, 16, 1024);
+              const uint64_t bl = smem_desc(lo + L::A_BYTES + k * C::KSTEP * 128, L::B_BOX, 1024);
+              mma<DT>(tmem_d, al, bh, (kb | k) != 0);   // lo_a * hi_b
+              mma<DT>(tmem_d, ah, bl, 1);               // hi_a * lo_b
+              mma<DT>(tmem_d, ah, bh, 1);               // hi_a * hi_b
+            }
           }
           mma_commit(empty + stage);   // smem stage free once these MMAs complete
           if (++stage == STAGES) {
@@ -203,7 +257,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         mma_commit(tfull + acc);   // accumulator ready
       }
     }
-  } else if (warp >= 4) {   // ---------------- epilogue
+  } else if (warp >= 4 && warp < 8) {   // ---------------- epilogue
     const int ew = warp & 3;   // TMEM lanes [32*ew, 32*ew+32)
     int local = 0;
     for (int64_t tile = seq.next(); tile >= 0; tile = seq.next(), ++local) {
@@ -243,6 +297,39 @@ __global__ void __launch_bounds__(THREADS, 1)
       __syncwarp();
       if (lane == 0) tma_mbar_arrive(tempty + acc);
     }
+  } else if constexpr (DT == UPIR_F32) {
+    if (warp >= 8) {   // ---------------- 3xTF32 split: copy0 <- hi, copy1 <- lo (elementwise)
+      const int tid = threadIdx.x - 256;   // 0..127
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t tile = seq.next(); tile >= 0; tile = seq.next()) {
+        for (int kb = 0; kb < KB; ++kb) {
+          tma_mbar_wait(full + stage, phase);
+          float4 *hi = reinterpret_cast<float4 *>(smem + stage * L::STAGE);
+          float4 *lo = reinterpret_cast<float4 *>(smem + stage * L::STAGE + L::COPY);
+          for (int v = tid; v < L::COPY / 16; v += 128) {
+            float4 x = hi[v], h, l;
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&h.x)) : "f"(x.x));
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&h.y)) : "f"(x.y));
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&h.z)) : "f"(x.z));
+            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&h.w)) : "f"(x.w));
+            l.x = __fsub_rn(x.x, h.x);
+            l.y = __fsub_rn(x.y, h.y);
+            l.z = __fsub_rn(x.z, h.z);
+            l.w = __fsub_rn(x.w, h.w);
+            hi[v] = h;
+            lo[v] = l;
+          }
+          tma_fence_proxy();   // generic smem writes -> visible to the tensor-core (async) proxy
+          __syncwarp();
+          if (lane == 0) tma_mbar_arrive(ready + stage);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
   }
   tc_fence_before();
   __syncthreads();
@@ -255,26 +342,34 @@ __global__ void __launch_bounds__(THREADS, 1)
 
 int matmul_tile_m() { return BM; }
 int matmul_tile_n() { return BN; }
-int matmul_required_units() { return THREADS; }
+int matmul_required_units(int dtype) { return dtype == UPIR_F32 ? Cfg<UPIR_F32>::THREADS : Cfg<UPIR_BF16>::THREADS; }
 
 bool matmul_encode_tmaps(void *tma, void *tmb, const void *A, const void *B, int dtype, int64_t M, int64_t N,
                          int64_t K, int64_t lda, int64_t ldb) {
-  if (dtype != UPIR_BF16) return false;
-  return encode_tmap_2d(reinterpret_cast<CUtensorMap *>(tma), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, A, (uint64_t)K,
-                        (uint64_t)M, (uint64_t)lda * 2, BK, BM, CU_TENSOR_MAP_SWIZZLE_128B,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B) &&
-         encode_tmap_2d(reinterpret_cast<CUtensorMap *>(tmb), CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, B, (uint64_t)N,
-                        (uint64_t)K, (uint64_t)ldb * 2, 64, BK, CU_TENSOR_MAP_SWIZZLE_128B,
-                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+  const bool f32 = dtype == UPIR_F32;
+  const CUtensorMapDataType dt = f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+  const int es = f32 ? 4 : 2, bk = f32 ? Cfg<UPIR_F32>::BK : Cfg<UPIR_BF16>::BK, boxn = 128 / es;
+  return encode_tmap_2d(reinterpret_cast<CUtensorMap *>(tma), dt, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda * es,
+                        bk, BM, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) &&
+         encode_tmap_2d(reinterpret_cast<CUtensorMap *>(tmb), dt, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb * es,
+                        boxn, bk, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+}
+
+template <int DT>
+static cudaError_t launch_dt(const MatmulArgs &a, int teams, cudaStream_t s) {
+  using L = MLayout<DT>;
+  cudaError_t e = cudaFuncSetAttribute(matmul_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+  if (e != cudaSuccess) return e;
+  matmul_kernel<DT><<<teams, Cfg<DT>::THREADS, L::SMEM, s>>>(a, *reinterpret_cast<const CUtensorMap *>(a.tmap_a),
+                                                             *reinterpret_cast<const CUtensorMap *>(a.tmap_b));
+  return cudaGetLastError();
 }
 
 cudaError_t launch_matmul(const MatmulArgs &a, int dtype, int teams, int units, cudaStream_t s) {
-  if (dtype != UPIR_BF16 || units != THREADS) return cudaErrorInvalidValue;
-  cudaError_t e = cudaFuncSetAttribute(matmul_bf16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-  if (e != cudaSuccess) return e;
-  matmul_bf16_kernel<<<teams, THREADS, SMEM_BYTES, s>>>(a, *reinterpret_cast<const CUtensorMap *>(a.tmap_a),
-                                                        *reinterpret_cast<const CUtensorMap *>(a.tmap_b));
-  return cudaGetLastError();
+  if (units != matmul_required_units(dtype)) return cudaErrorInvalidValue;
+  if (dtype == UPIR_BF16) return launch_dt<UPIR_BF16>(a, teams, s);
+  if (dtype == UPIR_F32) return launch_dt<UPIR_F32>(a, teams, s);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace upir

@@ -111,6 +111,6 @@ bool matmul_encode_tmaps(void *tma, void *tmb, const void *A, const void *B, int
                          int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb);
 int matmul_tile_m();
 int matmul_tile_n();
-int matmul_required_units();
+int matmul_required_units(int dtype);
 
 }  // namespace upir

@@ -962,21 +962,22 @@ static upir_status exec_matmul(upir_spmd s, const upir_loop_desc *l, const upir_
   if ((st = check_map(c, b->in0, "in0 (A)")) != UPIR_OK) return st;
   if ((st = check_map(c, b->in1, "in1 (B)")) != UPIR_OK) return st;
   if ((st = check_map(c, b->out, "out (C)")) != UPIR_OK) return st;
-  if (b->dtype != UPIR_BF16) return fail(UPIR_E_UNSUPPORTED, "MATMUL: only bf16 inputs are built (fp32 3xTF32 is next)");
   const int64_t K = b->dims[0], M = b->dims[1], N = b->dims[2];
   const int64_t lda = b->ld[0], ldb = b->ld[1], ldc = b->ld[2];
   if (M < 1 || N < 1 || K < 1) return fail(UPIR_E_INVALID, "MATMUL needs dims = (K, M, N) >= 1");
   if (lda < K || ldb < N || ldc < N) return fail(UPIR_E_INVALID, "MATMUL leading dimensions too small");
   if (lda % 8 || ldb % 8 || ldc % 8)
     return fail(UPIR_E_UNSUPPORTED, "MATMUL needs lda, ldb, ldc multiples of 8 elements (TMA / 32-B stores)");
-  if ((int64_t)b->in0->dev_bytes < ((M - 1) * lda + K) * 2 || (int64_t)b->in1->dev_bytes < ((K - 1) * ldb + N) * 2 ||
+  const int64_t es = b->dtype == UPIR_F32 ? 4 : 2;
+  if (es == 4 && (lda % 4 || ldb % 4)) return fail(UPIR_E_UNSUPPORTED, "fp32 MATMUL needs lda, ldb multiples of 4");
+  if ((int64_t)b->in0->dev_bytes < ((M - 1) * lda + K) * es || (int64_t)b->in1->dev_bytes < ((K - 1) * ldb + N) * es ||
       (int64_t)b->out->dev_bytes < ((M - 1) * ldc + N) * 4)
     return fail(UPIR_E_INVALID, "MATMUL maps smaller than the matrices they hold");
   if (l->lb[0] < 0 || l->ub[0] > M || l->lb[1] < 0 || l->ub[1] > N)
     return fail(UPIR_E_INVALID, "MATMUL iteration space must lie in [0,M) x [0,N)");
-  if (sd.num_units != matmul_required_units())
-    return fail(UPIR_E_INVALID, "the tcgen05 MATMUL body runs %d units per team (got %d): geometry is not clamped",
-                matmul_required_units(), sd.num_units);
+  if (sd.num_units != matmul_required_units(b->dtype))
+    return fail(UPIR_E_INVALID, "the tcgen05 MATMUL body runs %d units per team for this dtype (got %d): geometry is not clamped",
+                matmul_required_units(b->dtype), sd.num_units);
   int sk;
   int64_t chunk;
   if ((st = tile_sched(l, sk, chunk)) != UPIR_OK) return st;

@@ -29,11 +29,15 @@ def to_bf16_bits(x):
     return (x.view(np.uint32) >> 16).astype(np.uint16)
 
 
-def matmul_gpu(ctx, A, B, teams=148, policy=U.SCHED_STATIC, chunk=1, space=None, trace=False, C0=None):
+def matmul_gpu(ctx, A, B, teams=148, policy=U.SCHED_STATIC, chunk=1, space=None, trace=False, C0=None,
+               dtype=U.BF16):
     M, K = A.shape
     _, N = B.shape
-    a = to_bf16_bits(A)
-    b = to_bf16_bits(B)
+    if dtype == U.BF16:
+        a, b = to_bf16_bits(A), to_bf16_bits(B)
+    else:
+        a, b = np.ascontiguousarray(A, np.float32), np.ascontiguousarray(B, np.float32)
+    units = 256 if dtype == U.BF16 else 384
     C = np.zeros((M, N), np.float32) if C0 is None else C0.copy()
     ma = U.upir_data_map(ctx, a, U.MAP_TO)
     mb = U.upir_data_map(ctx, b, U.MAP_TO)
@@ -44,10 +48,10 @@ def matmul_gpu(ctx, A, B, teams=148, policy=U.SCHED_STATIC, chunk=1, space=None,
         nt = ((ub0 + 127) // 128 - lb0 // 128) * ((ub1 + 255) // 256 - lb1 // 256)
         tr = np.zeros(3 * nt, np.int32)
         tm = U.upir_data_map(ctx, tr, U.MAP_TOFROM)
-    s = U.upir_spmd_launch(ctx, U.spmd_desc(teams, 256))
+    s = U.upir_spmd_launch(ctx, U.spmd_desc(teams, units))
     try:
         U.upir_loop_exec(s, U.loop_desc([lb0, lb1], [ub0, ub1], policy=policy, chunk=chunk, distribute=U.DIST_TEAMS),
-                         U.body(U.BODY_MATMUL, U.BF16, in0=ma, in1=mb, out=mc, ld=(K, N, N), dims=(K, M, N)),
+                         U.body(U.BODY_MATMUL, dtype, in0=ma, in1=mb, out=mc, ld=(K, N, N), dims=(K, M, N)),
                          trace=tm)
     finally:
         U.upir_spmd_end(s)
@@ -143,6 +147,50 @@ def test_matmul_rejects_bad_geometry(ctx):
             U.upir_loop_exec(s, U.loop_desc([0, 0], [128, 256], distribute=U.DIST_TEAMS),
                              U.body(U.BODY_MATMUL, U.BF16, in0=ma, in1=ma, out=ma, ld=(64, 256, 256),
                                     dims=(64, 128, 256)))
+        U.upir_spmd_end(s)
+    finally:
+        U.upir_data_unmap(ctx, ma)
+
+
+# ---- fp32 inputs: 3xTF32 on kind::tf32 ------------------------------------------
+@pytest.mark.parametrize("M,N,K", [(128, 256, 32), (256, 512, 512), (200, 312, 72), (130, 264, 4096)])
+def test_matmul_f32_parity(ctx, M, N, K):
+    A = synth.f32_sym(3, 0, M * K).reshape(M, K)
+    B = synth.f32_sym(4, 0, K * N).reshape(K, N)
+    C, _ = matmul_gpu(ctx, A, B, dtype=U.F32)
+    assert scaled_err(C, A, B, oracle.matmul(A, B)) <= 1e-5
+
+
+def test_matmul_f32_small_integers_bit_exact(ctx):
+    rng = np.random.default_rng(11)
+    M, N, K = 256, 256, 256
+    A = rng.integers(-2, 3, (M, K)).astype(np.float32)
+    B = rng.integers(-2, 3, (K, N)).astype(np.float32)
+    C, _ = matmul_gpu(ctx, A, B, dtype=U.F32)
+    assert (C == oracle.matmul(A, B)).all()
+
+
+@pytest.mark.parametrize("teams,chunk", [(1, 1), (148, 0), (5, 2)])
+def test_matmul_f32_schedules_and_trace(ctx, teams, chunk):
+    M, N, K = 384, 512, 96
+    A = synth.f32_sym(3, 0, M * K).reshape(M, K)
+    B = synth.f32_sym(4, 0, K * N).reshape(K, N)
+    C, tr = matmul_gpu(ctx, A, B, teams=teams, chunk=chunk, trace=True, dtype=U.F32)
+    assert scaled_err(C, A, B, oracle.matmul(A, B)) <= 1e-5
+    nt = len(tr) // 3
+    assert (tr[2 * nt:] == 1).all()
+    assert (tr[:nt] == oracle.tile_owner(M, N, 128, 256, oracle.STATIC, chunk, teams)).all()
+
+
+def test_matmul_f32_needs_384_units(ctx):
+    a = np.zeros((128, 32), np.float32)
+    ma = U.upir_data_map(ctx, a, U.MAP_TO)
+    try:
+        s = U.upir_spmd_launch(ctx, U.spmd_desc(4, 256))
+        with pytest.raises(U.UpirError):
+            U.upir_loop_exec(s, U.loop_desc([0, 0], [128, 32], distribute=U.DIST_TEAMS),
+                             U.body(U.BODY_MATMUL, U.F32, in0=ma, in1=ma, out=ma, ld=(32, 32, 32),
+                                    dims=(32, 128, 32)))
         U.upir_spmd_end(s)
     finally:
         U.upir_data_unmap(ctx, ma)
