@@ -496,11 +496,33 @@ def bench_matmul(args, U, ctx, stream, peaks, peak_src, n=8192):
     for m in (mc, mb, ma):
         U.upir_data_unmap(ctx, m)
     U.upir_sync(ctx)
+    del A, B
     tflops = 2.0 * n ** 3 / (ms / 1e3) / 1e12
     peak = float(peaks.get("bf16_tflops", 1590.0))
+    # fp32 inputs (3xTF32 on kind::tf32): 384 units per team
+    A32 = torch.empty(n * n, dtype=torch.float32, device="cuda")
+    B32 = torch.empty(n * n, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    ma32, mb32, mc = U.upir_data_adopt(ctx, A32), U.upir_data_adopt(ctx, B32), U.upir_data_adopt(ctx, C)
+    U.upir_synth_fill(ctx, ma32, 1, 3)
+    U.upir_synth_fill(ctx, mb32, 1, 4)
+    s32 = U.upir_spmd_launch(ctx, U.spmd_desc(teams, 384))
+    body32 = U.body(U.BODY_MATMUL, U.F32, in0=ma32, in1=mb32, out=mc, ld=(n, n, n), dims=(n, n, n))
+    U.upir_loop_exec(s32, loop, body32)
+    ms32 = _time_graph(U, ctx, stream, lambda: U.upir_loop_exec(s32, loop, body32), 3)
+    U.upir_spmd_end(s32)
+    for m in (mc, mb32, ma32):
+        U.upir_data_unmap(ctx, m)
+    U.upir_sync(ctx)
+    del A32, B32
+    tf32_peak = peak / 2.0      # tf32 dense = 1/2 of bf16 (nominal ratio) x measured bf16
+    fp32_tflops = 2.0 * n ** 3 / (ms32 / 1e3) / 1e12
     return {"workload": f"C4: bf16 matmul {n}^3 -> fp32, 128x256 tiles static,1 over {teams} teams x 256 units "
                         "(tcgen05.mma kind::f16, TMA SW128, TMEM accumulators)",
             "ms": ms, "TFLOP/s": tflops, "bound": "tensor",
+            "fp32_3xtf32": {"ms": ms32, "TFLOP/s": fp32_tflops, "tensor_TFLOP/s": 3 * fp32_tflops,
+                            "peak_tf32": tf32_peak, "frac_of_tf32_over_3": fp32_tflops / (tf32_peak / 3),
+                            "peak_source": peak_src + " bf16 burst x nominal tf32/bf16 ratio 1/2"},
             "roofline": {"achieved": tflops, "peak": peak, "unit": "TFLOP/s", "frac": tflops / peak,
                          "peak_source": peak_src + " bf16 burst", "traffic": ncu_traffic("matmul")}}
 

@@ -62,13 +62,16 @@ struct MLayout {
   static constexpr int TX = COPY;                                 // bytes TMA delivers per stage
 };
 
-__device__ __forceinline__ uint64_t smem_desc(const void *p, uint32_t lbo, uint32_t sbo) {
+// UMMA shared-memory layout types (descriptor bits [61,64))
+constexpr uint64_t LT_SW128 = 2, LT_SW128_BASE32B = 1;
+
+__device__ __forceinline__ uint64_t smem_desc(const void *p, uint32_t lbo, uint32_t sbo, uint64_t lt = LT_SW128) {
   // tcgen05 shared-memory matrix descriptor: start >> 4 [0,14), LBO >> 4
   // [16,30), SBO >> 4 [32,46), version 1 [46,48), base offset 0, layout
-  // SWIZZLE_128B = 2 at [61,64).
+  // type at [61,64).
   const uint64_t a = (uint64_t)((tma_smem(p) >> 4) & 0x3FFF);
   return a | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) | ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | (1ull << 46) |
-         (2ull << 61);
+         (lt << 61);
 }
 
 // instruction descriptor: D f32, A/B fmt, A K-major, B MN-major, N=256, M=128
@@ -91,6 +94,13 @@ __device__ __forceinline__ void mma(uint32_t tmem_d, uint64_t adesc, uint64_t bd
         " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
         "l"(adesc), "l"(bdesc), "r"(idesc<DT>()), "r"(accum));
 }
+// round-to-nearest (ties away) to tf32, returned as an fp32 bit pattern
+__device__ __forceinline__ float to_tf32(float x) {
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return __uint_as_float(r);
+}
+
 __device__ __forceinline__ void mma_commit(uint64_t *bar) {
   asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(tma_smem(bar))
                : "memory");
@@ -235,14 +245,17 @@ __global__ void __launch_bounds__(Cfg<DT>::THREADS, 1)
           for (int k = 0; k < BK / C::KSTEP; ++k) {
             // A K-major SW128: K step = 32 B inside the atom; SBO = 8 rows x 128 B.
             // B MN-major SW128: K step = KSTEP k-rows (x 128 B); LBO = box stride, SBO = 8 k-rows.
+            // (MN-major tf32 must use SWIZZLE_128B_BASE32B: 32-B atoms, 4-row groups, SBO = 512 B.)
+            constexpr uint64_t BLT = DT == UPIR_F32 ? LT_SW128_BASE32B : LT_SW128;
+            constexpr uint32_t BSBO = DT == UPIR_F32 ? 512 : 1024;
             const uint64_t ah = smem_desc(hi + k * 32, 16, 1024);
-            const uint64_t bh = smem_desc(hi + L::A_BYTES + k * C::KSTEP * 128, L::B_BOX, 1024);
+            const uint64_t bh = smem_desc(hi + L::A_BYTES + k * C::KSTEP * 128, L::B_BOX, BSBO, BLT);
             if constexpr (DT == UPIR_BF16) {
               mma<DT>(tmem_d, ah, bh, (kb | k) != 0);
             } else {
               const char *lo = hi + L::COPY;
               const uint64_t al = smem_desc(lo + k * 32, 16, 1024);
-              const uint64_t bl = smem_desc(lo + L::A_BYTES + k * C::KSTEP * 128, L::B_BOX, 1024);
+              const uint64_t bl = smem_desc(lo + L::A_BYTES + k * C::KSTEP * 128, L::B_BOX, BSBO, BLT);
               mma<DT>(tmem_d, al, bh, (kb | k) != 0);   // lo_a * hi_b
               mma<DT>(tmem_d, ah, bl, 1);               // hi_a * lo_b
               mma<DT>(tmem_d, ah, bh, 1);               // hi_a * hi_b
@@ -308,11 +321,12 @@ __global__ void __launch_bounds__(Cfg<DT>::THREADS, 1)
           float4 *hi = reinterpret_cast<float4 *>(smem + stage * L::STAGE);
           float4 *lo = reinterpret_cast<float4 *>(smem + stage * L::STAGE + L::COPY);
           for (int v = tid; v < L::COPY / 16; v += 128) {
-            float4 x = hi[v], h, l;
-            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&h.x)) : "f"(x.x));
-            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&h.y)) : "f"(x.y));
-            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&h.z)) : "f"(x.z));
-            asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(*reinterpret_cast<uint32_t *>(&h.w)) : "f"(x.w));
+            const float4 x = hi[v];
+            float4 h, l;
+            h.x = to_tf32(x.x);
+            h.y = to_tf32(x.y);
+            h.z = to_tf32(x.z);
+            h.w = to_tf32(x.w);
             l.x = __fsub_rn(x.x, h.x);
             l.y = __fsub_rn(x.y, h.y);
             l.z = __fsub_rn(x.z, h.z);
@@ -352,7 +366,8 @@ bool matmul_encode_tmaps(void *tma, void *tmb, const void *A, const void *B, int
   return encode_tmap_2d(reinterpret_cast<CUtensorMap *>(tma), dt, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda * es,
                         bk, BM, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) &&
          encode_tmap_2d(reinterpret_cast<CUtensorMap *>(tmb), dt, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb * es,
-                        boxn, bk, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
+                        boxn, bk, f32 ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B);
 }
 
 template <int DT>

@@ -104,7 +104,7 @@ struct MatmulArgs {
   int64_t ticket_m;
   unsigned long long *dyn_counter;
   int32_t *trace;               // tile -> team owner (tile granularity) or null
-  void *tmap_a, *tmap_b;        // device CUtensorMaps
+  void *tmap_a, *tmap_b;        // host CUtensorMaps (passed by value at launch)
 };
 cudaError_t launch_matmul(const MatmulArgs &a, int dtype, int teams, int units, cudaStream_t s);
 bool matmul_encode_tmaps(void *tma, void *tmb, const void *A, const void *B, int dtype,
