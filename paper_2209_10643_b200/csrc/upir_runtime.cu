@@ -173,6 +173,16 @@ extern "C" upir_status upir_init(int cuda_device, const upir_world *world, upir_
       return cleanup(fail(UPIR_E_CUDA, "stream create failed"));
     c->own_copy = true;
   }
+  // stream-ordered allocations of map(to/from/alloc) stay cached in the
+  // device's default pool across map exit / enter (no re-mapping per map)
+  {
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, cuda_device) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+  }
   if (cudaMalloc(&c->done, 256) != cudaSuccess || cudaMemset(c->done, 0, 256) != cudaSuccess)
     return cleanup(fail(UPIR_E_OOM, "workspace allocation failed"));
   c->dyn = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(c->done) + 64);
