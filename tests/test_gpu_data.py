@@ -1,0 +1,193 @@
+"""GPU parity of upir.data map semantics (o9, reading c18/c19) and of the
+CLUSTER-target code paths at world size 1, through the C-ABI."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2209_10643_b200 as U
+import synth
+from oracle.mapspace import MapSpace
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture()
+def ctx(upir):
+    c = U.upir_init(0)
+    yield c
+    U.upir_finalize(c)
+
+
+def test_to_from_round_trip_and_counters(ctx):
+    x = synth.f32_sym(1, 0, 10_000)
+    y = x.copy()
+    m = U.upir_data_map(ctx, y, U.MAP_TOFROM)
+    st = U.upir_ctx_stats(ctx)
+    assert st["h2d_bytes"] == x.nbytes and st["live_maps"] == 1
+    y[:] = 0                                 # host copy changes; device keeps the data
+    U.upir_data_unmap(ctx, m)
+    U.upir_sync(ctx)
+    assert (y == x).all()                    # tofrom: copied back at exit
+    st = U.upir_ctx_stats(ctx)
+    assert st["d2h_bytes"] == x.nbytes and st["live_maps"] == 0
+
+
+def test_present_table_refcount_copies_once(ctx):
+    # reading c18 vs the oracle's MapSpace on the same sequence
+    orc = MapSpace()
+    x = np.arange(1000, dtype=np.float64)
+    orc.host_buffer("x", x)
+    m1 = U.upir_data_map(ctx, x, U.MAP_TOFROM)
+    orc.enter("x", oracle.mapspace.TOFROM)
+    m2 = U.upir_data_map(ctx, x, U.MAP_TOFROM)   # present: refcount only
+    orc.enter("x", oracle.mapspace.TOFROM)
+    assert m1.value == m2.value
+    U.upir_data_unmap(ctx, m2)
+    orc.exit("x")
+    st = U.upir_ctx_stats(ctx)
+    assert st["live_maps"] == 1 and st["d2h_bytes"] == 0
+    U.upir_data_unmap(ctx, m1)
+    orc.exit("x")
+    U.upir_sync(ctx)
+    st = U.upir_ctx_stats(ctx)
+    assert st["h2d_bytes"] == orc.h2d and st["d2h_bytes"] == orc.d2h
+
+
+def test_alloc_and_from_do_not_copy_in(ctx):
+    a = np.full(4096, 7, np.int64)
+    m = U.upir_data_map(ctx, a, U.MAP_ALLOC)
+    b = np.full(4096, 9, np.int64)
+    mf = U.upir_data_map(ctx, b, U.MAP_FROM)
+    assert U.upir_ctx_stats(ctx)["h2d_bytes"] == 0
+    # the loop writes the FROM buffer: fill it on the device, then exit copies back
+    U.upir_synth_fill(ctx, mf, 2, 6)
+    U.upir_data_unmap(ctx, mf)
+    U.upir_data_unmap(ctx, m)
+    U.upir_sync(ctx)
+    assert (b == synth.i64_sym(6, 0, 4096)).all()
+    assert (a == 7).all()                    # alloc: never copied back
+
+
+def test_update_directions(ctx):
+    x = np.arange(256, dtype=np.int64)
+    m = U.upir_data_map(ctx, x, U.MAP_TO)
+    x[:] = -5
+    U.upir_data_update(ctx, m, 0)            # forward: host -> device
+    r = torch.zeros(1, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    s = U.upir_spmd_launch(ctx, U.spmd_desc(2, 64))
+    U.upir_loop_exec(s, U.loop_desc(0, 256), U.body(U.BODY_REDUCE, U.I64, in0=m), [U.reduction(U.OP_SUM, U.I64, r)])
+    U.upir_spmd_end(s)
+    U.upir_sync(ctx)
+    assert r.item() == -5 * 256
+    U.upir_synth_fill(ctx, m, 2, 6)
+    U.upir_data_update(ctx, m, 1)            # backward: device -> host
+    U.upir_sync(ctx)
+    assert (x == synth.i64_sym(6, 0, 256)).all()
+    U.upir_data_unmap(ctx, m)
+    U.upir_sync(ctx)
+
+
+def test_errors_not_mapped_leak_and_sync(upir):
+    c = U.upir_init(0)
+    x = np.zeros(16, np.int64)
+    m = U.upir_data_map(c, x, U.MAP_TO)
+    U.upir_data_unmap(c, m)
+    s = U.upir_spmd_launch(c, U.spmd_desc(1, 32))
+    with pytest.raises(U.UpirError) as ei:         # body names an unmapped buffer
+        U.upir_loop_exec(s, U.loop_desc(0, 16), U.body(U.BODY_REDUCE, U.I64, in0=m),
+                         [U.reduction(U.OP_SUM, U.I64, 0)])
+    assert ei.value.status == U.E_NOT_MAPPED
+    U.upir_spmd_end(s)
+    with pytest.raises(U.UpirError) as ei:         # wait without arrive
+        U.upir_sync(c, U.SYNC_WAIT)
+    assert ei.value.status == U.E_SYNC
+    tok = U.upir_sync(c, U.SYNC_ARRIVE)
+    U.upir_sync(c, U.SYNC_WAIT, token=tok)
+    m2 = U.upir_data_map(c, x, U.MAP_TO)
+    with pytest.raises(U.UpirError) as ei:         # finalize with a live map
+        U.upir_finalize(c)
+    assert ei.value.status == U.E_LEAK
+    U.upir_data_unmap(c, m2)
+    U.upir_finalize(c)
+
+
+def test_cluster_target_world1_reduce_and_world_combine(ctx):
+    n = 50_000
+    x = synth.i64_sym(6, 0, n)
+    d = U.dist(n, 1, 8)
+    m = U.upir_data_map(ctx, x, U.MAP_TO, d)
+    _, local, off = U.upir_data_device_ptr(m)
+    assert local == n and off == 0
+    r = torch.zeros(4, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    s = U.upir_spmd_launch(ctx, U.spmd_desc(16, 128, U.TARGET_CLUSTER))
+    U.upir_loop_exec(s, U.loop_desc(0, n), U.body(U.BODY_REDUCE, U.I64, in0=m),
+                     [U.reduction(U.OP_SUM, U.I64, r.data_ptr()), U.reduction(U.OP_MAX, U.I64, r.data_ptr() + 8)])
+    U.upir_spmd_end(s)
+    U.upir_reduce(ctx, U.OP_SUM, U.I64, r.data_ptr(), 1, r.data_ptr() + 16, U.SCOPE_WORLD)
+    U.upir_reduce(ctx, U.OP_MAX, U.I64, r.data_ptr() + 8, 1, r.data_ptr() + 24, U.SCOPE_WORLD)
+    U.upir_sync(ctx, U.SYNC_WORLD_BARRIER)
+    got = r.cpu().tolist()
+    assert got[2] == oracle.world_reduce(oracle.SUM, [oracle.reduce_i64(oracle.SUM, x)]) == got[0]
+    assert got[3] == int(x.max())
+    U.upir_data_unmap(ctx, m)
+    U.upir_sync(ctx)
+
+
+def test_device_scope_reduce(ctx):
+    x = torch.from_numpy(synth.f32_sym(7, 0, 1_000_003)).cuda()
+    xi = torch.from_numpy(synth.i64_sym(6, 0, 777_777)).cuda()
+    out = torch.zeros(2, dtype=torch.float32, device="cuda")
+    outi = torch.zeros(1, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    U.upir_reduce(ctx, U.OP_SUM, U.F32, x, x.numel(), out, U.SCOPE_DEVICE)
+    U.upir_sync(ctx)
+    U.upir_reduce(ctx, U.OP_MAX, U.F32, x, x.numel(), out.data_ptr() + 4, U.SCOPE_DEVICE)
+    U.upir_sync(ctx)
+    U.upir_reduce(ctx, U.OP_MIN, U.I64, xi, xi.numel(), outi, U.SCOPE_DEVICE)
+    U.upir_sync(ctx)
+    xs = x.cpu().numpy()
+    assert abs(out[0].item() - oracle.reduce_f32(oracle.SUM, xs)) <= 1e-5 * np.abs(xs).sum()
+    assert out[1].item() == float(xs.max())
+    assert outi.item() == int(xi.cpu().numpy().min())
+
+
+def test_cluster_jacobi_world1_with_halo_sync(ctx):
+    ny, nx, S = 66, 132, 4
+    g = synth.jacobi_init(ny, nx)
+    a, b = g.copy(), g.copy()
+    d = U.dist(ny, nx, 4, halo_rows=1)
+    ma = U.upir_data_map(ctx, a, U.MAP_TOFROM, d)
+    mb = U.upir_data_map(ctx, b, U.MAP_TOFROM, d)
+    s = U.upir_spmd_launch(ctx, U.spmd_desc(8, 256, U.TARGET_CLUSTER))
+    loop = U.loop_desc([1, 1], [ny - 1, nx - 1], tile=[32, 128], distribute=U.DIST_TEAMS, inner_chunk=4)
+    src, dst = ma, mb
+    for _ in range(S):
+        U.upir_sync(ctx, U.SYNC_HALO, halo_map=src)     # no-op at world size 1
+        U.upir_loop_exec(s, loop, U.body(U.BODY_JACOBI5, U.F32, in0=src, out=dst, ld=(nx, 0, 0), dims=(ny, 0, 0)))
+        src, dst = dst, src
+    U.upir_spmd_end(s)
+    U.upir_data_unmap(ctx, mb)
+    U.upir_data_unmap(ctx, ma)
+    U.upir_sync(ctx)
+    ref = oracle.jacobi5(g, S)
+    assert np.abs(a - ref).max() <= 1e-5 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("teams,units", [(1, 1), (148 * 4, 256)])
+def test_c1_axpy_sum_1e6(ctx, teams, units):
+    """BASELINE configs[0]: axpy + fp32 sum, n = 1,000,000, static schedule;
+    literal 1 unit and the default geometry (reading c21)."""
+    from gpu_helpers import run_axpy
+    n = 1_000_000
+    x = synth.f32_unit(1, 0, n)
+    y = synth.f32_unit(2, 0, n)
+    yy, s, (team, unit, hits) = run_axpy(ctx, 2.0, x, y, teams, units, sum_=True, trace=True)
+    ref = oracle.axpy(2.0, x, y)
+    assert (yy == ref.astype(np.float32)).all()          # exact on the 2^-24 grid
+    assert abs(s - oracle.reduce_f32(oracle.SUM, yy, p=teams * units)) <= 1e-5 * abs(s)
+    assert (hits == 1).all()
+    g = team.astype(np.int64) * units + unit
+    assert (g == oracle.owner_map(oracle.STATIC, 0, n, teams * units)).all()
