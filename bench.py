@@ -20,6 +20,7 @@ Inputs (12 GiB per GPU) are far larger than L2 (126 MB): no flush needed.
 """
 import argparse
 import json
+import math
 import os
 import statistics
 import subprocess
@@ -41,7 +42,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="upir", choices=["upir", "reference"])
-    ap.add_argument("--workload", default="reduce", choices=["reduce", "axpy", "jacobi", "matmul"])
+    ap.add_argument("--workload", default="reduce", choices=["reduce", "reduce34", "jacobi32k"],
+                    help="reduce = C2 (default); reduce34 = C5a 2^34 int64 strong scaling; "
+                         "jacobi32k = C5b 32768^2 Jacobi with halo exchange, strong scaling")
     ap.add_argument("--sched", default="static", choices=["static", "static1", "dynamic"])
     ap.add_argument("--n-log2", type=int, default=30)
     ap.add_argument("--e2e-steps", type=int, default=3)
@@ -185,6 +188,19 @@ def cpu_baseline_reduce():
                       "GB/s counted as 12 B per element pair like the GPU metric"}
 
 
+def cpu_baseline_jacobi():
+    import oracle
+    import synth
+    ny = nx = 2048
+    S = 10
+    g = synth.jacobi_init(ny, nx)
+    t0 = time.perf_counter()
+    oracle.jacobi5(g, S)
+    dt = time.perf_counter() - t0
+    return {"value": (ny - 2) * (nx - 2) * S / dt / 1e9, "unit": "GLUP/s", "cores": 1, "kind": "oracle",
+            "sample": "2048^2 grid, 10 sweeps (fp64 oracle), GLUP/s"}
+
+
 # --------------------------------------------------------------------------- UPIR arm
 def run_upir(args):
     import torch
@@ -197,6 +213,7 @@ def run_upir(args):
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         pg = dist
+        _PG[0] = dist
         idb = [U.upir_comm_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(idb, src=0)
         ctx = U.upir_init(local, rank=rank, nranks=world, nccl_id=idb[0])
@@ -213,10 +230,14 @@ def run_upir(args):
 
     if args.workload == "reduce":
         res = bench_reduce(args, U, ctx, stream, barrier, rank, world, peaks, peak_src)
+    elif args.workload == "reduce34":
+        res = bench_reduce34(args, U, ctx, stream, barrier, rank, world, peaks, peak_src)
+    elif args.workload == "jacobi32k":
+        res = bench_jacobi32k(args, U, ctx, stream, barrier, rank, world, peaks, peak_src)
     else:
-        raise SystemExit(f"workload {args.workload} not built yet")
+        raise SystemExit(f"workload {args.workload} is a kernel line of the default run (see 'kernels')")
     # the other loop bodies of the path, each timed on its own (single GPU)
-    if world == 1 and not args.no_kernels:
+    if world == 1 and not args.no_kernels and args.workload == "reduce":
         res["kernels"] = {}
         for name, fn in (("axpy", bench_axpy), ("jacobi", bench_jacobi), ("matmul", bench_matmul)):
             try:
@@ -224,16 +245,21 @@ def run_upir(args):
             except Exception as e:   # report, never hide
                 res["kernels"][name] = {"error": str(e)[:300]}
     # max over ranks of the timed values
-    if pg:
-        t = torch.tensor([res["ms_per_step"], res["e2e_ms"]], device="cuda")
-        pg.all_reduce(t, op=pg.ReduceOp.MAX)
-        res["ms_per_step"], res["e2e_ms"] = t.tolist()
-    res["value"] = res["bytes_all_ranks"] / (res["ms_per_step"] / 1e3) / 1e9
-    res["e2e"]["value"] = res["bytes_all_ranks"] / (res["e2e_ms"] / 1e3) / 1e9
+    if args.workload == "reduce":
+        if pg:
+            t = torch.tensor([res["ms_per_step"], res["e2e_ms"]], device="cuda")
+            pg.all_reduce(t, op=pg.ReduceOp.MAX)
+            res["ms_per_step"], res["e2e_ms"] = t.tolist()
+        res["value"] = res["bytes_all_ranks"] / (res["ms_per_step"] / 1e3) / 1e9
+        res["e2e"]["value"] = res["bytes_all_ranks"] / (res["e2e_ms"] / 1e3) / 1e9
+    elif args.workload == "reduce34":
+        res["value"] = res["bytes_all_ranks"] / (res["ms_per_step"] / 1e3) / 1e9
+    else:
+        res["value"] = res.pop("glups")
     if rank == 0:
         out = {k: v for k, v in res.items() if k not in ("bytes_all_ranks", "e2e_ms")}
         if world == 1 and not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline_reduce()
+            out["cpu_baseline"] = cpu_baseline_jacobi() if args.workload == "jacobi32k" else cpu_baseline_reduce()
         print(json.dumps(out), flush=True)
     U.upir_finalize(ctx)
     if pg:
@@ -441,8 +467,9 @@ def bench_jacobi(args, U, ctx, stream, peaks, peak_src, ny=8192, nx=8192, S=100)
     ma, mb = U.upir_data_adopt(ctx, a_t), U.upir_data_adopt(ctx, b_t)
     U.upir_synth_fill(ctx, ma, 4, 5, 0, ny, nx)
     U.upir_synth_fill(ctx, mb, 4, 5, 0, ny, nx)
-    teams = int(os.environ.get("UPIR_JACOBI_TEAMS", 296))
-    bm, bn = (int(v) for v in os.environ.get("UPIR_JACOBI_TILE", "32x256").split("x"))
+    # 16x256 tiles, 3 teams per SM: measured best of the r01 sweep (tools/sweep_jacobi_axpy.sh)
+    teams = int(os.environ.get("UPIR_JACOBI_TEAMS", 444))
+    bm, bn = (int(v) for v in os.environ.get("UPIR_JACOBI_TILE", "16x256").split("x"))
     loop = U.loop_desc([1, 1], [ny - 1, nx - 1], tile=[bm, bn], policy=U.SCHED_STATIC, chunk=1,
                        distribute=U.DIST_TEAMS, inner_chunk=4)
     s = U.upir_spmd_launch(ctx, U.spmd_desc(teams, 256))
@@ -525,6 +552,149 @@ def bench_matmul(args, U, ctx, stream, peaks, peak_src, n=8192):
                             "peak_source": peak_src + " bf16 burst x nominal tf32/bf16 ratio 1/2"},
             "roofline": {"achieved": tflops, "peak": peak, "unit": "TFLOP/s", "frac": tflops / peak,
                          "peak_source": peak_src + " bf16 burst", "traffic": ncu_traffic("matmul")}}
+
+
+def _ranks_max(pg, vals):
+    import torch
+    if not pg:
+        return vals
+    t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return t.tolist()
+
+
+def bench_reduce34(args, U, ctx, stream, barrier, rank, world, peaks, peak_src):
+    """C5a: one int64 sum+max reduction over n = 2^34 elements distributed over
+    the ranks (upir_dist BLOCK, CLUSTER-target loop), combined with
+    upir_reduce(WORLD).  Strong scaling (the global n is fixed)."""
+    import torch
+    n = 1 << int(os.environ.get("UPIR_C5A_LOG2", 34))
+    lo, hi = U.upir_dist_owned_rows(n, rank, world)
+    x = torch.empty(hi - lo, dtype=torch.int64, device="cuda")
+    res_t = torch.zeros(4, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    m = U.upir_data_adopt(ctx, x, U.dist(n, 1, 8))
+    U.upir_synth_fill(ctx, m, 2, 6)
+    base = res_t.data_ptr()
+    reds = [U.reduction(U.OP_SUM, U.I64, base), U.reduction(U.OP_MAX, U.I64, base + 8)]
+    spmd = U.upir_spmd_launch(ctx, U.spmd_desc(148 * 4, 256, U.TARGET_CLUSTER))
+    loop = U.loop_desc(0, n)
+
+    def step():
+        U.upir_loop_exec(spmd, loop, U.body(U.BODY_REDUCE, U.I64, in0=m), reds)
+        U.upir_reduce(ctx, U.OP_SUM, U.I64, base, 1, base + 16, U.SCOPE_WORLD)
+        U.upir_reduce(ctx, U.OP_MAX, U.I64, base + 8, 1, base + 24, U.SCOPE_WORLD)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    st0 = U.upir_ctx_stats(ctx)["launches"]
+    clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    clk.start()
+    ms = _time_graph(U, ctx, stream, step, args.steps)
+    barrier()
+    clocks = clk.stop()
+    launches = U.upir_ctx_stats(ctx)["launches"] - st0
+    ms_local = ms
+    (ms,) = _ranks_max(pg_of(), [ms])
+    U.upir_spmd_end(spmd)
+    U.upir_data_unmap(ctx, m)
+    U.upir_sync(ctx)
+    peak = float(peaks["hbm_gbs"])
+    per_rank_gbs = (hi - lo) * 8 / (ms_local / 1e3) / 1e9
+    return {
+        "metric": "GB/s of the 2^34-element int64 sum+max reduction (C5a), whole job", "unit": "GB/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "i64", "data": "synthetic",
+        "config": {"workload": f"C5a: int64 sum+max over n=2^{int(math.log2(n))} BLOCK-distributed over {world} "
+                               "GPU(s), 592x256 per GPU, static schedule, upir_reduce(WORLD)",
+                   "n_global": n, "parallelism": f"dp{world}", "l2": "inputs >> L2"},
+        "roofline": {"bound": "hbm", "achieved": per_rank_gbs, "peak": peak, "unit": "GB/s",
+                     "frac": per_rank_gbs / peak, "traffic": ncu_traffic("reduce_i64_1"),
+                     "kernel": "stream_loop_kernel<RED_I64,1 or 2> (per rank)", "peak_source": peak_src},
+        "clocks": clocks, "gpu_launches": launches,
+        "e2e": {"value": None, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0,
+                "note": "inputs generated on device (2^34 x 8 B exceeds host staging)"},
+        "bytes_all_ranks": n * 8, "e2e_ms": float("nan"),
+    }
+
+
+_PG = [None]
+
+
+def pg_of():
+    return _PG[0]
+
+
+def bench_jacobi32k(args, U, ctx, stream, barrier, rank, world, peaks, peak_src, n=None, S=100):
+    """C5b: Jacobi 5-point on a 32768^2 fp32 grid, 100 sweeps, BLOCK row slabs
+    with 1-row halos exchanged by upir_sync(HALO) before every sweep (NCCL
+    send/recv in stream order), the 100 sweeps captured as one CUDA graph.
+    Strong scaling."""
+    import torch
+    n = n or int(os.environ.get("UPIR_C5B_N", 32768))
+    lo, hi = U.upir_dist_owned_rows(n, rank, world)
+    llo, lhi = max(0, lo - 1), min(n, hi + 1)
+    a_t = torch.empty((lhi - llo) * n, dtype=torch.float32, device="cuda")
+    b_t = torch.empty((lhi - llo) * n, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    d = U.dist(n, n, 4, halo_rows=1)
+    ma, mb = U.upir_data_adopt(ctx, a_t, d), U.upir_data_adopt(ctx, b_t, d)
+    U.upir_synth_fill(ctx, ma, 4, 5, 0, n, n)
+    U.upir_synth_fill(ctx, mb, 4, 5, 0, n, n)
+    teams = int(os.environ.get("UPIR_JACOBI_TEAMS", 444))
+    bm, bn = (int(v) for v in os.environ.get("UPIR_JACOBI_TILE", "16x256").split("x"))
+    loop = U.loop_desc([1, 1], [n - 1, n - 1], tile=[bm, bn], policy=U.SCHED_STATIC, chunk=1,
+                       distribute=U.DIST_TEAMS, inner_chunk=4)
+    s = U.upir_spmd_launch(ctx, U.spmd_desc(teams, 256, U.TARGET_CLUSTER))
+    bodies = [(ma, U.body(U.BODY_JACOBI5, U.F32, in0=ma, out=mb, ld=(n, 0, 0), dims=(n, 0, 0))),
+              (mb, U.body(U.BODY_JACOBI5, U.F32, in0=mb, out=ma, ld=(n, 0, 0), dims=(n, 0, 0)))]
+
+    def sweeps():
+        for k in range(S):
+            src, body = bodies[k % 2]
+            U.upir_sync(ctx, U.SYNC_HALO, halo_map=src)
+            U.upir_loop_exec(s, loop, body)
+
+    U.upir_graph_begin(ctx)
+    sweeps()
+    g = U.upir_graph_end(ctx)
+    U.upir_graph_launch(ctx, g)
+    barrier()
+    st0 = U.upir_ctx_stats(ctx)["launches"]
+    clk = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+    clk.start()
+    reps = max(1, min(args.steps, 3))
+    ms_local = _time_graph(U, ctx, stream, lambda: U.upir_graph_launch(ctx, g), reps)
+    barrier()
+    clocks = clk.stop()
+    launches = U.upir_ctx_stats(ctx)["launches"] - st0
+    (ms,) = _ranks_max(pg_of(), [ms_local])
+    U.upir_graph_destroy(g)
+    U.upir_spmd_end(s)
+    U.upir_data_unmap(ctx, ma)
+    U.upir_data_unmap(ctx, mb)
+    U.upir_sync(ctx)
+    lups = (n - 2) * (n - 2) * S
+    own = (min(hi, n - 1) - max(lo, 1)) * (n - 2) * S
+    per_rank_gbs = 8 * own / (ms_local / 1e3) / 1e9
+    peak = float(peaks["hbm_gbs"])
+    glups = lups / (ms / 1e3) / 1e9
+    return {
+        "metric": "Jacobi GLUP/s (C5b 32768^2, 100 sweeps), whole job", "unit": "GLUP/s",
+        "n_gpus": world, "steps": reps, "warmup": 1, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"C5b: Jacobi 5-point {n}x{n} fp32, {S} sweeps as one CUDA graph, BLOCK row slabs "
+                               f"over {world} GPU(s) with 1-row halos (upir_sync HALO before each sweep), tiles "
+                               f"{bm}x{bn} static,1 over {teams} teams",
+                   "parallelism": f"dp{world}", "l2": "2 x 4 GiB grids >> L2"},
+        "roofline": {"bound": "hbm", "achieved": per_rank_gbs, "peak": peak, "unit": "GB/s",
+                     "frac": per_rank_gbs / peak, "traffic": ncu_traffic("jacobi"),
+                     "kernel": f"jacobi5_kernel<{bm},{bn}>", "peak_source": peak_src},
+        "clocks": clocks, "gpu_launches": launches,
+        "e2e": {"value": None, "unit": "GLUP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "glups": glups, "e2e_ms": float("nan"), "bytes_all_ranks": None,
+    }
 
 
 def main():
