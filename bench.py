@@ -45,7 +45,9 @@ def parse():
     ap.add_argument("--workload", default="reduce", choices=["reduce", "reduce34", "jacobi32k"],
                     help="reduce = C2 (default); reduce34 = C5a 2^34 int64 strong scaling; "
                          "jacobi32k = C5b 32768^2 Jacobi with halo exchange, strong scaling")
-    ap.add_argument("--sched", default="static", choices=["static", "static1", "dynamic"])
+    ap.add_argument("--sched", default=None, choices=["static", "static1", "dynamic"],
+                    help="default: static for C2; static1 (one 16-B vector per chunk) for C5a, whose 2^34-element "
+                         "static blocks put ~65k distinct 2 MB pages in flight (TLB-bound, see DESIGN.md)")
     ap.add_argument("--n-log2", type=int, default=30)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -578,7 +580,8 @@ def bench_reduce34(args, U, ctx, stream, barrier, rank, world, peaks, peak_src):
     base = res_t.data_ptr()
     reds = [U.reduction(U.OP_SUM, U.I64, base), U.reduction(U.OP_MAX, U.I64, base + 8)]
     spmd = U.upir_spmd_launch(ctx, U.spmd_desc(148 * 4, 256, U.TARGET_CLUSTER))
-    loop = U.loop_desc(0, n)
+    pol = {"static": U.SCHED_STATIC, "static1": U.SCHED_STATIC, "dynamic": U.SCHED_DYNAMIC}[args.sched]
+    loop = U.loop_desc(0, n, policy=pol, chunk=0 if args.sched == "static" else 2)
 
     def step():
         U.upir_loop_exec(spmd, loop, U.body(U.BODY_REDUCE, U.I64, in0=m), reds)
@@ -607,7 +610,7 @@ def bench_reduce34(args, U, ctx, stream, barrier, rank, world, peaks, peak_src):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "i64", "data": "synthetic",
         "config": {"workload": f"C5a: int64 sum+max over n=2^{int(math.log2(n))} BLOCK-distributed over {world} "
-                               "GPU(s), 592x256 per GPU, static schedule, upir_reduce(WORLD)",
+                               f"GPU(s), 592x256 per GPU, schedule {args.sched}, upir_reduce(WORLD)",
                    "n_global": n, "parallelism": f"dp{world}", "l2": "inputs >> L2"},
         "roofline": {"bound": "hbm", "achieved": per_rank_gbs, "peak": peak, "unit": "GB/s",
                      "frac": per_rank_gbs / peak, "traffic": ncu_traffic("reduce_i64_1"),
@@ -699,6 +702,8 @@ def bench_jacobi32k(args, U, ctx, stream, barrier, rank, world, peaks, peak_src,
 
 def main():
     args = parse()
+    if args.sched is None:
+        args.sched = "static1" if args.workload == "reduce34" else "static"
     if args.impl == "reference":
         run_reference(args)
         return
