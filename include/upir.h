@@ -39,7 +39,7 @@ extern "C" {
 typedef enum {
     UPIR_OK = 0,
     UPIR_E_INVALID = 1,     /* bad descriptor / geometry / argument           */
-    UPIR_E_UNSUPPORTED = 2, /* valid UPIR, not implemented (guided, taskloop)  */
+    UPIR_E_UNSUPPORTED = 2, /* valid UPIR, not implemented (e.g. taskloop)      */
     UPIR_E_NOT_MAPPED = 3,  /* body names a buffer absent from the present table */
     UPIR_E_OOM = 4,
     UPIR_E_CUDA = 5,
@@ -175,8 +175,10 @@ upir_status upir_spmd_end(upir_spmd spmd);
  *   STATIC, chunk c  : chunk k = [k*c, min((k+1)*c, T)) -> unit k mod p
  *   DYNAMIC, chunk c : same chunk partition (default c = 1); chunks are claimed
  *                      at run time; each unit's chunks are increasing
+ *   GUIDED, chunk c  : chunks cut in dispatch order, each max(ceil(remaining /
+ *                      p), c) long (default c = 1), claimed at run time like
+ *                      DYNAMIC (1-D loops; tiled nests: UPIR_E_UNSUPPORTED)
  *   RUNTIME, AUTO    : resolve to STATIC
- *   GUIDED           : UPIR_E_UNSUPPORTED in this build
  * distribute: TEAMS_UNITS: p = teams*units over flat g;
  *   TEAMS: p = teams, executed by unit 0 of each team (reading c6);
  *   UNITS: p = units, requires num_teams == 1 (reading c7).

@@ -80,14 +80,39 @@ static int64_t n_chunks(int64_t T, int64_t c) { return (T + c - 1) / c; }
  *     FIFO queue initially ordered by id; the unit at the head takes the next
  *     chunk, runs it, and re-enters the queue at the tail.
  * runtime / auto resolve to static (reading c3).
- * guided is not part of this build's scope: -1. */
+ * guided, chunk c (default 1; PAPER.md:644 'guided'): chunks
+ *     are cut in dispatch order, each max(ceil(remaining / p), c) long
+ *     (clipped at T), remaining = T - start of the chunk; handed out by the
+ *     same deterministic dispatcher as dynamic. */
 int64_t orc_schedule_chunks(int policy, int64_t chunk, int64_t T, int64_t p,
                             int64_t u, int64_t *lo, int64_t *hi, int64_t cap)
 {
     int64_t cnt = 0;
     if (p <= 0 || u < 0 || u >= p || T < 0) return -1;
     if (policy == ORC_RUNTIME || policy == ORC_AUTO) { policy = ORC_STATIC; chunk = 0; }
-    if (policy == ORC_GUIDED) return -1;
+    if (policy == ORC_GUIDED) {
+        int64_t c = chunk <= 0 ? 1 : chunk;
+        int64_t *queue = (int64_t *)malloc(sizeof(int64_t) * (size_t)p);
+        if (!queue) return -1;
+        int64_t head = 0, count = p, start = 0;
+        for (int64_t i = 0; i < p; ++i) queue[i] = i;
+        while (start < T) {
+            int64_t rem = T - start;
+            int64_t len = (rem + p - 1) / p;          /* ceil(remaining / p) */
+            if (len < c) len = c;
+            if (len > rem) len = rem;
+            int64_t w = queue[head];
+            head = (head + 1) % p; --count;
+            if (w == u) {
+                if (cnt < cap) { lo[cnt] = start; hi[cnt] = start + len; }
+                ++cnt;
+            }
+            queue[(head + count) % p] = w; ++count;
+            start += len;
+        }
+        free(queue);
+        return cnt;
+    }
     if (policy == ORC_STATIC && chunk <= 0) {
         int64_t q = T / p, r = T % p;
         int64_t start = u * q + (u < r ? u : r);

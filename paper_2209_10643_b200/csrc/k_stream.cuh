@@ -664,22 +664,23 @@ __global__ void __launch_bounds__(1024) stream_loop_kernel(const __grid_constant
     else direct_run<BODY, NRED, TRACE>(a, w, acc, team, unit);
   };
 
-  if (a.sched == SK_DYNAMIC) {
+  if (a.sched == SK_DYNAMIC || a.sched == SK_GUIDED) {
     __shared__ long long s_base;
-    const int64_t nchunks = (a.T + a.chunk - 1) / a.chunk;
-    const unsigned long long tu = (unsigned long long)u.p_team * (unsigned long long)a.ticket_m;
+    const bool guided = a.sched == SK_GUIDED;
+    const int64_t nchunks = guided ? a.gchunks : (a.T + a.chunk - 1) / a.chunk;
+    const unsigned long long tu = (unsigned long long)u.p_team * (unsigned long long)(guided ? 1 : a.ticket_m);
     for (;;) {
       if (threadIdx.x == 0) s_base = (long long)atomicAdd(a.dyn_counter, tu);
       __syncthreads();
       const int64_t b = s_base;
       __syncthreads();
       if (b >= nchunks) break;
-      run(ticket_work(b, a.ticket_m, a.T, a.chunk, u));
+      run(guided ? guided_work(b, nchunks, a.gtab, u) : ticket_work(b, a.ticket_m, a.T, a.chunk, u));
     }
   } else {
     run(static_work(a.sched, a.T, a.chunk, u));
   }
-  reduce_epilogue<BODY, NRED>(a, acc, NRED > 0 || a.sched == SK_DYNAMIC);
+  reduce_epilogue<BODY, NRED>(a, acc, NRED > 0 || a.sched == SK_DYNAMIC || a.sched == SK_GUIDED);
 }
 
 // Host-side dispatch over (NRED, TRACE, PATH config) for one body.

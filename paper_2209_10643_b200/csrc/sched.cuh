@@ -10,6 +10,9 @@
 //                 atomicAdd; unit u of the team takes chunks b + u + j*p_team
 //                 (j < m): chunk boundaries are exact, each unit's chunks are
 //                 increasing, the unit assignment is decided at run time (c8).
+// guided c      : the same tickets (m = 1) over the guided chunk sequence
+//                 b_{g+1} = b_g + max(ceil((T - b_g)/p), c), precomputed on the
+//                 host into a boundary table.
 #pragma once
 #include <stdint.h>
 
@@ -19,6 +22,7 @@ namespace upir {
 
 struct LaneWork {
   int64_t lo0, kstride, nk, c;
+  const int64_t *tab;   // guided: lo0 / kstride index chunks of this boundary table
 };
 
 struct UnitIds {
@@ -58,7 +62,7 @@ __device__ __forceinline__ UnitIds unit_ids(int distribute) {
 }
 
 __device__ __forceinline__ LaneWork static_work(int sched, int64_t T, int64_t c, const UnitIds &u) {
-  LaneWork w{0, 0, 0, 1};
+  LaneWork w{0, 0, 0, 1, nullptr};
   if (!u.active || T <= 0) return w;
   if (sched == SK_STATIC_BLOCK) {
     const int64_t q = T / u.p, r = T % u.p;
@@ -81,7 +85,7 @@ __device__ __forceinline__ LaneWork static_work(int sched, int64_t T, int64_t c,
 // Unit's chunks of a dynamic ticket starting at chunk b (m chunks per unit).
 __device__ __forceinline__ LaneWork ticket_work(int64_t b, int64_t m, int64_t T, int64_t c,
                                                 const UnitIds &u) {
-  LaneWork w{0, 0, 0, c};
+  LaneWork w{0, 0, 0, c, nullptr};
   if (!u.active) return w;
   const int64_t nchunks = (T + c - 1) / c;
   const int64_t first = b + u.u_team;
@@ -93,9 +97,28 @@ __device__ __forceinline__ LaneWork ticket_work(int64_t b, int64_t m, int64_t T,
   return w;
 }
 
+// guided: the unit's chunks of a ticket starting at chunk index b of the
+// boundary table (chunk g = [tab[g], tab[g+1])); chunk sizes vary, so the
+// long-chunk memory paths are used (c = "long").
+__device__ __forceinline__ LaneWork guided_work(int64_t b, int64_t nc, const int64_t *tab, const UnitIds &u) {
+  LaneWork w{0, 0, 0, ((int64_t)1 << 40), tab};
+  if (!u.active) return w;
+  const int64_t first = b + u.u_team;
+  if (first >= nc) return w;
+  w.nk = 1;
+  w.lo0 = first;
+  return w;
+}
+
 // Chunk j of a lane's work, in the normalised space.
 __device__ __forceinline__ void chunk_bounds(const LaneWork &w, int64_t j, int64_t T, int64_t &klo,
                                              int64_t &khi) {
+  if (w.tab) {
+    const int64_t g = w.lo0 + j * w.kstride;
+    klo = w.tab[g];
+    khi = w.tab[g + 1];
+    return;
+  }
   klo = w.lo0 + j * w.kstride;
   khi = klo + w.c;
   if (khi > T) khi = T;

@@ -9,7 +9,7 @@
 namespace upir {
 
 // Schedule kinds after host-side resolution (readings c3-c8).
-enum SchedKind : int32_t { SK_STATIC_BLOCK = 0, SK_STATIC_CHUNK = 1, SK_DYNAMIC = 2 };
+enum SchedKind : int32_t { SK_STATIC_BLOCK = 0, SK_STATIC_CHUNK = 1, SK_DYNAMIC = 2, SK_GUIDED = 3 };
 
 // Memory path of the 1-D streaming kernels.
 enum PathKind : int32_t {
@@ -36,7 +36,9 @@ struct StreamArgs {
   int32_t distribute;   // upir_distribute
   int64_t chunk;        // static-chunk / dynamic chunk size (iterations)
   int64_t ticket_m;     // dynamic: chunks per unit per ticket
-  unsigned long long *dyn_counter;  // dynamic: chunk counter (zeroed per launch)
+  unsigned long long *dyn_counter;  // dynamic / guided: chunk counter (reset by the last team)
+  const int64_t *gtab;  // guided: chunk boundaries b_0 = 0 < b_1 < ... < b_nc = T (nc + 1 entries)
+  int64_t gchunks;      // guided: nc
   // body (pointers already shifted so that element i lives at ptr[i])
   const void *in0;      // reduce: data; axpy: x
   void *out;            // axpy: y

@@ -103,6 +103,10 @@ struct upir_ctx_s {
   void *scratch = nullptr;      // world-reduce gather buffer
   size_t scratch_bytes = 0;
   void *one = nullptr;          // 1-element buffer for the world barrier
+  // guided-schedule boundary table cache (T, p, c) -> device table
+  int64_t *gtab = nullptr;
+  size_t gtab_cap = 0;
+  int64_t g_T = -1, g_p = -1, g_c = -1, g_n = 0;
   // present table: host pointer -> map
   std::map<void *, upir_map> present;
   std::vector<upir_map> adopted;
@@ -237,6 +241,7 @@ extern "C" upir_status upir_finalize(upir_ctx c) {
   cudaFree(c->done);
   cudaFree(c->one);
   if (c->scratch) cudaFree(c->scratch);
+  if (c->gtab) cudaFree(c->gtab);
   if (c->own_compute) cudaStreamDestroy(c->compute);
   if (c->own_copy) cudaStreamDestroy(c->copy);
   delete c;
@@ -591,7 +596,9 @@ static upir_status resolve_sched(int policy, int64_t chunk, int &sk, int64_t &c)
       c = chunk > 0 ? chunk : 1;
       return UPIR_OK;
     case UPIR_SCHED_GUIDED:
-      return fail(UPIR_E_UNSUPPORTED, "schedule(guided) is not implemented in this build");
+      sk = SK_GUIDED;
+      c = chunk > 0 ? chunk : 1;
+      return UPIR_OK;
   }
   return fail(UPIR_E_INVALID, "unknown schedule policy %d", policy);
 }
@@ -604,7 +611,8 @@ extern "C" upir_status upir_schedule_chunks(int32_t policy, int64_t chunk, int64
   int64_t c;
   upir_status st = resolve_sched(policy, chunk, sk, c);
   if (st != UPIR_OK) return st;
-  if (sk == SK_DYNAMIC) return fail(UPIR_E_INVALID, "dynamic assignment is decided at run time");
+  if (sk == SK_DYNAMIC || sk == SK_GUIDED)
+    return fail(UPIR_E_INVALID, "dynamic / guided assignment is decided at run time");
   int64_t n = 0;
   if (sk == SK_STATIC_BLOCK) {
     const int64_t q = T / p, r = T % p;
@@ -726,6 +734,43 @@ static const char *env_path() {
   return p ? p : "";
 }
 
+// Guided chunk boundaries b_0 = 0, b_{g+1} = b_g + max(ceil((T - b_g)/p), c)
+// (PAPER.md:644 'guided'), cached on the device per (T, p, c).
+static upir_status guided_table(upir_ctx c, int64_t T, int64_t p, int64_t ch, const int64_t **tab, int64_t *nc) {
+  if (c->g_T == T && c->g_p == p && c->g_c == ch) {
+    *tab = c->gtab;
+    *nc = c->g_n;
+    return UPIR_OK;
+  }
+  if (c->capturing) return fail(UPIR_E_INVALID, "guided table must be built before graph capture");
+  std::vector<int64_t> b;
+  b.push_back(0);
+  int64_t start = 0;
+  while (start < T) {
+    const int64_t rem = T - start;
+    int64_t len = (rem + p - 1) / p;
+    if (len < ch) len = ch;
+    if (len > rem) len = rem;
+    start += len;
+    b.push_back(start);
+  }
+  const size_t bytes = b.size() * sizeof(int64_t);
+  CUDA_TRY(cudaStreamSynchronize(c->compute));
+  if (bytes > c->gtab_cap) {
+    if (c->gtab) CUDA_TRY(cudaFree(c->gtab));
+    CUDA_TRY(cudaMalloc(&c->gtab, bytes));
+    c->gtab_cap = bytes;
+  }
+  CUDA_TRY(cudaMemcpy(c->gtab, b.data(), bytes, cudaMemcpyHostToDevice));
+  c->g_T = T;
+  c->g_p = p;
+  c->g_c = ch;
+  c->g_n = (int64_t)b.size() - 1;
+  *tab = c->gtab;
+  *nc = c->g_n;
+  return UPIR_OK;
+}
+
 static upir_status exec_stream(upir_spmd s, const upir_loop_desc *l, const upir_body *b, const upir_reduction *reds,
                                int n_reds, upir_map trace) {
   upir_ctx c = s->ctx;
@@ -801,6 +846,14 @@ static upir_status exec_stream(upir_spmd s, const upir_loop_desc *l, const upir_
   if (const char *dv = getenv("UPIR_DVAR")) a.dvar = atoi(dv);
   // dynamic tickets: m chunks per unit so a ticket covers >= ~256 KiB
   const int p_team = l->distribute == UPIR_DIST_TEAMS ? 1 : sd.num_units;
+  const int64_t p_sched = l->distribute == UPIR_DIST_TEAMS ? sd.num_teams
+                         : l->distribute == UPIR_DIST_UNITS ? sd.num_units
+                         : (int64_t)sd.num_teams * sd.num_units;
+  if (sk == SK_GUIDED) {
+    st = guided_table(c, T, p_sched, chunk, &a.gtab, &a.gchunks);
+    if (st != UPIR_OK) return st;
+    a.dyn_counter = c->dyn;
+  }
   if (sk == SK_DYNAMIC) {
     const int64_t want = (256 * 1024) / esz;
     a.ticket_m = std::max<int64_t>(1, (want + (int64_t)p_team * chunk - 1) / ((int64_t)p_team * chunk));
@@ -890,6 +943,7 @@ extern "C" upir_status upir_loop_exec(upir_spmd s, const upir_loop_desc *l, cons
 static upir_status tile_sched(const upir_loop_desc *l, int &sk, int64_t &chunk) {
   upir_status st = resolve_sched(l->policy, l->chunk, sk, chunk);
   if (st != UPIR_OK) return st;
+  if (sk == SK_GUIDED) return fail(UPIR_E_UNSUPPORTED, "guided tile loops are not built (static / dynamic)");
   if (sk == SK_STATIC_BLOCK) chunk = 1;
   return UPIR_OK;
 }

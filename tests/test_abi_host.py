@@ -89,8 +89,8 @@ def test_validation_error_paths():
     assert _st(U.spmd_desc(0, 256), loop, U.BODY_REDUCE, [red]) == U.E_INVALID
     assert _st(U.spmd_desc(1, 0), loop, U.BODY_REDUCE, [red]) == U.E_INVALID
     assert _st(U.spmd_desc(1, 1024), loop, U.BODY_REDUCE, [red]) == U.OK
-    # guided is valid UPIR but not built
-    assert _st(ok_spmd, U.loop_desc(0, 10, policy=U.SCHED_GUIDED), U.BODY_REDUCE, [red]) == U.E_UNSUPPORTED
+    # guided is built for 1-D loops
+    assert _st(ok_spmd, U.loop_desc(0, 10, policy=U.SCHED_GUIDED), U.BODY_REDUCE, [red]) == U.OK
     assert _st(ok_spmd, U.loop_desc(0, 10, policy=9), U.BODY_REDUCE, [red]) == U.E_INVALID
     # distribute(units) with several teams would replicate (reading c7)
     assert _st(ok_spmd, U.loop_desc(0, 10, distribute=U.DIST_UNITS), U.BODY_REDUCE, [red]) == U.E_INVALID

@@ -20,7 +20,8 @@ GEOMS = [(1, 1), (3, 37), (7, 64), (148, 256), (5, 1024)]
 SCHEDS = [(U.SCHED_STATIC, 0), (U.SCHED_STATIC, 1), (U.SCHED_STATIC, 2), (U.SCHED_STATIC, 3),
           (U.SCHED_STATIC, 64), (U.SCHED_DYNAMIC, 0), (U.SCHED_DYNAMIC, 5), (U.SCHED_DYNAMIC, 100),
           (U.SCHED_RUNTIME, 0)]
-OPOL = {U.SCHED_STATIC: oracle.STATIC, U.SCHED_DYNAMIC: oracle.DYNAMIC, U.SCHED_RUNTIME: oracle.RUNTIME}
+OPOL = {U.SCHED_STATIC: oracle.STATIC, U.SCHED_DYNAMIC: oracle.DYNAMIC, U.SCHED_RUNTIME: oracle.RUNTIME,
+        U.SCHED_GUIDED: oracle.GUIDED}
 
 
 @pytest.fixture(scope="module")
@@ -211,3 +212,39 @@ def test_synth_fill_matches_host_generator(ctx):
     U.upir_data_unmap(ctx, m)
     U.upir_sync(ctx)
     assert h.tolist() == synth.GOLDEN[(6, "i64")]
+
+
+# ---- guided ------------------------------------------------
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("teams,units", [(1, 32), (3, 37), (148, 256)])
+@pytest.mark.parametrize("chunk", [0, 1, 5, 1000])
+def test_guided_reduce_parity_and_chunks(ctx, path, teams, units, chunk):
+    n = 60_013
+    x = synth.i64_sym(6, 0, n)
+    with upir_path(path):
+        (s, mx), (team, unit, hits) = run_reduce(ctx, x, [U.OP_SUM, U.OP_MAX], teams, units,
+                                                 U.SCHED_GUIDED, chunk, trace=True)
+    p = teams * units
+    assert s == oracle.reduce_i64(oracle.SUM, x, policy=oracle.GUIDED, chunk=chunk, p=p)
+    assert mx == int(x.max())
+    assert (hits == 1).all()
+    # chunk boundaries are the oracle's guided sequence: every oracle chunk is
+    # executed by one unit (reading c8: the assignment itself is decided at run time)
+    g = flat_unit(team, unit, units, U.DIST_TEAMS_UNITS)
+    bounds = sorted(lo for u in range(p) for lo, hi in oracle.schedule_chunks(oracle.GUIDED, chunk, n, p, u)
+                    ) + [n] if p <= 4096 else None
+    if bounds is not None:
+        for a_, b_ in zip(bounds[:-1], bounds[1:]):
+            assert (g[a_:b_] == g[a_]).all()
+
+
+@pytest.mark.parametrize("path", PATHS)
+def test_guided_axpy_f32(ctx, path):
+    n = 40_000
+    x = synth.f32_sym(1, 0, n)
+    y = synth.f32_sym(2, 0, n)
+    with upir_path(path):
+        yy, s, _ = run_axpy(ctx, 0.5, x, y, 8, 128, U.SCHED_GUIDED, 3, sum_=True)
+    ref = oracle.axpy(0.5, x, y)
+    assert np.abs(yy - ref).max() <= 1e-5 * np.abs(ref).max()
+    assert abs(s - oracle.reduce_f32(oracle.SUM, yy)) <= 1e-5 * np.abs(yy).sum()

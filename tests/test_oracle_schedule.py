@@ -146,9 +146,36 @@ def test_dynamic_chunk_boundaries():
     assert allchunks == [(k * c, min((k + 1) * c, T)) for k in range((T + c - 1) // c)]
 
 
-def test_guided_is_rejected():
-    with pytest.raises(ValueError):
-        oracle.schedule_chunks(oracle.GUIDED, 1, 10, 2, 0)
+# ---- guided ---------------------------------------------
+def _guided_bounds(T, p, c):
+    return sorted(lo for u in range(p) for lo, hi in oracle.schedule_chunks(oracle.GUIDED, c, T, p, u))
+
+
+def test_guided_boundaries_vs_libgomp():
+    # independent runtime: every run start libgomp shows is a chunk boundary of
+    # the oracle, and across 12 runs most boundaries are observed
+    data = json.load(open(os.path.join(GOLDEN, "libgomp_guided.json")))
+    seen = total = 0
+    for T, p, c, starts in data["cases"]:
+        b = set(_guided_bounds(T, p, c))
+        assert set(starts) <= b, (T, p, c)
+        seen += len(starts)
+        total += len(b)
+    assert seen >= 0.6 * total
+
+
+def test_guided_partition_and_special_cases():
+    for T in (0, 1, 10, 97, 1000):
+        for p in (1, 2, 5, 16):
+            for c in (0, 1, 3, 50):
+                _check_partition(oracle.GUIDED, c, T, p)
+    # p = 1: one chunk [0, T); c >= T: one chunk
+    assert oracle.schedule_chunks(oracle.GUIDED, 1, 37, 1, 0) == [(0, 37)]
+    assert _guided_bounds(37, 4, 100) == [0]
+    # first chunk is ceil(T/p); chunk sizes never grow
+    b = _guided_bounds(1000, 7, 1) + [1000]
+    sizes = [b[i + 1] - b[i] for i in range(len(b) - 1)]
+    assert sizes[0] == 143 and all(sizes[i] >= sizes[i + 1] for i in range(len(sizes) - 1))
 
 
 def test_tile_owner_static1_round_robin():
