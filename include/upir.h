@@ -227,10 +227,17 @@ typedef struct {
  *            (kind::tf32, hi/lo split in shared memory), teams of exactly 384
  *            units.  The tile loop (128 x 256 tiles) runs over the teams;
  *            other unit counts are rejected, never clamped.
+ *  MATVEC  : y[i] = sum_k A[i][k] * x[k] over the loop's rows i (collapse 1,
+ *            step 1, the paper's fourth kernel); in0 = A (M x K
+ *            fp32, row pitch ld[0]), in1 = x (K), out = y (M); dims = (K, M).
+ *            distribute(teams): rows over teams, the k-loop over the team's
+ *            units with schedule(static, inner_chunk, default 4) and a
+ *            reduction(+); distribute(teams,units) / (units): rows over the
+ *            flat units, k sequential per unit.
  * The element index used by a body is the induction value itself (global
  * index; for distributed maps the runtime subtracts the local offset). */
 typedef enum { UPIR_BODY_AXPY = 0, UPIR_BODY_REDUCE = 1, UPIR_BODY_JACOBI5 = 2,
-               UPIR_BODY_MATMUL = 3 } upir_body_kind;
+               UPIR_BODY_MATMUL = 3, UPIR_BODY_MATVEC = 4 } upir_body_kind;
 typedef struct {
     int32_t kind;            /* upir_body_kind */
     int32_t dtype;           /* element type of in0 (matmul: of A and B) */

@@ -63,6 +63,7 @@ def lib():
             "orc_matmul_rows": (i32, [i64, i64, i64, vp, vp, vp, i64, vp]),
             "orc_tile_owner": (i32, [i64, i64, i64, i64, i32, i64, i64, vp]),
             "orc_tiled_owner": (i64, [i64, i64, i64, i64, i64, i64, i32, i64, i64, i64, i64, vp, vp]),
+            "orc_matvec": (i32, [i64, i64, i64, i64, i64, vp, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -222,6 +223,18 @@ def matmul_rows(A, B, rows):
     _check(lib().orc_matmul_rows(M, N, K, _p(A), _p(B), _p(rows), len(rows), _p(C)),
            "matmul_rows")
     return C
+
+
+def matvec(A, x, lb=0, ub=None, y_in=None):
+    """y = A x over rows [lb, ub) in fp64 (NEXT #2 body)."""
+    A = np.ascontiguousarray(A, dtype=np.float32)
+    x = np.ascontiguousarray(x, dtype=np.float32)
+    M, K = A.shape
+    ub = M if ub is None else ub
+    yi = np.zeros(M) if y_in is None else np.ascontiguousarray(y_in, dtype=np.float64)
+    y = np.zeros(M, dtype=np.float64)
+    _check(lib().orc_matvec(M, K, K, lb, ub, _p(A), _p(x), _p(yi), _p(y)), "matvec")
+    return y
 
 
 def matmul(A, B):

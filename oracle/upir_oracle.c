@@ -449,3 +449,20 @@ int64_t orc_tiled_owner(int64_t lb0, int64_t ub0, int64_t lb1, int64_t ub1, int6
     free(towner);
     return nt;
 }
+
+/* ---- matvec (PAPER.md:1217 'matrix-vector
+ * multiplication', sizes PAPER.md:1405-1430) ----------------------------------
+ * y[i] = sum_k A[i][k] * x[k] for i in [lb, ub), row-major A with leading
+ * dimension lda, fp64 from the fp32 inputs; rows outside [lb, ub) keep y_in. */
+int orc_matvec(int64_t M, int64_t K, int64_t lda, int64_t lb, int64_t ub, const float *A,
+               const float *x, const double *y_in, double *y)
+{
+    if (lb < 0 || ub > M || lda < K) return -1;
+    for (int64_t i = 0; i < M; ++i) y[i] = y_in[i];
+    for (int64_t i = lb; i < ub; ++i) {
+        double acc = 0.0;
+        for (int64_t k = 0; k < K; ++k) acc += (double)A[i * lda + k] * (double)x[k];
+        y[i] = acc;
+    }
+    return 0;
+}

@@ -95,6 +95,21 @@ bool jacobi_supported_tile(int bm, int bn);
 cudaError_t launch_jacobi_tma(const JacobiArgs &a, const void *tmc, const void *tmh, int teams, int units, int bm,
                               int bn, bool trace, cudaStream_t s);
 
+// ---- matvec (NEXT #2) -------------------------------------------------------------
+struct MatvecArgs {
+  const float *A, *x;
+  float *y;
+  int64_t K, lda;
+  int64_t lb, T;                // rows [lb, lb + T)
+  int32_t sched, distribute;
+  int64_t chunk;
+  int32_t inner_chunk;
+  unsigned long long *dyn_counter;
+  unsigned int *done;
+  int32_t *trace;               // [team | unit | hits] x T, or null
+};
+cudaError_t launch_matvec(const MatvecArgs &a, int teams, int units, cudaStream_t s);
+
 // ---- matmul (tcgen05) ------------------------------------------------------------
 struct MatmulArgs {
   const void *A, *B;

@@ -636,6 +636,7 @@ static int body_dtype_ok(int kind, int dtype) {
     case UPIR_BODY_REDUCE: return dtype == UPIR_I64 || dtype == UPIR_F32;
     case UPIR_BODY_JACOBI5: return dtype == UPIR_F32;
     case UPIR_BODY_MATMUL: return dtype == UPIR_BF16 || dtype == UPIR_F32;
+    case UPIR_BODY_MATVEC: return dtype == UPIR_F32;
   }
   return 0;
 }
@@ -657,13 +658,21 @@ static upir_status validate_loop(const upir_spmd_desc *sd, const upir_loop_desc 
   const bool tiled = l->collapse == 2 && (l->tile[0] > 0 || l->tile[1] > 0);
   if (l->distribute == UPIR_DIST_UNITS && sd->num_teams > 1 && !tiled)
     return fail(UPIR_E_INVALID, "distribute(units) with num_teams > 1 would replicate the loop per team (reading c7)");
-  if (kind < UPIR_BODY_AXPY || kind > UPIR_BODY_MATMUL) return fail(UPIR_E_INVALID, "unknown body kind %d", kind);
+  if (kind < UPIR_BODY_AXPY || kind > UPIR_BODY_MATVEC) return fail(UPIR_E_INVALID, "unknown body kind %d", kind);
   if (dtype >= 0 && !body_dtype_ok(kind, dtype)) return fail(UPIR_E_INVALID, "dtype %d not valid for body %d", dtype, kind);
   if (n_reds < 0 || n_reds > 2) return fail(UPIR_E_INVALID, "n_reds=%d outside [0,2]", n_reds);
   if (n_reds > 0 && !reds) return fail(UPIR_E_INVALID, "reds is NULL");
   if (kind == UPIR_BODY_REDUCE && n_reds == 0) return fail(UPIR_E_INVALID, "REDUCE body needs a reduction");
-  if ((kind == UPIR_BODY_JACOBI5 || kind == UPIR_BODY_MATMUL) && n_reds > 0)
+  if ((kind == UPIR_BODY_JACOBI5 || kind == UPIR_BODY_MATMUL || kind == UPIR_BODY_MATVEC) && n_reds > 0)
     return fail(UPIR_E_INVALID, "reductions are not defined for this body");
+  if (kind == UPIR_BODY_MATVEC) {
+    if (l->collapse != 1 || l->step[0] != 1) return fail(UPIR_E_INVALID, "MATVEC is a collapse(1) row loop with step 1");
+    if (l->distribute == UPIR_DIST_UNITS && sd->num_teams > 1)
+      return fail(UPIR_E_INVALID, "distribute(units) with num_teams > 1 would replicate rows (reading c7)");
+    if (l->distribute == UPIR_DIST_TEAMS && l->inner_policy != UPIR_SCHED_STATIC)
+      return fail(UPIR_E_UNSUPPORTED, "the k-loop inside a team is schedule(static, c) over units");
+    return UPIR_OK;
+  }
   for (int r = 0; r < n_reds; ++r) {
     if (reds[r].op < UPIR_OP_SUM || reds[r].op > UPIR_OP_MIN) return fail(UPIR_E_INVALID, "bad reduction op");
     if (reds[r].dtype != UPIR_I64 && reds[r].dtype != UPIR_F32) return fail(UPIR_E_INVALID, "reduction dtype must be I64 or F32");
@@ -914,6 +923,7 @@ static upir_status exec_stream(upir_spmd s, const upir_loop_desc *l, const upir_
 }
 
 static upir_status exec_jacobi(upir_spmd s, const upir_loop_desc *l, const upir_body *b, upir_map trace);
+static upir_status exec_matvec(upir_spmd s, const upir_loop_desc *l, const upir_body *b, upir_map trace);
 static upir_status exec_matmul(upir_spmd s, const upir_loop_desc *l, const upir_body *b, upir_map trace);
 
 extern "C" upir_status upir_loop_exec(upir_spmd s, const upir_loop_desc *l, const upir_body *b,
@@ -931,6 +941,7 @@ extern "C" upir_status upir_loop_exec(upir_spmd s, const upir_loop_desc *l, cons
     case UPIR_BODY_REDUCE: st = exec_stream(s, l, b, reds, n_reds, trace); break;
     case UPIR_BODY_JACOBI5: st = exec_jacobi(s, l, b, trace); break;
     case UPIR_BODY_MATMUL: st = exec_matmul(s, l, b, trace); break;
+    case UPIR_BODY_MATVEC: st = exec_matvec(s, l, b, trace); break;
   }
   if (st != UPIR_OK) return st;
   // implicit barrier at the end of a worksharing loop: stream
@@ -1019,6 +1030,56 @@ static upir_status exec_jacobi(upir_spmd s, const upir_loop_desc *l, const upir_
   c->launches++;
   return UPIR_OK;
 }
+static upir_status exec_matvec(upir_spmd s, const upir_loop_desc *l, const upir_body *b, upir_map trace) {
+  upir_ctx c = s->ctx;
+  const upir_spmd_desc &sd = s->d;
+  upir_status st;
+  if ((st = check_map(c, b->in0, "in0 (A)")) != UPIR_OK) return st;
+  if ((st = check_map(c, b->in1, "in1 (x)")) != UPIR_OK) return st;
+  if ((st = check_map(c, b->out, "out (y)")) != UPIR_OK) return st;
+  const int64_t K = b->dims[0], M = b->dims[1], lda = b->ld[0];
+  if (K < 1 || M < 1 || lda < K) return fail(UPIR_E_INVALID, "MATVEC needs dims = (K, M) >= 1 and ld[0] >= K");
+  if ((int64_t)b->in0->dev_bytes < ((M - 1) * lda + K) * 4 || (int64_t)b->in1->dev_bytes < K * 4 ||
+      (int64_t)b->out->dev_bytes < M * 4)
+    return fail(UPIR_E_INVALID, "MATVEC maps smaller than A (M x K), x (K) and y (M)");
+  int64_t T;
+  upir_loop_normalize(l, &T, nullptr);
+  const int64_t lb = l->lb[0];
+  if (lb < 0 || lb + T > M) return fail(UPIR_E_INVALID, "MATVEC rows must lie in [0, M)");
+  int sk;
+  int64_t chunk;
+  if ((st = resolve_sched(l->policy, l->chunk, sk, chunk)) != UPIR_OK) return st;
+  if (sk == SK_GUIDED) return fail(UPIR_E_UNSUPPORTED, "guided MATVEC row loops are not built");
+  if (sk == SK_DYNAMIC && l->distribute != UPIR_DIST_TEAMS)
+    return fail(UPIR_E_UNSUPPORTED, "dynamic MATVEC rows are scheduled over teams only");
+  if (sk == SK_STATIC_BLOCK) chunk = 1;
+  MatvecArgs a;
+  memset(&a, 0, sizeof a);
+  a.A = (const float *)b->in0->dev;
+  a.x = (const float *)b->in1->dev;
+  a.y = (float *)b->out->dev;
+  a.K = K;
+  a.lda = lda;
+  a.lb = lb;
+  a.T = T;
+  a.sched = sk;
+  a.chunk = chunk;
+  a.distribute = l->distribute;
+  a.inner_chunk = l->inner_chunk > 0 ? (int)l->inner_chunk : 4;
+  a.dyn_counter = c->dyn;
+  a.done = c->done;
+  if (trace) {
+    if ((st = check_map(c, trace, "trace")) != UPIR_OK) return st;
+    if ((int64_t)trace->dev_bytes < 3 * T * 4) return fail(UPIR_E_INVALID, "trace map needs 3*T int32");
+    a.trace = (int32_t *)trace->dev;
+  }
+  if (T == 0) return UPIR_OK;
+  cudaError_t e = launch_matvec(a, sd.num_teams, sd.num_units, c->compute);
+  if (e != cudaSuccess) return fail(UPIR_E_CUDA, "MATVEC launch failed: %s", cudaGetErrorString(e));
+  c->launches++;
+  return UPIR_OK;
+}
+
 static upir_status exec_matmul(upir_spmd s, const upir_loop_desc *l, const upir_body *b, upir_map trace) {
   upir_ctx c = s->ctx;
   const upir_spmd_desc &sd = s->d;

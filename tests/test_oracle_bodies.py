@@ -241,3 +241,26 @@ def test_matmul_rank1_closed_form_and_rows():
     assert np.allclose(C, K * np.outer(u.astype(np.float64), v.astype(np.float64)), rtol=0, atol=1e-12)
     rows = np.array([11, 0, 5])
     assert (oracle.matmul_rows(A, B, rows) == C[rows]).all()
+
+
+# ---- matvec (NEXT #2) ---------------------------------------------------------------
+def test_matvec_numpy_and_identity():
+    A = synth.f32_sym(3, 0, 41 * 67).reshape(41, 67)
+    x = synth.f32_sym(1, 0, 67)
+    assert np.abs(oracle.matvec(A, x) - A.astype(np.float64) @ x.astype(np.float64)).max() <= 1e-13
+    eye = np.eye(16, dtype=np.float32)
+    v = synth.f32_sym(2, 0, 16)
+    assert (oracle.matvec(eye, v) == v).all()
+
+
+def test_matvec_small_integers_rows_and_rank1():
+    rng = np.random.default_rng(3)
+    A = rng.integers(-3, 4, (30, 50)).astype(np.float32)
+    x = rng.integers(-3, 4, 50).astype(np.float32)
+    y0 = np.full(30, 9.0)
+    y = oracle.matvec(A, x, lb=4, ub=20, y_in=y0)
+    assert (y[4:20] == (A.astype(np.int64) @ x.astype(np.int64))[4:20]).all()
+    assert (y[:4] == 9).all() and (y[20:] == 9).all()
+    u = synth.f32_sym(1, 0, 12)
+    B = np.repeat(u[:, None], 40, axis=1)            # rows u_i * 1^T
+    assert np.allclose(oracle.matvec(B, np.ones(40, np.float32)), 40 * u.astype(np.float64), rtol=0, atol=1e-12)
