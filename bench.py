@@ -241,7 +241,8 @@ def run_upir(args):
     # the other loop bodies of the path, each timed on its own (single GPU)
     if world == 1 and not args.no_kernels and args.workload == "reduce":
         res["kernels"] = {}
-        for name, fn in (("axpy", bench_axpy), ("jacobi", bench_jacobi), ("matmul", bench_matmul)):
+        for name, fn in (("axpy", bench_axpy), ("jacobi", bench_jacobi), ("matmul", bench_matmul),
+                         ("matvec", bench_matvec)):
             try:
                 res["kernels"][name] = fn(args, U, ctx, stream, peaks, peak_src)
             except Exception as e:   # report, never hide
@@ -500,6 +501,37 @@ def bench_jacobi(args, U, ctx, stream, peaks, peak_src, ny=8192, nx=8192, S=100)
             "roofline": {"achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                          "algorithmic_bytes_per_lup": 8, "peak_source": peak_src,
                          "traffic": ncu_traffic("jacobi")}}
+
+
+def bench_matvec(args, U, ctx, stream, peaks, peak_src, n=16384):
+    """NEXT #2: matvec y = A x at the paper's largest size N = 16384
+    (PAPER.md:1430), rows static,1 over 592 teams, k static,4 over 256 units."""
+    import torch
+    A = torch.empty(n * n, dtype=torch.float32, device="cuda")
+    x = torch.empty(n, dtype=torch.float32, device="cuda")
+    y = torch.empty(n, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    ma, mx, my = U.upir_data_adopt(ctx, A), U.upir_data_adopt(ctx, x), U.upir_data_adopt(ctx, y)
+    U.upir_synth_fill(ctx, ma, 1, 3)
+    U.upir_synth_fill(ctx, mx, 1, 1)
+    out = {}
+    for teams, units in ((592, 256), (296, 512)):
+        s = U.upir_spmd_launch(ctx, U.spmd_desc(teams, units))
+        loop = U.loop_desc(0, n, chunk=1, distribute=U.DIST_TEAMS, inner_chunk=4)
+        body = U.body(U.BODY_MATVEC, U.F32, in0=ma, in1=mx, out=my, ld=(n, 0, 0), dims=(n, n, 0))
+        for _ in range(3):
+            U.upir_loop_exec(s, loop, body)
+        ms = _time_graph(U, ctx, stream, lambda: U.upir_loop_exec(s, loop, body), 10)
+        U.upir_spmd_end(s)
+        gbs = 4.0 * n * n / (ms / 1e3) / 1e9
+        out[f"{teams}x{units}"] = {"ms": ms, "GB/s": gbs, "frac": gbs / float(peaks["hbm_gbs"])}
+    for m in (my, mx, ma):
+        U.upir_data_unmap(ctx, m)
+    U.upir_sync(ctx)
+    del A
+    return {"workload": f"matvec {n}x{n} fp32 (PAPER.md:1430 size), rows static,1 over teams, "
+                        "k static,4 over units + reduction(+); 4 B of A per iteration", "bound": "hbm",
+            "peak_source": peak_src, "paper_v100_end_to_end_ms": 583.45, **out}
 
 
 def bench_matmul(args, U, ctx, stream, peaks, peak_src, n=8192):

@@ -128,6 +128,14 @@ upir_status upir_data_adopt(upir_ctx ctx, void *dev_ptr, size_t bytes,
 upir_status upir_data_unmap(upir_ctx ctx, upir_map map);
 /* data_update: direction 0 = forward (host -> device), 1 = backward. */
 upir_status upir_data_update(upir_ctx ctx, upir_map map, int direction);
+/* data_update of an array section (Fig. 5 data-section [lo:len], stride 1):
+ * bytes [byte_offset, byte_offset + bytes) of the map's LOCAL buffer (and of
+ * the matching host range).  A forward update makes only LATER compute work
+ * wait for THIS copy, so a loop over section k overlaps the copy of section
+ * k+1 (chunk-pipelined map: overlap of data movement and
+ * computation). */
+upir_status upir_data_update_section(upir_ctx ctx, upir_map map, int64_t byte_offset, int64_t bytes,
+                                     int direction);
 /* Device pointer of the local buffer, the number of local elements (rows *
  * row_elems, halo included) and the global element index of its first
  * element. */
@@ -305,9 +313,16 @@ upir_status upir_reduce(upir_ctx ctx, int32_t op, int32_t dtype, const void *dev
  *                   records a token after the work enqueued so far; *token out.
  *   WAIT          : step 'wait-release': the host waits for *token and frees it.
  *   HALO          : send/recv of halo rows of a BLOCK-distributed map with
- *                   ranks r-1 / r+1 (Fig. 7 send/recv), in stream order. */
+ *                   ranks r-1 / r+1 (Fig. 7 send/recv), in stream order.
+ *                   With token != NULL (*token == NULL on entry) it is the
+ *                   async 'arrive-compute' step: the exchange runs on the copy
+ *                   stream, overlapping later compute work, and *token
+ *                   receives its completion event.
+ *   JOIN          : async 'wait-release' on the DEVICE: later compute work
+ *                   waits for *token (no host block); the token is freed.
+ *                   UPIR_E_SYNC without a token. */
 typedef enum { UPIR_SYNC_BARRIER = 0, UPIR_SYNC_WORLD_BARRIER = 1, UPIR_SYNC_ARRIVE = 2,
-               UPIR_SYNC_WAIT = 3, UPIR_SYNC_HALO = 4 } upir_sync_kind;
+               UPIR_SYNC_WAIT = 3, UPIR_SYNC_HALO = 4, UPIR_SYNC_JOIN = 5 } upir_sync_kind;
 upir_status upir_sync(upir_ctx ctx, int32_t kind, upir_map halo_map, upir_event *token);
 
 /* ---- CUDA-graph capture of a loop sequence (e.g. 100 Jacobi sweeps) ------ */

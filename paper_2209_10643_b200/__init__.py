@@ -147,6 +147,10 @@ def upir_data_update(ctx, m, direction):
     check(lib().upir_data_update(ctx, m, direction))
 
 
+def upir_data_update_section(ctx, m, byte_offset, nbytes, direction):
+    check(lib().upir_data_update_section(ctx, m, byte_offset, nbytes, direction))
+
+
 def upir_data_device_ptr(m):
     p, n, off = ctypes.c_void_p(), ctypes.c_int64(), ctypes.c_int64()
     check(lib().upir_data_device_ptr(m, ctypes.byref(p), ctypes.byref(n), ctypes.byref(off)))
@@ -217,7 +221,12 @@ def upir_reduce(ctx, op, dtype, dev_in, count, dev_out, scope=_abi.SCOPE_DEVICE)
     check(lib().upir_reduce(ctx, op, dtype, dev_ptr(dev_in), count, dev_ptr(dev_out), scope))
 
 
-def upir_sync(ctx, kind=_abi.SYNC_BARRIER, halo_map=None, token=None):
+def upir_sync(ctx, kind=_abi.SYNC_BARRIER, halo_map=None, token=None, async_=False):
+    """Returns the token (ARRIVE, async HALO).  HALO is synchronous unless
+    async_=True (then the C call receives a token out-param)."""
+    if kind == _abi.SYNC_HALO and not async_:
+        check(lib().upir_sync(ctx, kind, halo_map, None))
+        return None
     tok = token if token is not None else ctypes.c_void_p()
     check(lib().upir_sync(ctx, kind, halo_map, ctypes.byref(tok)))
     return tok

@@ -23,7 +23,7 @@ NOWAIT = 1
 BODY_AXPY, BODY_REDUCE, BODY_JACOBI5, BODY_MATMUL, BODY_MATVEC = 0, 1, 2, 3, 4
 OP_SUM, OP_MAX, OP_MIN = 0, 1, 2
 SCOPE_DEVICE, SCOPE_WORLD = 0, 1
-SYNC_BARRIER, SYNC_WORLD_BARRIER, SYNC_ARRIVE, SYNC_WAIT, SYNC_HALO = 0, 1, 2, 3, 4
+SYNC_BARRIER, SYNC_WORLD_BARRIER, SYNC_ARRIVE, SYNC_WAIT, SYNC_HALO, SYNC_JOIN = 0, 1, 2, 3, 4, 5
 
 i32, i64, u32, u64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64
 vp = ctypes.c_void_p
@@ -70,6 +70,7 @@ _SIGS = {
     "upir_data_adopt": (i32, [vp, vp, ctypes.c_size_t, ctypes.POINTER(Dist), ctypes.POINTER(vp)]),
     "upir_data_unmap": (i32, [vp, vp]),
     "upir_data_update": (i32, [vp, vp, ctypes.c_int]),
+    "upir_data_update_section": (i32, [vp, vp, i64, i64, ctypes.c_int]),
     "upir_data_device_ptr": (i32, [vp, ctypes.POINTER(vp), ctypes.POINTER(i64), ctypes.POINTER(i64)]),
     "upir_dist_owned_rows": (i32, [i64, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]),
     "upir_halo_plan": (i32, [i64, i32, i32, i32, ctypes.POINTER(i64)]),

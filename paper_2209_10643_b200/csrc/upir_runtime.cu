@@ -515,6 +515,29 @@ extern "C" upir_status upir_data_update(upir_ctx c, upir_map m, int direction) {
   return copy_to_compute(c);
 }
 
+extern "C" upir_status upir_data_update_section(upir_ctx c, upir_map m, int64_t off, int64_t bytes, int direction) {
+  if (!c || !m || m->ctx != c || !m->owned || !m->host) return fail(UPIR_E_INVALID, "bad map");
+  if (direction != 0 && direction != 1) return fail(UPIR_E_INVALID, "direction must be 0 or 1");
+  if (off < 0 || bytes < 0 || off + bytes > (int64_t)m->dev_bytes)
+    return fail(UPIR_E_INVALID, "section [%lld, +%lld) outside the local buffer (%zu B)", (long long)off,
+                (long long)bytes, m->dev_bytes);
+  if (bytes == 0) return UPIR_OK;
+  // host offset of local byte 0: the first local row of a BLOCK map
+  size_t ho, dof, len;
+  map_range(m, false, ho, dof, len);
+  char *h = (char *)m->host + ho - dof + off;
+  upir_status st = compute_to_copy(c);
+  if (st != UPIR_OK) return st;
+  if (direction == 0) {
+    CUDA_TRY(cudaMemcpyAsync((char *)m->dev + off, h, (size_t)bytes, cudaMemcpyHostToDevice, c->copy));
+    c->h2d_bytes += bytes;
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(h, (char *)m->dev + off, (size_t)bytes, cudaMemcpyDeviceToHost, c->copy));
+    c->d2h_bytes += bytes;
+  }
+  return copy_to_compute(c);
+}
+
 extern "C" upir_status upir_data_device_ptr(upir_map m, void **dptr, int64_t *local_elems, int64_t *global_offset) {
   if (!m) return fail(UPIR_E_INVALID, "map is NULL");
   if (dptr) *dptr = m->dev;
@@ -1202,7 +1225,7 @@ extern "C" upir_status upir_reduce(upir_ctx c, int32_t op, int32_t dtype, const 
   return UPIR_OK;
 }
 
-static upir_status halo_exchange(upir_ctx c, upir_map m) {
+static upir_status halo_exchange(upir_ctx c, upir_map m, cudaStream_t strm) {
   if (m->dist.pattern != UPIR_PATTERN_BLOCK || m->dist.halo_rows < 1)
     return fail(UPIR_E_INVALID, "HALO needs a BLOCK-distributed map with halo_rows >= 1");
   if (c->nranks == 1) return UPIR_OK;
@@ -1215,12 +1238,12 @@ static upir_status halo_exchange(upir_ctx c, upir_map m) {
   // Fig. 7 send/recv with rank units, in stream order before the next sweep
   NCCL_TRY(ncclGroupStart());
   if (plan[1] > plan[0]) {
-    NCCL_TRY(ncclSend(at(plan[0]), (size_t)((plan[1] - plan[0]) * rb), ncclChar, c->rank - 1, c->comm, c->compute));
-    NCCL_TRY(ncclRecv(at(plan[2]), (size_t)((plan[3] - plan[2]) * rb), ncclChar, c->rank - 1, c->comm, c->compute));
+    NCCL_TRY(ncclSend(at(plan[0]), (size_t)((plan[1] - plan[0]) * rb), ncclChar, c->rank - 1, c->comm, strm));
+    NCCL_TRY(ncclRecv(at(plan[2]), (size_t)((plan[3] - plan[2]) * rb), ncclChar, c->rank - 1, c->comm, strm));
   }
   if (plan[5] > plan[4]) {
-    NCCL_TRY(ncclSend(at(plan[4]), (size_t)((plan[5] - plan[4]) * rb), ncclChar, c->rank + 1, c->comm, c->compute));
-    NCCL_TRY(ncclRecv(at(plan[6]), (size_t)((plan[7] - plan[6]) * rb), ncclChar, c->rank + 1, c->comm, c->compute));
+    NCCL_TRY(ncclSend(at(plan[4]), (size_t)((plan[5] - plan[4]) * rb), ncclChar, c->rank + 1, c->comm, strm));
+    NCCL_TRY(ncclRecv(at(plan[6]), (size_t)((plan[7] - plan[6]) * rb), ncclChar, c->rank + 1, c->comm, strm));
   }
   NCCL_TRY(ncclGroupEnd());
   return UPIR_OK;
@@ -1279,7 +1302,33 @@ extern "C" upir_status upir_sync(upir_ctx c, int32_t kind, upir_map halo_map, up
       if (!halo_map) return fail(UPIR_E_INVALID, "HALO needs a map");
       upir_status st = check_map(c, halo_map, "halo map");
       if (st != UPIR_OK) return st;
-      return halo_exchange(c, halo_map);
+      if (!token) return halo_exchange(c, halo_map, c->compute);
+      // async arrive-compute: exchange on the copy stream
+      upir_event ev = new upir_event_s();
+      if (cudaEventCreateWithFlags(&ev->ev, cudaEventDisableTiming) != cudaSuccess) {
+        delete ev;
+        return fail(UPIR_E_CUDA, "event create failed");
+      }
+      st = compute_to_copy(c);
+      if (st == UPIR_OK) st = halo_exchange(c, halo_map, c->copy);
+      if (st != UPIR_OK) {
+        cudaEventDestroy(ev->ev);
+        delete ev;
+        return st;
+      }
+      CUDA_TRY(cudaEventRecord(ev->ev, c->copy));
+      *token = ev;
+      return UPIR_OK;
+    }
+    case UPIR_SYNC_JOIN: {
+      if (!token || !*token) return fail(UPIR_E_SYNC, "JOIN without a matching async token");
+      upir_event ev = *token;
+      cudaError_t e = cudaStreamWaitEvent(c->compute, ev->ev, 0);
+      cudaEventDestroy(ev->ev);   // destruction is deferred until the event completes
+      delete ev;
+      *token = nullptr;
+      if (e != cudaSuccess) return fail(UPIR_E_CUDA, "join failed: %s", cudaGetErrorString(e));
+      return UPIR_OK;
     }
   }
   return fail(UPIR_E_INVALID, "unknown sync kind %d", kind);

@@ -191,3 +191,84 @@ def test_c1_axpy_sum_1e6(ctx, teams, units):
     assert (hits == 1).all()
     g = team.astype(np.int64) * units + unit
     assert (g == oracle.owner_map(oracle.STATIC, 0, n, teams * units)).all()
+
+
+# ---- NEXT #1: async two-step sync and chunk-pipelined map -----------------------
+def test_pipelined_map_sections_reduce(ctx):
+    """map(alloc) + per-section forward update + a loop over that section:
+    the loop of section k waits only for copy k (overlap), results combine
+    with a device-scope upir_reduce."""
+    n, K = 1_000_000, 8
+    x = synth.i64_sym(6, 0, n)
+    m = U.upir_data_map(ctx, x, U.MAP_ALLOC)
+    parts = torch.zeros(K, dtype=torch.int64, device="cuda")
+    total = torch.zeros(1, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    s = U.upir_spmd_launch(ctx, U.spmd_desc(148, 256))
+    bounds = np.linspace(0, n, K + 1).astype(np.int64)
+    for k in range(K):
+        lo, hi = int(bounds[k]), int(bounds[k + 1])
+        U.upir_data_update_section(ctx, m, lo * 8, (hi - lo) * 8, 0)
+        U.upir_loop_exec(s, U.loop_desc(lo, hi), U.body(U.BODY_REDUCE, U.I64, in0=m),
+                         [U.reduction(U.OP_SUM, U.I64, parts.data_ptr() + 8 * k)])
+    U.upir_spmd_end(s)
+    U.upir_reduce(ctx, U.OP_SUM, U.I64, parts, K, total, U.SCOPE_DEVICE)
+    U.upir_sync(ctx)
+    assert total.item() == oracle.reduce_i64(oracle.SUM, x)
+    assert U.upir_ctx_stats(ctx)["h2d_bytes"] == x.nbytes
+    # backward section update
+    y = np.zeros(1000, np.int64)
+    my = U.upir_data_map(ctx, y, U.MAP_ALLOC)
+    U.upir_synth_fill(ctx, my, 2, 6)
+    U.upir_data_update_section(ctx, my, 800, 1600, 1)     # elements [100, 300)
+    U.upir_sync(ctx)
+    ref = synth.i64_sym(6, 0, 1000)
+    assert (y[100:300] == ref[100:300]).all() and (y[:100] == 0).all() and (y[300:] == 0).all()
+    with pytest.raises(U.UpirError):
+        U.upir_data_update_section(ctx, my, 7000, 2000, 0)
+    U.upir_data_unmap(ctx, my)
+    U.upir_data_unmap(ctx, m)
+    U.upir_sync(ctx)
+
+
+def test_async_halo_join_overlapped_sweeps(ctx):
+    """Per sweep: HALO arrive-compute (async) -> interior rows -> JOIN
+    (wait-release on the device) -> boundary rows; equals plain sweeps bit for
+    bit (world size 1: the exchange is empty, the ordering is exercised)."""
+    ny, nx, S = 70, 264, 6
+    g = synth.jacobi_init(ny, nx)
+    d = U.dist(ny, nx, 4, halo_rows=1)
+
+    def run(split):
+        a, b = g.copy(), g.copy()
+        ma = U.upir_data_map(ctx, a, U.MAP_TOFROM, d)
+        mb = U.upir_data_map(ctx, b, U.MAP_TOFROM, d)
+        s = U.upir_spmd_launch(ctx, U.spmd_desc(6, 256, U.TARGET_CLUSTER))
+        src, dst = ma, mb
+        for _ in range(S):
+            body = U.body(U.BODY_JACOBI5, U.F32, in0=src, out=dst, ld=(nx, 0, 0), dims=(ny, 0, 0))
+            if split:
+                tok = U.upir_sync(ctx, U.SYNC_HALO, halo_map=src, async_=True)
+                U.upir_loop_exec(s, U.loop_desc([2, 1], [ny - 2, nx - 1], tile=[16, 256], distribute=U.DIST_TEAMS,
+                                                inner_chunk=4), body)
+                U.upir_sync(ctx, U.SYNC_JOIN, token=tok)
+                for r0 in (1, ny - 2):
+                    U.upir_loop_exec(s, U.loop_desc([r0, 1], [r0 + 1, nx - 1], tile=[16, 256],
+                                                    distribute=U.DIST_TEAMS, inner_chunk=4), body)
+            else:
+                U.upir_sync(ctx, U.SYNC_HALO, halo_map=src)
+                U.upir_loop_exec(s, U.loop_desc([1, 1], [ny - 1, nx - 1], tile=[16, 256], distribute=U.DIST_TEAMS,
+                                                inner_chunk=4), body)
+            src, dst = dst, src
+        U.upir_spmd_end(s)
+        U.upir_data_unmap(ctx, mb)
+        U.upir_data_unmap(ctx, ma)
+        U.upir_sync(ctx)
+        return a if S % 2 == 0 else b
+
+    plain, split = run(False), run(True)
+    assert (plain == split).all()
+    assert np.abs(plain - oracle.jacobi5(g, S)).max() <= 1e-5
+    with pytest.raises(U.UpirError) as ei:
+        U.upir_sync(ctx, U.SYNC_JOIN)
+    assert ei.value.status == U.E_SYNC
