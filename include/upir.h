@@ -242,10 +242,15 @@ typedef struct {
  *            units with schedule(static, inner_chunk, default 4) and a
  *            reduction(+); distribute(teams,units) / (units): rows over the
  *            flat units, k sequential per unit.
+ *  STENCIL2D: out[i][j] = sum_{a,b in [-R,R]} w[a+R][b+R] * in[i+a][j+b]
+ *            (the paper's "2D stencil, filter size = 7"; the
+ *            weights are an input, reading c28); in0 = in, in1 = w (F x F
+ *            fp32, F = 2R+1 in {3,5,7}), out = out; ld[0] = row pitch,
+ *            dims = (ny, F).  Tiled like JACOBI5 (tiles 16x128 or 8x64).
  * The element index used by a body is the induction value itself (global
  * index; for distributed maps the runtime subtracts the local offset). */
 typedef enum { UPIR_BODY_AXPY = 0, UPIR_BODY_REDUCE = 1, UPIR_BODY_JACOBI5 = 2,
-               UPIR_BODY_MATMUL = 3, UPIR_BODY_MATVEC = 4 } upir_body_kind;
+               UPIR_BODY_MATMUL = 3, UPIR_BODY_MATVEC = 4, UPIR_BODY_STENCIL2D = 5 } upir_body_kind;
 typedef struct {
     int32_t kind;            /* upir_body_kind */
     int32_t dtype;           /* element type of in0 (matmul: of A and B) */

@@ -64,6 +64,7 @@ def lib():
             "orc_tile_owner": (i32, [i64, i64, i64, i64, i32, i64, i64, vp]),
             "orc_tiled_owner": (i64, [i64, i64, i64, i64, i64, i64, i32, i64, i64, i64, i64, vp, vp]),
             "orc_matvec": (i32, [i64, i64, i64, i64, i64, vp, vp, vp, vp]),
+            "orc_stencil2d": (i32, [i64, i64, i64, i64, vp, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -208,6 +209,18 @@ def jacobi5_window(ny, nx, S, wr0, wc0, win):
     out = np.zeros((wy, wx), dtype=np.float64)
     _check(lib().orc_jacobi5_window(ny, nx, S, wr0, wc0, wy, wx, _p(w), _p(out)),
            "jacobi5_window")
+    return out
+
+
+def stencil2d(grid, w, S=1):
+    """2-D filter stencil of radius R = (len(w)-1)/2 (NEXT #4; reading c28)."""
+    g = np.ascontiguousarray(grid, dtype=np.float32)
+    w = np.ascontiguousarray(w, dtype=np.float32)
+    F = w.shape[0]
+    assert w.shape == (F, F) and F % 2 == 1
+    ny, nx = g.shape
+    out = np.zeros((ny, nx), dtype=np.float64)
+    _check(lib().orc_stencil2d(ny, nx, (F - 1) // 2, S, _p(w), _p(g), _p(out)), "stencil2d")
     return out
 
 

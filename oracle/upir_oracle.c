@@ -466,3 +466,36 @@ int orc_matvec(int64_t M, int64_t K, int64_t lda, int64_t lb, int64_t ub, const 
     }
     return 0;
 }
+
+/* ---- 2-D filter stencil (the paper's "2D stencil,
+ * filter size = 7", whose weights and boundary are unstated:
+ * reading c28) -------------------------------------------------------------
+ * out[i][j] = sum_{a,b in [-R,R]} w[a+R][b+R] * in[i+a][j+b] for
+ * R <= i < ny-R, R <= j < nx-R; every other point copied unchanged.  S sweeps
+ * ping-pong, fp64 from the fp32 initial grid and weights. */
+int orc_stencil2d(int64_t ny, int64_t nx, int64_t R, int64_t S, const float *w, const float *init,
+                  double *out)
+{
+    if (ny < 1 || nx < 1 || R < 0 || S < 0) return -1;
+    int64_t F = 2 * R + 1;
+    size_t N = (size_t)ny * (size_t)nx;
+    double *a = (double *)malloc(N * sizeof(double));
+    double *b = (double *)malloc(N * sizeof(double));
+    if (!a || !b) { free(a); free(b); return -1; }
+    for (size_t e = 0; e < N; ++e) a[e] = (double)init[e];
+    memcpy(b, a, N * sizeof(double));
+    for (int64_t s = 0; s < S; ++s) {
+        for (int64_t i = R; i < ny - R; ++i)
+            for (int64_t j = R; j < nx - R; ++j) {
+                double acc = 0.0;
+                for (int64_t p = 0; p < F; ++p)
+                    for (int64_t q = 0; q < F; ++q)
+                        acc += (double)w[p * F + q] * a[(i + p - R) * nx + (j + q - R)];
+                b[i * nx + j] = acc;
+            }
+        double *t = a; a = b; b = t;
+    }
+    memcpy(out, a, N * sizeof(double));
+    free(a); free(b);
+    return 0;
+}

@@ -20,7 +20,7 @@ TARGET_GPU, TARGET_CLUSTER = 1, 2
 SCHED_STATIC, SCHED_DYNAMIC, SCHED_GUIDED, SCHED_RUNTIME, SCHED_AUTO = 0, 1, 2, 3, 4
 DIST_TEAMS, DIST_UNITS, DIST_TEAMS_UNITS = 1, 2, 3
 NOWAIT = 1
-BODY_AXPY, BODY_REDUCE, BODY_JACOBI5, BODY_MATMUL, BODY_MATVEC = 0, 1, 2, 3, 4
+BODY_AXPY, BODY_REDUCE, BODY_JACOBI5, BODY_MATMUL, BODY_MATVEC, BODY_STENCIL2D = 0, 1, 2, 3, 4, 5
 OP_SUM, OP_MAX, OP_MIN = 0, 1, 2
 SCOPE_DEVICE, SCOPE_WORLD = 0, 1
 SYNC_BARRIER, SYNC_WORLD_BARRIER, SYNC_ARRIVE, SYNC_WAIT, SYNC_HALO, SYNC_JOIN = 0, 1, 2, 3, 4, 5

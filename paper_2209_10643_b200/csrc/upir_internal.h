@@ -95,6 +95,22 @@ bool jacobi_supported_tile(int bm, int bn);
 cudaError_t launch_jacobi_tma(const JacobiArgs &a, const void *tmc, const void *tmh, int teams, int units, int bm,
                               int bn, bool trace, cudaStream_t s);
 
+// ---- 2-D filter stencil (NEXT #4) ---------------------------------------------------
+struct StencilArgs {
+  const float *in, *w;
+  float *out;
+  int64_t ld, row0, ny, nx;
+  int64_t lb0, ub0, lb1, ub1;
+  int64_t ti0, tj0, ntr, ntc;
+  int32_t sched, inner_chunk;
+  int64_t chunk;
+  unsigned long long *dyn_counter;
+  unsigned int *done;
+  int32_t *trace;
+};
+bool stencil_supported(int F, int bm, int bn);
+cudaError_t launch_stencil(const StencilArgs &a, int F, int bm, int bn, int teams, int units, cudaStream_t s);
+
 // ---- matvec (NEXT #2) -------------------------------------------------------------
 struct MatvecArgs {
   const float *A, *x;

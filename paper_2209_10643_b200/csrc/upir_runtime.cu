@@ -660,6 +660,7 @@ static int body_dtype_ok(int kind, int dtype) {
     case UPIR_BODY_JACOBI5: return dtype == UPIR_F32;
     case UPIR_BODY_MATMUL: return dtype == UPIR_BF16 || dtype == UPIR_F32;
     case UPIR_BODY_MATVEC: return dtype == UPIR_F32;
+    case UPIR_BODY_STENCIL2D: return dtype == UPIR_F32;
   }
   return 0;
 }
@@ -681,12 +682,13 @@ static upir_status validate_loop(const upir_spmd_desc *sd, const upir_loop_desc 
   const bool tiled = l->collapse == 2 && (l->tile[0] > 0 || l->tile[1] > 0);
   if (l->distribute == UPIR_DIST_UNITS && sd->num_teams > 1 && !tiled)
     return fail(UPIR_E_INVALID, "distribute(units) with num_teams > 1 would replicate the loop per team (reading c7)");
-  if (kind < UPIR_BODY_AXPY || kind > UPIR_BODY_MATVEC) return fail(UPIR_E_INVALID, "unknown body kind %d", kind);
+  if (kind < UPIR_BODY_AXPY || kind > UPIR_BODY_STENCIL2D) return fail(UPIR_E_INVALID, "unknown body kind %d", kind);
   if (dtype >= 0 && !body_dtype_ok(kind, dtype)) return fail(UPIR_E_INVALID, "dtype %d not valid for body %d", dtype, kind);
   if (n_reds < 0 || n_reds > 2) return fail(UPIR_E_INVALID, "n_reds=%d outside [0,2]", n_reds);
   if (n_reds > 0 && !reds) return fail(UPIR_E_INVALID, "reds is NULL");
   if (kind == UPIR_BODY_REDUCE && n_reds == 0) return fail(UPIR_E_INVALID, "REDUCE body needs a reduction");
-  if ((kind == UPIR_BODY_JACOBI5 || kind == UPIR_BODY_MATMUL || kind == UPIR_BODY_MATVEC) && n_reds > 0)
+  if ((kind == UPIR_BODY_JACOBI5 || kind == UPIR_BODY_MATMUL || kind == UPIR_BODY_MATVEC ||
+       kind == UPIR_BODY_STENCIL2D) && n_reds > 0)
     return fail(UPIR_E_INVALID, "reductions are not defined for this body");
   if (kind == UPIR_BODY_MATVEC) {
     if (l->collapse != 1 || l->step[0] != 1) return fail(UPIR_E_INVALID, "MATVEC is a collapse(1) row loop with step 1");
@@ -709,8 +711,8 @@ static upir_status validate_loop(const upir_spmd_desc *sd, const upir_loop_desc 
     for (int d = 0; d < 2; ++d)
       if (l->step[d] != 1) return fail(UPIR_E_INVALID, "JACOBI5/MATMUL levels need step 1");
   }
-  if (kind == UPIR_BODY_JACOBI5) {
-    if (l->tile[0] <= 0 || l->tile[1] <= 0) return fail(UPIR_E_INVALID, "JACOBI5 needs tile[0], tile[1] > 0");
+  if (kind == UPIR_BODY_JACOBI5 || kind == UPIR_BODY_STENCIL2D) {
+    if (l->tile[0] <= 0 || l->tile[1] <= 0) return fail(UPIR_E_INVALID, "tiled stencils need tile[0], tile[1] > 0");
     if (l->distribute != UPIR_DIST_TEAMS) return fail(UPIR_E_INVALID, "the tile loop of a tiled nest is distributed over teams");
     if (l->inner_policy != UPIR_SCHED_STATIC || l->inner_chunk < 1)
       return fail(UPIR_E_UNSUPPORTED, "intra-tile loop supports schedule(static, c>=1) over units");
@@ -947,6 +949,7 @@ static upir_status exec_stream(upir_spmd s, const upir_loop_desc *l, const upir_
 
 static upir_status exec_jacobi(upir_spmd s, const upir_loop_desc *l, const upir_body *b, upir_map trace);
 static upir_status exec_matvec(upir_spmd s, const upir_loop_desc *l, const upir_body *b, upir_map trace);
+static upir_status exec_stencil(upir_spmd s, const upir_loop_desc *l, const upir_body *b, upir_map trace);
 static upir_status exec_matmul(upir_spmd s, const upir_loop_desc *l, const upir_body *b, upir_map trace);
 
 extern "C" upir_status upir_loop_exec(upir_spmd s, const upir_loop_desc *l, const upir_body *b,
@@ -965,6 +968,7 @@ extern "C" upir_status upir_loop_exec(upir_spmd s, const upir_loop_desc *l, cons
     case UPIR_BODY_JACOBI5: st = exec_jacobi(s, l, b, trace); break;
     case UPIR_BODY_MATMUL: st = exec_matmul(s, l, b, trace); break;
     case UPIR_BODY_MATVEC: st = exec_matvec(s, l, b, trace); break;
+    case UPIR_BODY_STENCIL2D: st = exec_stencil(s, l, b, trace); break;
   }
   if (st != UPIR_OK) return st;
   // implicit barrier at the end of a worksharing loop: stream
@@ -1053,6 +1057,73 @@ static upir_status exec_jacobi(upir_spmd s, const upir_loop_desc *l, const upir_
   c->launches++;
   return UPIR_OK;
 }
+static upir_status exec_stencil(upir_spmd s, const upir_loop_desc *l, const upir_body *b, upir_map trace) {
+  upir_ctx c = s->ctx;
+  const upir_spmd_desc &sd = s->d;
+  upir_status st;
+  if ((st = check_map(c, b->in0, "in0")) != UPIR_OK) return st;
+  if ((st = check_map(c, b->in1, "in1 (weights)")) != UPIR_OK) return st;
+  if ((st = check_map(c, b->out, "out")) != UPIR_OK) return st;
+  const int64_t ny = b->dims[0], F = b->dims[1], ld = b->ld[0];
+  const int R = (int)(F - 1) / 2;
+  const int bm = (int)l->tile[0], bn = (int)l->tile[1];
+  if (!stencil_supported((int)F, bm, bn))
+    return fail(UPIR_E_UNSUPPORTED, "STENCIL2D: filter size %lld / tile %dx%d not built (F 3/5/7, tiles 16x128, 8x64)",
+                (long long)F, bm, bn);
+  if ((int64_t)b->in1->dev_bytes < F * F * 4) return fail(UPIR_E_INVALID, "weights map needs F*F fp32");
+  ElemView vi, vo;
+  if ((st = elem_view(b->in0, 4, vi)) != UPIR_OK) return st;
+  if ((st = elem_view(b->out, 4, vo)) != UPIR_OK) return st;
+  if (vi.lo != vo.lo || vi.hi != vo.hi) return fail(UPIR_E_INVALID, "in0 and out must have the same layout");
+  if (ld < 1 || vi.lo % ld != 0 || vi.hi % ld != 0) return fail(UPIR_E_INVALID, "maps must hold whole rows");
+  const int64_t row0 = vi.lo / ld, rows_local = (vi.hi - vi.lo) / ld;
+  int64_t lb0 = l->lb[0], ub0 = l->ub[0], lb1 = l->lb[1], ub1 = l->ub[1];
+  if (lb0 < R || ub0 > ny - R || lb1 < R || ub1 > ld - R)
+    return fail(UPIR_E_INVALID, "STENCIL2D iteration space must lie in [R, ny-R) x [R, ld-R)");
+  if (sd.target == UPIR_TARGET_CLUSTER && c->nranks > 1) {
+    upir_map m = b->in0;
+    if (m->dist.pattern != UPIR_PATTERN_BLOCK || m->dist.halo_rows < R)
+      return fail(UPIR_E_INVALID, "cluster STENCIL2D needs BLOCK maps with halo_rows >= R");
+    lb0 = std::max(lb0, m->row_lo);
+    ub0 = std::min(ub0, m->row_hi);
+  }
+  if (ub0 > lb0 && (lb0 - R < row0 || ub0 + R > row0 + rows_local))
+    return fail(UPIR_E_INVALID, "rows need halo rows outside the local buffer");
+  StencilArgs a;
+  memset(&a, 0, sizeof a);
+  a.in = (const float *)b->in0->dev;
+  a.out = (float *)b->out->dev;
+  a.w = (const float *)b->in1->dev;
+  a.ld = ld;
+  a.row0 = row0;
+  a.ny = std::min(ny, row0 + rows_local);
+  a.nx = ld;
+  a.lb0 = lb0; a.ub0 = ub0; a.lb1 = lb1; a.ub1 = ub1;
+  if (ub0 <= lb0 || ub1 <= lb1) return UPIR_OK;
+  a.ti0 = lb0 / bm;
+  a.tj0 = lb1 / bn;
+  a.ntr = (ub0 + bm - 1) / bm - a.ti0;
+  a.ntc = (ub1 + bn - 1) / bn - a.tj0;
+  int sk;
+  int64_t chunk;
+  if ((st = tile_sched(l, sk, chunk)) != UPIR_OK) return st;
+  a.sched = sk;
+  a.chunk = chunk;
+  a.inner_chunk = (int)l->inner_chunk;
+  a.dyn_counter = c->dyn;
+  a.done = c->done;
+  if (trace) {
+    if ((st = check_map(c, trace, "trace")) != UPIR_OK) return st;
+    const int64_t need = 3 * a.ntr * a.ntc * bm * bn * 4;
+    if ((int64_t)trace->dev_bytes < need) return fail(UPIR_E_INVALID, "trace map needs %lld bytes", (long long)need);
+    a.trace = (int32_t *)trace->dev;
+  }
+  cudaError_t e = launch_stencil(a, (int)F, bm, bn, sd.num_teams, sd.num_units, c->compute);
+  if (e != cudaSuccess) return fail(UPIR_E_CUDA, "STENCIL2D launch failed: %s", cudaGetErrorString(e));
+  c->launches++;
+  return UPIR_OK;
+}
+
 static upir_status exec_matvec(upir_spmd s, const upir_loop_desc *l, const upir_body *b, upir_map trace) {
   upir_ctx c = s->ctx;
   const upir_spmd_desc &sd = s->d;

@@ -1,0 +1,111 @@
+"""GPU parity of the STENCIL2D loop body (NEXT #4: the paper's "2D stencil,
+filter size = 7", reading c28) against the fp64 oracle.
+Tolerance: max|d| / max over points of sum |w||in| <= 1e-5; the tile -> team
+and position -> unit maps are bit-exact (reading c24)."""
+import numpy as np
+import pytest
+
+import oracle
+import paper_2209_10643_b200 as U
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ctx(upir):
+    c = U.upir_init(0)
+    yield c
+    U.upir_finalize(c)
+
+
+def weights(F, seed=9):
+    return synth.f32_sym(seed, 0, F * F).reshape(F, F)
+
+
+def stencil_gpu(ctx, g, w, S=1, teams=16, units=256, tile=(16, 128), policy=U.SCHED_STATIC, chunk=1, ic=4,
+                trace=False):
+    ny, nx = g.shape
+    F = w.shape[0]
+    R = (F - 1) // 2
+    a, b = g.copy(), g.copy()
+    ma, mb, mw = U.upir_data_map(ctx, a, U.MAP_TOFROM), U.upir_data_map(ctx, b, U.MAP_TOFROM), \
+        U.upir_data_map(ctx, np.ascontiguousarray(w), U.MAP_TO)
+    loop = U.loop_desc([R, R], [ny - R, nx - R], tile=list(tile), policy=policy, chunk=chunk,
+                       distribute=U.DIST_TEAMS, inner_chunk=ic)
+    tr = tm = None
+    if trace:
+        nt = ((ny - R + tile[0] - 1) // tile[0] - R // tile[0]) * ((nx - R + tile[1] - 1) // tile[1] - R // tile[1])
+        tr = np.zeros(3 * nt * tile[0] * tile[1], np.int32)
+        tm = U.upir_data_map(ctx, tr, U.MAP_TOFROM)
+    s = U.upir_spmd_launch(ctx, U.spmd_desc(teams, units))
+    try:
+        src, dst = ma, mb
+        for k in range(S):
+            U.upir_loop_exec(s, loop, U.body(U.BODY_STENCIL2D, U.F32, in0=src, in1=mw, out=dst, ld=(nx, 0, 0),
+                                             dims=(ny, F, 0)), trace=tm if k == 0 else None)
+            src, dst = dst, src
+    finally:
+        U.upir_spmd_end(s)
+        if tm is not None:
+            U.upir_data_unmap(ctx, tm)
+        for m in (mw, mb, ma):
+            U.upir_data_unmap(ctx, m)
+        U.upir_sync(ctx)
+    return (b if S % 2 else a), tr
+
+
+def err(out, g, w, S):
+    ref = oracle.stencil2d(g, w, S)
+    scale = oracle.stencil2d(np.abs(g), np.abs(w), S)
+    return np.abs(out - ref).max() / max(np.abs(scale).max(), 1e-30)
+
+
+@pytest.mark.parametrize("F", [7, 5, 3])
+@pytest.mark.parametrize("shape", [(70, 300), (33, 140), (130, 515)])
+@pytest.mark.parametrize("tile", [(16, 128), (8, 64)])
+def test_stencil_parity(ctx, F, shape, tile):
+    g = synth.jacobi_init(*shape)
+    w = weights(F)
+    out, _ = stencil_gpu(ctx, g, w, S=2, tile=tile)
+    assert err(out, g, w, 2) <= 1e-5
+    R = (F - 1) // 2
+    mask = np.ones_like(g, bool)
+    mask[R:-R, R:-R] = False
+    assert (out[mask] == g[mask]).all()
+
+
+@pytest.mark.parametrize("policy,chunk", [(U.SCHED_STATIC, 0), (U.SCHED_STATIC, 2), (U.SCHED_DYNAMIC, 1)])
+@pytest.mark.parametrize("ic", [4, 1, 5])
+def test_stencil_schedules(ctx, policy, chunk, ic):
+    g = synth.jacobi_init(90, 260)
+    w = weights(7)
+    out, _ = stencil_gpu(ctx, g, w, teams=7, units=128, policy=policy, chunk=chunk, ic=ic)
+    assert err(out, g, w, 1) <= 1e-5
+
+
+def test_stencil_identity_and_fixed_point(ctx):
+    g = synth.jacobi_init(64, 192)
+    d = np.zeros((7, 7), np.float32)
+    d[3, 3] = 1
+    out, _ = stencil_gpu(ctx, g, d, S=3)
+    assert (out == g).all()
+    v = np.array([1, 2, 3, 4, 3, 2, 1], np.float64)
+    w = (np.outer(v, v) / 256.0).astype(np.float32)
+    i = np.arange(64)[:, None].astype(np.float64)
+    j = np.arange(192)[None, :].astype(np.float64)
+    lin = (2 * i - 3 * j + 5).astype(np.float32)
+    out, _ = stencil_gpu(ctx, lin, w, S=2)
+    assert np.abs(out - lin).max() <= 1e-4      # exact in fp64; fp32 FMA order differs
+
+
+def test_stencil_trace_mapping(ctx):
+    g = synth.jacobi_init(50, 200)
+    w = weights(7)
+    teams, units, tile = 5, 96, (16, 128)
+    _, tr = stencil_gpu(ctx, g, w, teams=teams, units=units, tile=tile, chunk=1, trace=True)
+    n = len(tr) // 3
+    ot, ou = oracle.tiled_owner(3, 47, 3, 197, tile[0], tile[1], oracle.STATIC, 1, teams, 4, units)
+    it = ot >= 0
+    assert (tr[2 * n:][it] == 1).all() and (tr[2 * n:][~it] == 0).all()
+    assert (tr[:n][it] == ot[it]).all() and (tr[n:2 * n][it] == ou[it]).all()

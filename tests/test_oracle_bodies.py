@@ -264,3 +264,37 @@ def test_matvec_small_integers_rows_and_rank1():
     u = synth.f32_sym(1, 0, 12)
     B = np.repeat(u[:, None], 40, axis=1)            # rows u_i * 1^T
     assert np.allclose(oracle.matvec(B, np.ones(40, np.float32)), 40 * u.astype(np.float64), rtol=0, atol=1e-12)
+
+
+# ---- 2-D filter stencil, radius 3 (NEXT #4) -----------------------------------------
+def _w7():
+    # symmetric dyadic weights summing to exactly 1
+    v = np.array([1, 2, 3, 4, 3, 2, 1], np.float64)
+    return (np.outer(v, v) / 256.0).astype(np.float32)
+
+
+def test_stencil_library_routine_correlate2d():
+    from scipy.signal import correlate2d
+    g = synth.jacobi_init(30, 41)
+    w = synth.f32_sym(9, 0, 49).reshape(7, 7)
+    out = oracle.stencil2d(g, w)
+    ref = correlate2d(g.astype(np.float64), w.astype(np.float64), mode="valid")
+    assert np.abs(out[3:-3, 3:-3] - ref).max() <= 1e-12
+    mask = np.ones_like(g, bool)
+    mask[3:-3, 3:-3] = False
+    assert (out[mask] == g[mask]).all()
+
+
+def test_stencil_delta_and_shift_and_fixed_points():
+    g = synth.jacobi_init(20, 25)
+    d = np.zeros((7, 7), np.float32)
+    d[3, 3] = 1
+    assert (oracle.stencil2d(g, d, 3) == g).all()            # identity
+    sh = np.zeros((7, 7), np.float32)
+    sh[3, 5] = 1                                              # reads in[i][j+2]
+    out = oracle.stencil2d(g, sh)
+    assert (out[3:-3, 3:-3] == g[3:-3, 5:-1]).all()
+    i = np.arange(40)[:, None].astype(np.float64)
+    j = np.arange(40)[None, :].astype(np.float64)
+    lin = (2 * i - 3 * j + 5).astype(np.float32)              # linear field, symmetric weights summing to 1
+    assert (oracle.stencil2d(lin, _w7(), 4) == lin).all()
