@@ -242,7 +242,7 @@ def run_upir(args):
     if world == 1 and not args.no_kernels and args.workload == "reduce":
         res["kernels"] = {}
         for name, fn in (("axpy", bench_axpy), ("jacobi", bench_jacobi), ("matmul", bench_matmul),
-                         ("matvec", bench_matvec)):
+                         ("matvec", bench_matvec), ("stencil7", bench_stencil7)):
             try:
                 res["kernels"][name] = fn(args, U, ctx, stream, peaks, peak_src)
             except Exception as e:   # report, never hide
@@ -501,6 +501,39 @@ def bench_jacobi(args, U, ctx, stream, peaks, peak_src, ny=8192, nx=8192, S=100)
             "roofline": {"achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
                          "algorithmic_bytes_per_lup": 8, "peak_source": peak_src,
                          "traffic": ncu_traffic("jacobi")}}
+
+
+def bench_stencil7(args, U, ctx, stream, peaks, peak_src):
+    """NEXT #4: 2-D filter stencil, filter size 7 (the paper's stencil,
+    PAPER.md:1483), at the paper's largest size 2048^2 and at 8192^2."""
+    import torch
+    out = {}
+    v = torch.tensor([1, 2, 3, 4, 3, 2, 1], dtype=torch.float64)
+    w = (torch.outer(v, v) / 256.0).float().cuda()
+    for n in (2048, 8192):
+        a_t = torch.empty(n * n, dtype=torch.float32, device="cuda")
+        b_t = torch.empty(n * n, dtype=torch.float32, device="cuda")
+        torch.cuda.synchronize()
+        ma, mb, mw = U.upir_data_adopt(ctx, a_t), U.upir_data_adopt(ctx, b_t), U.upir_data_adopt(ctx, w)
+        U.upir_synth_fill(ctx, ma, 4, 5, 0, n, n)
+        U.upir_synth_fill(ctx, mb, 4, 5, 0, n, n)
+        s = U.upir_spmd_launch(ctx, U.spmd_desc(148 * 4, 256))
+        loop = U.loop_desc([3, 3], [n - 3, n - 3], tile=[16, 128], chunk=1, distribute=U.DIST_TEAMS, inner_chunk=4)
+        body = U.body(U.BODY_STENCIL2D, U.F32, in0=ma, in1=mw, out=mb, ld=(n, 0, 0), dims=(n, 7, 0))
+        for _ in range(3):
+            U.upir_loop_exec(s, loop, body)
+        ms = _time_graph(U, ctx, stream, lambda: U.upir_loop_exec(s, loop, body), 10)
+        U.upir_spmd_end(s)
+        for m in (mw, mb, ma):
+            U.upir_data_unmap(ctx, m)
+        U.upir_sync(ctx)
+        lups = (n - 6) ** 2
+        out[f"{n}x{n}"] = {"ms_per_sweep": ms, "GLUP/s": lups / (ms / 1e3) / 1e9,
+                           "GB/s": 8 * lups / (ms / 1e3) / 1e9, "GFLOP/s": 98 * lups / (ms / 1e3) / 1e9}
+        del a_t, b_t
+    return {"workload": "2-D 7x7 filter stencil (49 taps, fp32 FMA), tiles 16x128 static,1 over 592 teams, "
+                        "static,4 over 256 units; one sweep per launch", "bound": "alu (49 FMA per point)",
+            "paper_v100_end_to_end_ms_2048": 56.47, **out}
 
 
 def bench_matvec(args, U, ctx, stream, peaks, peak_src, n=16384):

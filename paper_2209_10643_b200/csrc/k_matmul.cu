@@ -214,7 +214,7 @@ __global__ void __launch_bounds__(Cfg<DT>::THREADS, 1)
           char *sa = smem + stage * L::STAGE;
           char *sb = sa + L::A_BYTES;
           tma_mbar_expect_tx(full + stage, L::TX);
-          tma_load_2d(sa, &tma, kb * BK, m0, full + stage);
+          tma_load_2d(sa, &tma, kb * BK, m0 - (int)a.row0, full + stage);
 #pragma unroll
           for (int j = 0; j < BN / L::BOXN; ++j)
             tma_load_2d(sb + j * L::B_BOX, &tmb, n0 + L::BOXN * j, kb * BK, full + stage);
@@ -281,7 +281,7 @@ __global__ void __launch_bounds__(Cfg<DT>::THREADS, 1)
       tc_fence_after();
       const int64_t row = m0 + 32 * ew + lane;
       const bool row_ok = row >= a.lb0 && row < a.ub0;
-      float *crow = a.C + row * a.ldc;
+      float *crow = a.C + (row - a.row0) * a.ldc;
 #pragma unroll 1
       for (int c = 0; c < BN; c += 32) {
         uint32_t r[32];

@@ -131,7 +131,8 @@ struct MatmulArgs {
   const void *A, *B;
   float *C;
   int64_t M, N, K, lda, ldb, ldc;
-  int64_t lb0, ub0, lb1, ub1;   // (i, j) iteration space
+  int64_t lb0, ub0, lb1, ub1;   // (i, j) iteration space (global rows)
+  int64_t row0;                 // global row of local row 0 of A and C (BLOCK maps)
   int32_t sched;
   int64_t chunk;
   int64_t ticket_m;

@@ -1189,11 +1189,25 @@ static upir_status exec_matmul(upir_spmd s, const upir_loop_desc *l, const upir_
     return fail(UPIR_E_UNSUPPORTED, "MATMUL needs lda, ldb, ldc multiples of 8 elements (TMA / 32-B stores)");
   const int64_t es = b->dtype == UPIR_F32 ? 4 : 2;
   if (es == 4 && (lda % 4 || ldb % 4)) return fail(UPIR_E_UNSUPPORTED, "fp32 MATMUL needs lda, ldb multiples of 4");
-  if ((int64_t)b->in0->dev_bytes < ((M - 1) * lda + K) * es || (int64_t)b->in1->dev_bytes < ((K - 1) * ldb + N) * es ||
-      (int64_t)b->out->dev_bytes < ((M - 1) * ldc + N) * 4)
+  const int64_t MA = b->in0->dist.pattern == UPIR_PATTERN_BLOCK ? b->in0->loc_row_hi - b->in0->loc_row_lo : M;
+  if (MA > 0 && ((int64_t)b->in0->dev_bytes < ((MA - 1) * lda + K) * es ||
+                 (int64_t)b->in1->dev_bytes < ((K - 1) * ldb + N) * es ||
+                 (int64_t)b->out->dev_bytes < ((MA - 1) * ldc + N) * 4))
     return fail(UPIR_E_INVALID, "MATMUL maps smaller than the matrices they hold");
   if (l->lb[0] < 0 || l->ub[0] > M || l->lb[1] < 0 || l->ub[1] > N)
     return fail(UPIR_E_INVALID, "MATMUL iteration space must lie in [0,M) x [0,N)");
+  // rows of A and C may be BLOCK-distributed over ranks (B replicated): the
+  // local buffers hold global rows [row0, row0 + local rows)
+  int64_t row0 = 0, rows_here = M;
+  const upir_map mA = b->in0, mC = b->out;
+  if (mA->dist.pattern == UPIR_PATTERN_BLOCK || mC->dist.pattern == UPIR_PATTERN_BLOCK) {
+    if (mA->dist.pattern != UPIR_PATTERN_BLOCK || mC->dist.pattern != UPIR_PATTERN_BLOCK ||
+        mA->loc_row_lo != mC->loc_row_lo || mA->loc_row_hi != mC->loc_row_hi || mA->dist.n_rows != M ||
+        mC->dist.n_rows != M)
+      return fail(UPIR_E_INVALID, "distributed MATMUL needs A and C BLOCK-distributed over the same M rows");
+    row0 = mA->loc_row_lo;
+    rows_here = mA->loc_row_hi - mA->loc_row_lo;
+  }
   if (sd.num_units != matmul_required_units(b->dtype))
     return fail(UPIR_E_INVALID, "the tcgen05 MATMUL body runs %d units per team for this dtype (got %d): geometry is not clamped",
                 matmul_required_units(b->dtype), sd.num_units);
@@ -1209,6 +1223,16 @@ static upir_status exec_matmul(upir_spmd s, const upir_loop_desc *l, const upir_
   a.M = M; a.N = N; a.K = K;
   a.lda = lda; a.ldb = ldb; a.ldc = ldc;
   a.lb0 = l->lb[0]; a.ub0 = l->ub[0]; a.lb1 = l->lb[1]; a.ub1 = l->ub[1];
+  a.row0 = row0;
+  if (sd.target == UPIR_TARGET_CLUSTER && c->nranks > 1) {
+    // cluster SPMD: the (i) level is block-distributed over the ranks (c20)
+    int64_t lo, hi;
+    upir_dist_owned_rows(M, c->rank, c->nranks, &lo, &hi);
+    a.lb0 = std::max(a.lb0, lo);
+    a.ub0 = std::min(a.ub0, hi);
+  }
+  if (a.ub0 > a.lb0 && (a.lb0 < row0 || a.ub0 > row0 + rows_here))
+    return fail(UPIR_E_INVALID, "MATMUL rows [%lld,%lld) are not held locally", (long long)a.lb0, (long long)a.ub0);
   if (a.ub0 <= a.lb0 || a.ub1 <= a.lb1) return UPIR_OK;
   a.sched = sk;
   a.chunk = chunk;
@@ -1220,7 +1244,7 @@ static upir_status exec_matmul(upir_spmd s, const upir_loop_desc *l, const upir_
     a.trace = (int32_t *)trace->dev;
   }
   alignas(64) CUtensorMap ta, tb;
-  if (!matmul_encode_tmaps(&ta, &tb, a.A, a.B, b->dtype, M, N, K, lda, ldb))
+  if (!matmul_encode_tmaps(&ta, &tb, a.A, a.B, b->dtype, rows_here, N, K, lda, ldb))
     return fail(UPIR_E_CUDA, "cuTensorMapEncodeTiled failed for MATMUL operands");
   a.tmap_a = &ta;
   a.tmap_b = &tb;

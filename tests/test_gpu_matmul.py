@@ -223,3 +223,24 @@ def test_matmul_full_size_sampled_rows(ctx):
     assert (np.abs(got - ref) / scale).max() <= 1e-5
     for m in (mc, mb, ma):
         U.upir_data_unmap(ctx, m)
+
+
+def test_matmul_cluster_block_rows_world1(ctx):
+    """NEXT #4 multi-GPU matmul: A and C BLOCK-distributed by rows, B
+    replicated, CLUSTER-target loop (world size 1 here: rank 0 holds all rows)."""
+    M, N, K = 384, 512, 128
+    A = synth.bf16_sym_as_f32(3, 0, M * K).reshape(M, K)
+    B = synth.bf16_sym_as_f32(4, 0, K * N).reshape(K, N)
+    a, b = to_bf16_bits(A), to_bf16_bits(B)
+    C = np.zeros((M, N), np.float32)
+    ma = U.upir_data_map(ctx, a, U.MAP_TO, U.dist(M, K, 2))
+    mb = U.upir_data_map(ctx, b, U.MAP_TO)
+    mc = U.upir_data_map(ctx, C, U.MAP_FROM, U.dist(M, N, 4))
+    s = U.upir_spmd_launch(ctx, U.spmd_desc(8, 256, U.TARGET_CLUSTER))
+    U.upir_loop_exec(s, U.loop_desc([0, 0], [M, N], chunk=1, distribute=U.DIST_TEAMS),
+                     U.body(U.BODY_MATMUL, U.BF16, in0=ma, in1=mb, out=mc, ld=(K, N, N), dims=(K, M, N)))
+    U.upir_spmd_end(s)
+    for m in (mc, mb, ma):
+        U.upir_data_unmap(ctx, m)
+    U.upir_sync(ctx)
+    assert scaled_err(C, A, B, oracle.matmul(A, B)) <= 1e-5
