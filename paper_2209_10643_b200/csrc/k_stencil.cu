@@ -3,26 +3,41 @@
 //   out[i][j] = sum_{a,b in [-R,R]} w[a+R][b+R] * in[i+a][j+b]
 // over a tiled collapse(2) upir.loop (reading c24: tiles anchored at 0, tile
 // loop over TEAMS, box positions static,ic over UNITS).  Each team stages the
-// (BM+2R) x (BN+2R) input window of its tile in shared memory with coalesced
-// loads (rows of the window are contiguous in HBM), the F x F weights once per
-// kernel; each unit produces 4 consecutive outputs per chunk from registers
+// (BM+2R) x (BN+8) input window of its tile in shared memory with one TMA
+// tensor load (zero fill out of range), double-buffered: one elected thread
+// has the next tile's window in flight while the team computes the current
+// one; the F x F weights are staged once; each unit produces 4 consecutive
+// outputs per chunk from registers
 // (register-blocked taps, fp32 FMA in the fixed order of the filter rows /
 // columns).  49 FMAs per point at F = 7: ALU-bound rather than HBM-bound.
+#include "dev_tma.cuh"
 #include "upir_internal.h"
 
 namespace upir {
 namespace {
 
 template <int R, int BM, int BN>
-__global__ void __launch_bounds__(1024) stencil_kernel(const __grid_constant__ StencilArgs a) {
-  constexpr int F = 2 * R + 1, WR = BM + 2 * R, WC = BN + 2 * R, WCP = WC + 1;
-  extern __shared__ float sm[];
-  float *win = sm;              // WR x WCP
-  float *w = sm + WR * WCP;     // F x F
-  __shared__ long long s_tile;
+struct SLayout {
+  static constexpr int F = 2 * R + 1, WR = BM + 2 * R, WC = BN + 8;
+  static constexpr int BUF = ((WR * WC * 4) + 127) / 128 * 128;
+  static constexpr int SMEM = 2 * BUF + 256 + F * F * 4 + 128;
+};
+
+template <int R, int BM, int BN>
+__global__ void __launch_bounds__(1024) stencil_kernel(const __grid_constant__ StencilArgs a,
+                                                       const __grid_constant__ CUtensorMap tmw) {
+  // window column c holds global column j0 - 4 + c (4-aligned so that a
+  // unit's taps are read as 16-B vectors)
+  using L = SLayout<R, BM, BN>;
+  constexpr int F = L::F, WR = L::WR, WCP = L::WC;
+  extern __shared__ __align__(128) char smc[];
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smc + 2 * L::BUF);
+  volatile long long *tile_s = reinterpret_cast<volatile long long *>(smc + 2 * L::BUF + 16);
+  float *w = reinterpret_cast<float *>(smc + 2 * L::BUF + 256);
   __shared__ unsigned s_last;
   const int units = blockDim.x, u = threadIdx.x;
   for (int e = threadIdx.x; e < F * F; e += blockDim.x) w[e] = a.w[e];
+  __syncthreads();
   const int64_t nt = a.ntr * a.ntc;
   // tile iterator (thread 0), as the Jacobi body
   int64_t cur = 0, end = 0, kk = 0;
@@ -50,21 +65,35 @@ __global__ void __launch_bounds__(1024) stencil_kernel(const __grid_constant__ S
     return cur++;
   };
   constexpr int POS = BM * BN;
-  for (;;) {
-    if (threadIdx.x == 0) s_tile = next_tile();
-    __syncthreads();
-    const int64_t tile = s_tile;
-    if (tile < 0) break;
+  auto issue = [&](int64_t tile, int buf) {
     const int64_t i0 = (a.ti0 + tile / a.ntc) * BM, j0 = (a.tj0 + tile % a.ntc) * BN;
-    // stage the window rows [i0-R, i0+BM+R) x cols [j0-R, j0+BN+R)
-    for (int e = threadIdx.x; e < WR * WC; e += units) {
-      const int r = e / WC, c = e % WC;
-      const int64_t gi = i0 - R + r, gj = j0 - R + c;
-      float v = 0.f;
-      if (gi >= a.row0 && gi < a.ny && gj >= 0 && gj < a.nx) v = __ldcs(a.in + (gi - a.row0) * a.ld + gj);
-      win[r * WCP + c] = v;
+    tma_fence_proxy();
+    tma_mbar_expect_tx(bars + buf, WR * WCP * 4);
+    // window rows [i0-R, i0+BM+R) x cols [j0-4, j0+BN+4) of the local buffer
+    tma_load_2d(smc + buf * L::BUF, &tmw, (int)(j0 - 4), (int)(i0 - R - a.row0), bars + buf);
+  };
+  if (threadIdx.x == 0) {
+    tma_prefetch_desc(&tmw);
+    tma_mbar_init(bars + 0, 1);
+    tma_mbar_init(bars + 1, 1);
+    tma_fence_init();
+    const int64_t t0 = next_tile();
+    tile_s[0] = t0;
+    if (t0 >= 0) issue(t0, 0);
+  }
+  __syncthreads();
+  for (int iter = 0;; ++iter) {
+    const int buf = iter & 1;
+    const int64_t tile = tile_s[buf];
+    if (tile < 0) break;
+    if (threadIdx.x == 0) {
+      const int64_t nx = next_tile();
+      tile_s[buf ^ 1] = nx;
+      if (nx >= 0) issue(nx, buf ^ 1);
     }
-    __syncthreads();
+    tma_mbar_wait(bars + buf, (unsigned)((iter >> 1) & 1));
+    const float *win = reinterpret_cast<const float *>(smc + buf * L::BUF);
+    const int64_t i0 = (a.ti0 + tile / a.ntc) * BM, j0 = (a.tj0 + tile % a.ntc) * BN;
     const int ic = a.inner_chunk;
     if (ic == 4) {
       for (int k = u; k * 4 < POS; k += units) {
@@ -74,14 +103,22 @@ __global__ void __launch_bounds__(1024) stencil_kernel(const __grid_constant__ S
         float acc[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
         for (int p = 0; p < F; ++p) {
-          float v[4 + 2 * R];
+          // window columns c .. c+11 = global j-4 .. j+7 as three 16-B vectors
+          float v[12];
+          const float4 *rowp = reinterpret_cast<const float4 *>(win + (r + p) * WCP + c);
 #pragma unroll
-          for (int q = 0; q < 4 + 2 * R; ++q) v[q] = win[(r + p) * WCP + c + q];
+          for (int q = 0; q < 3; ++q) {
+            const float4 t4 = rowp[q];
+            v[4 * q] = t4.x;
+            v[4 * q + 1] = t4.y;
+            v[4 * q + 2] = t4.z;
+            v[4 * q + 3] = t4.w;
+          }
 #pragma unroll
           for (int q = 0; q < F; ++q) {
             const float wq = w[p * F + q];
 #pragma unroll
-            for (int t = 0; t < 4; ++t) acc[t] = __fmaf_rn(wq, v[t + q], acc[t]);
+            for (int t = 0; t < 4; ++t) acc[t] = __fmaf_rn(wq, v[4 - R + t + q], acc[t]);
           }
         }
         float *dst = a.out + (i - a.row0) * a.ld + j;
@@ -111,7 +148,7 @@ __global__ void __launch_bounds__(1024) stencil_kernel(const __grid_constant__ S
           if (i < a.lb0 || i >= a.ub0 || j < a.lb1 || j >= a.ub1) continue;
           float acc = 0.f;
           for (int p = 0; p < F; ++p)
-            for (int q = 0; q < F; ++q) acc = __fmaf_rn(w[p * F + q], win[(r + p) * WCP + c + q], acc);
+            for (int q = 0; q < F; ++q) acc = __fmaf_rn(w[p * F + q], win[(r + p) * WCP + c + 4 - R + q], acc);
           a.out[(i - a.row0) * a.ld + j] = acc;
           if (a.trace) {
             const int64_t idx = tile * POS + pos;
@@ -122,7 +159,7 @@ __global__ void __launch_bounds__(1024) stencil_kernel(const __grid_constant__ S
         }
       }
     }
-    __syncthreads();
+    __syncthreads();   // buffer `buf` free; tile_s[buf ^ 1] visible
   }
   if (a.sched == SK_DYNAMIC) {
     if (threadIdx.x == 0) {
@@ -139,9 +176,15 @@ __global__ void __launch_bounds__(1024) stencil_kernel(const __grid_constant__ S
 
 template <int R, int BM, int BN>
 cudaError_t launch_r(const StencilArgs &a, int teams, int units, cudaStream_t s) {
-  constexpr int WR = BM + 2 * R, WC = BN + 2 * R + 1, F = 2 * R + 1;
-  const size_t smem = (size_t)(WR * WC + F * F) * sizeof(float);
-  stencil_kernel<R, BM, BN><<<teams, units, smem, s>>>(a);
+  using L = SLayout<R, BM, BN>;
+  CUtensorMap tm;
+  if (!encode_tmap_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, a.in, (uint64_t)a.nx, (uint64_t)(a.ny - a.row0),
+                      (uint64_t)a.ld * 4, L::WC, L::WR, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B))
+    return cudaErrorInvalidValue;
+  auto k = stencil_kernel<R, BM, BN>;
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+  if (e != cudaSuccess) return e;
+  k<<<teams, units, L::SMEM, s>>>(a, tm);
   return cudaGetLastError();
 }
 

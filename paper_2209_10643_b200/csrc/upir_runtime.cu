@@ -1071,6 +1071,7 @@ static upir_status exec_stencil(upir_spmd s, const upir_loop_desc *l, const upir
     return fail(UPIR_E_UNSUPPORTED, "STENCIL2D: filter size %lld / tile %dx%d not built (F 3/5/7, tiles 16x128, 8x64)",
                 (long long)F, bm, bn);
   if ((int64_t)b->in1->dev_bytes < F * F * 4) return fail(UPIR_E_INVALID, "weights map needs F*F fp32");
+  if (ld % 4 != 0) return fail(UPIR_E_UNSUPPORTED, "STENCIL2D row pitch must be a multiple of 4 elements (TMA stride)");
   ElemView vi, vo;
   if ((st = elem_view(b->in0, 4, vi)) != UPIR_OK) return st;
   if ((st = elem_view(b->out, 4, vo)) != UPIR_OK) return st;

@@ -62,7 +62,7 @@ def err(out, g, w, S):
 
 
 @pytest.mark.parametrize("F", [7, 5, 3])
-@pytest.mark.parametrize("shape", [(70, 300), (33, 140), (130, 515)])
+@pytest.mark.parametrize("shape", [(70, 300), (33, 140), (130, 516)])
 @pytest.mark.parametrize("tile", [(16, 128), (8, 64)])
 def test_stencil_parity(ctx, F, shape, tile):
     g = synth.jacobi_init(*shape)
