@@ -176,7 +176,11 @@ __device__ __forceinline__ void direct_vec(const StreamArgs &a, int64_t e, Acc<B
 // One unit's contiguous element range [elo, ehi) of a reduction body: NV
 // 16-B vectors per load (NV = 2: 256-bit LDG with a 256-B L2 prefetch), U
 // loads in flight.  Scalar head / tail.
-template <int BODY, int NRED, int NV, int U>
+// HINT (AXPY only): 0 = streaming loads and stores (.cs); 1 = streaming
+// loads, write-back stores (a unit's 32-B sectors of y' stay in L2 until the
+// whole line is dirty: no partial-line evictions / DRAM read-modify-write);
+// 2 = write-back stores and default-policy loads.
+template <int BODY, int NRED, int NV, int U, int HINT = 0>
 __device__ __forceinline__ void direct_long(const StreamArgs &a, int64_t elo, int64_t ehi, int64_t vec_hi,
                                             Acc<BODY, NRED> &acc) {
   constexpr int VEC = BODY == SB_RED_I64 ? 2 : 4;
@@ -206,12 +210,22 @@ __device__ __forceinline__ void direct_long(const StreamArgs &a, int64_t elo, in
       float4 x[U * NV], y[U * NV];
 #pragma unroll
       for (int q = 0; q < U; ++q) {
-        if constexpr (NV == 2) {
+        if constexpr (NV == 2 && HINT < 2) {
           asm("ld.global.cs.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
               : "=f"(x[2 * q].x), "=f"(x[2 * q].y), "=f"(x[2 * q].z), "=f"(x[2 * q].w), "=f"(x[2 * q + 1].x),
                 "=f"(x[2 * q + 1].y), "=f"(x[2 * q + 1].z), "=f"(x[2 * q + 1].w)
               : "l"(px + q * STEP));
           asm volatile("ld.global.cs.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                       : "=f"(y[2 * q].x), "=f"(y[2 * q].y), "=f"(y[2 * q].z), "=f"(y[2 * q].w), "=f"(y[2 * q + 1].x),
+                         "=f"(y[2 * q + 1].y), "=f"(y[2 * q + 1].z), "=f"(y[2 * q + 1].w)
+                       : "l"(py + q * STEP)
+                       : "memory");
+        } else if constexpr (NV == 2) {
+          asm("ld.global.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+              : "=f"(x[2 * q].x), "=f"(x[2 * q].y), "=f"(x[2 * q].z), "=f"(x[2 * q].w), "=f"(x[2 * q + 1].x),
+                "=f"(x[2 * q + 1].y), "=f"(x[2 * q + 1].z), "=f"(x[2 * q + 1].w)
+              : "l"(px + q * STEP));
+          asm volatile("ld.global.L2::256B.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                        : "=f"(y[2 * q].x), "=f"(y[2 * q].y), "=f"(y[2 * q].z), "=f"(y[2 * q].w), "=f"(y[2 * q + 1].x),
                          "=f"(y[2 * q + 1].y), "=f"(y[2 * q + 1].z), "=f"(y[2 * q + 1].w)
                        : "l"(py + q * STEP)
@@ -231,8 +245,13 @@ __device__ __forceinline__ void direct_long(const StreamArgs &a, int64_t elo, in
       }
 #pragma unroll
       for (int q = 0; q < U; ++q) {
-        if constexpr (NV == 2)
+        if constexpr (NV == 2 && HINT == 0)
           asm volatile("st.global.cs.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(py + q * STEP), "f"(y[2 * q].x),
+                       "f"(y[2 * q].y), "f"(y[2 * q].z), "f"(y[2 * q].w), "f"(y[2 * q + 1].x), "f"(y[2 * q + 1].y),
+                       "f"(y[2 * q + 1].z), "f"(y[2 * q + 1].w)
+                       : "memory");
+        else if constexpr (NV == 2)
+          asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(py + q * STEP), "f"(y[2 * q].x),
                        "f"(y[2 * q].y), "f"(y[2 * q].z), "f"(y[2 * q].w), "f"(y[2 * q + 1].x), "f"(y[2 * q + 1].y),
                        "f"(y[2 * q + 1].z), "f"(y[2 * q + 1].w)
                        : "memory");
@@ -310,6 +329,9 @@ __device__ void direct_run(const StreamArgs &a, const LaneWork &w, Acc<BODY, NRE
           case 1: direct_long<BODY, NRED, 2, 4>(a, elo, ehi, vec_hi, acc); break;
           case 2: direct_long<BODY, NRED, 2, 2>(a, elo, ehi, vec_hi, acc); break;
           case 3: direct_long<BODY, NRED, 1, 8>(a, elo, ehi, vec_hi, acc); break;
+          case 4: direct_long<BODY, NRED, 2, 4, 1>(a, elo, ehi, vec_hi, acc); break;
+          case 5: direct_long<BODY, NRED, 2, 4, 2>(a, elo, ehi, vec_hi, acc); break;
+          case 6: direct_long<BODY, NRED, 2, 2, 1>(a, elo, ehi, vec_hi, acc); break;
           default: direct_long<BODY, NRED, 1, 4>(a, elo, ehi, vec_hi, acc); break;
         }
         continue;
