@@ -53,19 +53,38 @@ __device__ __forceinline__ int64_t next_row(RowIter &it, const MatvecArgs &a, in
 }
 
 // distribute(teams): one team per row at a time, units split the k-loop.
+// One barrier per row: the row id of iteration it+1 and the warp partials of
+// row it are published together (double-buffered), and warp 0 finishes row
+// it's reduction while the team streams row it+1.
 __global__ void __launch_bounds__(1024) matvec_teams_kernel(const __grid_constant__ MatvecArgs a) {
-  __shared__ float s_part[32];
-  __shared__ long long s_row;
+  __shared__ float s_part[2][32];
+  __shared__ long long s_row[2];
   __shared__ unsigned s_last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = (blockDim.x + 31) >> 5;
   const int units = blockDim.x, u = threadIdx.x;
   const int64_t T = a.T;
   RowIter it{0, 0, 0, false};
   const bool vec = a.inner_chunk == 4 && (a.lda % 4) == 0 && (((uintptr_t)a.A | (uintptr_t)a.x) % 16) == 0;
-  for (;;) {
-    if (threadIdx.x == 0) s_row = next_row(it, a, T, gridDim.x, blockIdx.x);
-    __syncthreads();
-    const int64_t r = s_row;
+  if (threadIdx.x == 0) s_row[0] = next_row(it, a, T, gridDim.x, blockIdx.x);
+  __syncthreads();
+  int64_t prev = -1;   // row whose partials sit in s_part[(iter - 1) & 1]
+  for (int iter = 0;; ++iter) {
+    const int buf = iter & 1;
+    const int64_t r = s_row[buf];
+    // warp 0 finishes the previous row (its partials were published by the last barrier)
+    if (prev >= 0 && warp == 0) {
+      if (lane == 0) {
+        float s = 0.f;
+        for (int w = 0; w < nwarps; ++w) s += s_part[buf ^ 1][w];
+        a.y[a.lb + prev] = s;
+        if (a.trace) {
+          a.trace[prev] = blockIdx.x;
+          a.trace[T + prev] = 0;
+          atomicAdd(a.trace + 2 * T + prev, 1);
+        }
+      }
+      __syncwarp();
+    }
     if (r < 0) break;
     const int64_t i = a.lb + r;
     const float *Ai = a.A + i * a.lda;
@@ -106,30 +125,22 @@ __global__ void __launch_bounds__(1024) matvec_teams_kernel(const __grid_constan
         for (int64_t k = c * ic; k < min(a.K, c * ic + ic); ++k) acc0 = __fmaf_rn(Ai[k], a.x[k], acc0);
     }
     float v = (acc0 + acc1) + (acc2 + acc3);
-    // team reduction(+) in a fixed order (reading c10)
+    // team reduction(+) in a fixed order (reading c10): warp tree, then warps in order
     const int rem = units & 31;
     if (warp == nwarps - 1 && rem) {
-      float s = v;
-      for (int l = 1; l < rem; ++l) s += __shfl_sync((1u << rem) - 1u, v, l);
-      v = s;
+      float s2 = v;
+      for (int l = 1; l < rem; ++l) s2 += __shfl_sync((1u << rem) - 1u, v, l);
+      v = s2;
     } else {
       v = warp_sum(v);
     }
-    if (lane == 0) s_part[warp] = v;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      float s = 0.f;
-      for (int w = 0; w < nwarps; ++w) s += s_part[w];
-      a.y[i] = s;
-      if (a.trace) {
-        a.trace[r] = blockIdx.x;
-        a.trace[T + r] = 0;
-        atomicAdd(a.trace + 2 * T + r, 1);
-      }
-    }
+    if (lane == 0) s_part[buf][warp] = v;
+    if (threadIdx.x == 0) s_row[buf ^ 1] = next_row(it, a, T, gridDim.x, blockIdx.x);
+    prev = r;
     __syncthreads();
   }
   if (a.sched == SK_DYNAMIC) {
+    __syncthreads();
     if (threadIdx.x == 0) {
       __threadfence();
       s_last = atomicAdd(a.done, 1u) == gridDim.x - 1;
