@@ -180,13 +180,16 @@ __device__ __forceinline__ void direct_vec(const StreamArgs &a, int64_t e, Acc<B
 // loads, write-back stores (a unit's 32-B sectors of y' stay in L2 until the
 // whole line is dirty: no partial-line evictions / DRAM read-modify-write);
 // 2 = write-back stores and default-policy loads.
-template <int BODY, int NRED, int NV, int U, int HINT = 0>
+// LINE = 1: the scalar head aligns the main loop to U*32 B (a full line per
+// iteration, so every store of the unit completes whole lines).
+template <int BODY, int NRED, int NV, int U, int HINT = 0, int LINE = 0>
 __device__ __forceinline__ void direct_long(const StreamArgs &a, int64_t elo, int64_t ehi, int64_t vec_hi,
                                             Acc<BODY, NRED> &acc) {
   constexpr int VEC = BODY == SB_RED_I64 ? 2 : 4;
   constexpr int STEP = VEC * NV;   // elements per load
+  constexpr int AL = LINE ? STEP * U : STEP;
   int64_t e = elo;
-  const int64_t ea = min(ehi, ((elo + STEP - 1) / STEP) * STEP);
+  const int64_t ea = min(ehi, ((elo + AL - 1) / AL) * AL);
   for (; e < ea; ++e) body_scalar<BODY, NRED, false>(a, e, acc, 0, 0);
   const int64_t eb = max(e, min(ehi, vec_hi) / STEP * STEP);
   for (; e + U * STEP <= eb; e += U * STEP) {
@@ -332,6 +335,9 @@ __device__ void direct_run(const StreamArgs &a, const LaneWork &w, Acc<BODY, NRE
           case 4: direct_long<BODY, NRED, 2, 4, 1>(a, elo, ehi, vec_hi, acc); break;
           case 5: direct_long<BODY, NRED, 2, 4, 2>(a, elo, ehi, vec_hi, acc); break;
           case 6: direct_long<BODY, NRED, 2, 2, 1>(a, elo, ehi, vec_hi, acc); break;
+          case 7: direct_long<BODY, NRED, 2, 4, 1, 1>(a, elo, ehi, vec_hi, acc); break;
+          case 8: direct_long<BODY, NRED, 2, 4, 0, 1>(a, elo, ehi, vec_hi, acc); break;
+          case 9: direct_long<BODY, NRED, 2, 2, 1, 1>(a, elo, ehi, vec_hi, acc); break;
           default: direct_long<BODY, NRED, 1, 4>(a, elo, ehi, vec_hi, acc); break;
         }
         continue;

@@ -876,9 +876,10 @@ static upir_status exec_stream(upir_spmd s, const upir_loop_desc *l, const upir_
     }
   }
   a.trace = trace ? (int32_t *)trace->dev : nullptr;
-  // long per-unit chunks: 256-bit loads, 4 in flight for reductions, 2 for
-  // AXPY (read-read-write streams; measured best in tools/sweep_axpy.sh)
-  a.dvar = body == SB_AXPY ? 2 : 1;
+  // long per-unit chunks: 256-bit loads, 4 in flight; AXPY aligns each unit's
+  // main loop to whole 128-B lines so its stores complete lines (measured best
+  // in tools/sweep_axpy.sh: partial-line write-backs cost DRAM re-reads)
+  a.dvar = body == SB_AXPY ? 8 : 1;
   if (const char *dv = getenv("UPIR_DVAR")) a.dvar = atoi(dv);
   // dynamic tickets: m chunks per unit so a ticket covers >= ~256 KiB
   const int p_team = l->distribute == UPIR_DIST_TEAMS ? 1 : sd.num_units;
