@@ -120,6 +120,19 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
 }
 
+// Tile id -> (tile row, tile column) (reading c32): ids enumerate the tiles
+// in groups of GROUP tile rows, column-major inside a group -- a tiling of
+// the tile loop that keeps the tiles running at the same
+// time on a ~GROUP x 10 block, whose A rows and B columns fit in L2.
+constexpr int64_t GROUP = 16;
+__device__ __forceinline__ void tile_coords(int64_t tile, int64_t ntr, int64_t ntc, int64_t &ti, int64_t &tj) {
+  const int64_t per = GROUP * ntc;
+  const int64_t g = tile / per, w = tile % per;
+  const int64_t rows = min(GROUP, ntr - g * GROUP);   // last group may be short
+  ti = g * GROUP + w % rows;
+  tj = w / rows;
+}
+
 // Tile sequence of this team under a static tile schedule (reading c24).
 struct TileSeq {
   int64_t cur, end, k;
@@ -208,7 +221,9 @@ __global__ void __launch_bounds__(Cfg<DT>::THREADS, 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t tile = seq.next(); tile >= 0; tile = seq.next()) {
-        const int m0 = (int)((ti0 + tile / ntc) * BM), n0 = (int)((tj0 + tile % ntc) * BN);
+        int64_t ti, tj;
+        tile_coords(tile, ntr, ntc, ti, tj);
+        const int m0 = (int)((ti0 + ti) * BM), n0 = (int)((tj0 + tj) * BN);
         for (int kb = 0; kb < KB; ++kb) {
           tma_mbar_wait(empty + stage, phase ^ 1);
           char *sa = smem + stage * L::STAGE;
@@ -276,7 +291,9 @@ __global__ void __launch_bounds__(Cfg<DT>::THREADS, 1)
     for (int64_t tile = seq.next(); tile >= 0; tile = seq.next(), ++local) {
       const int acc = local & 1;
       const uint32_t acc_phase = (uint32_t)((local >> 1) & 1);
-      const int64_t m0 = (ti0 + tile / ntc) * BM, n0 = (tj0 + tile % ntc) * BN;
+      int64_t ti, tj;
+      tile_coords(tile, ntr, ntc, ti, tj);
+      const int64_t m0 = (ti0 + ti) * BM, n0 = (tj0 + tj) * BN;
       tma_mbar_wait(tfull + acc, acc_phase);
       tc_fence_after();
       const int64_t row = m0 + 32 * ew + lane;
