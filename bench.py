@@ -517,19 +517,22 @@ def bench_stencil7(args, U, ctx, stream, peaks, peak_src):
         ma, mb, mw = U.upir_data_adopt(ctx, a_t), U.upir_data_adopt(ctx, b_t), U.upir_data_adopt(ctx, w)
         U.upir_synth_fill(ctx, ma, 4, 5, 0, n, n)
         U.upir_synth_fill(ctx, mb, 4, 5, 0, n, n)
-        s = U.upir_spmd_launch(ctx, U.spmd_desc(148 * 4, 256))
-        loop = U.loop_desc([3, 3], [n - 3, n - 3], tile=[16, 128], chunk=1, distribute=U.DIST_TEAMS, inner_chunk=4)
-        body = U.body(U.BODY_STENCIL2D, U.F32, in0=ma, in1=mw, out=mb, ld=(n, 0, 0), dims=(n, 7, 0))
-        for _ in range(3):
-            U.upir_loop_exec(s, loop, body)
-        ms = _time_graph(U, ctx, stream, lambda: U.upir_loop_exec(s, loop, body), 10)
-        U.upir_spmd_end(s)
+        lups = (n - 6) ** 2
+        for teams, units, tile in ((592, 256, (16, 128)), (296, 128, (16, 512)), (148, 256, (16, 1024))):
+            s = U.upir_spmd_launch(ctx, U.spmd_desc(teams, units))
+            loop = U.loop_desc([3, 3], [n - 3, n - 3], tile=list(tile), chunk=1, distribute=U.DIST_TEAMS,
+                               inner_chunk=4)
+            body = U.body(U.BODY_STENCIL2D, U.F32, in0=ma, in1=mw, out=mb, ld=(n, 0, 0), dims=(n, 7, 0))
+            for _ in range(3):
+                U.upir_loop_exec(s, loop, body)
+            ms = _time_graph(U, ctx, stream, lambda: U.upir_loop_exec(s, loop, body), 10)
+            U.upir_spmd_end(s)
+            out[f"{n}x{n} tile {tile[0]}x{tile[1]} {teams}x{units}"] = {
+                "ms_per_sweep": ms, "GLUP/s": lups / (ms / 1e3) / 1e9, "GB/s": 8 * lups / (ms / 1e3) / 1e9,
+                "GFLOP/s": 98 * lups / (ms / 1e3) / 1e9}
         for m in (mw, mb, ma):
             U.upir_data_unmap(ctx, m)
         U.upir_sync(ctx)
-        lups = (n - 6) ** 2
-        out[f"{n}x{n}"] = {"ms_per_sweep": ms, "GLUP/s": lups / (ms / 1e3) / 1e9,
-                           "GB/s": 8 * lups / (ms / 1e3) / 1e9, "GFLOP/s": 98 * lups / (ms / 1e3) / 1e9}
         del a_t, b_t
     return {"workload": "2-D 7x7 filter stencil (49 taps, fp32 FMA), tiles 16x128 static,1 over 592 teams, "
                         "static,4 over 256 units; one sweep per launch", "bound": "alu (49 FMA per point)",

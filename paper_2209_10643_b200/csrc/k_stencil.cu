@@ -19,13 +19,33 @@ namespace {
 template <int R, int BM, int BN>
 struct SLayout {
   static constexpr int F = 2 * R + 1, WR = BM + 2 * R, WC = BN + 8;
+  // TMA boxes are at most 256 columns wide: a wide window is NB boxes of 256
+  // columns plus one of 8, each landing as its own dense [WR][box] block
+  static constexpr bool WIDE = WC > 256;
+  static constexpr int NB = WIDE ? (WC - 8) / 256 : 0;
   static constexpr int BUF = ((WR * WC * 4) + 127) / 128 * 128;
   static constexpr int SMEM = 2 * BUF + 256 + F * F * 4 + 128;
 };
 
+// smem offset (floats) of window (row, col) -- col a multiple of 4 for vectors
 template <int R, int BM, int BN>
-__global__ void __launch_bounds__(1024) stencil_kernel(const __grid_constant__ StencilArgs a,
-                                                       const __grid_constant__ CUtensorMap tmw) {
+__device__ __forceinline__ int win_off(int row, int col) {
+  using L = SLayout<R, BM, BN>;
+  if constexpr (!L::WIDE) {
+    return row * L::WC + col;
+  } else {
+    const int sub = col >> 8;
+    if (sub < L::NB) return sub * (L::WR * 256) + row * 256 + (col & 255);
+    return L::NB * (L::WR * 256) + row * 8 + (col - L::NB * 256);
+  }
+}
+
+// MAXT: the team size the kernel is compiled for (256 lets the 49 taps stay
+// in registers; 1024 caps registers at 64 for teams of up to 1024 units).
+template <int R, int BM, int BN, int MAXT>
+__global__ void __launch_bounds__(MAXT) stencil_kernel(const __grid_constant__ StencilArgs a,
+                                                       const __grid_constant__ CUtensorMap tmw,
+                                                       const __grid_constant__ CUtensorMap tmw8) {
   // window column c holds global column j0 - 4 + c (4-aligned so that a
   // unit's taps are read as 16-B vectors)
   using L = SLayout<R, BM, BN>;
@@ -38,6 +58,9 @@ __global__ void __launch_bounds__(1024) stencil_kernel(const __grid_constant__ S
   const int units = blockDim.x, u = threadIdx.x;
   for (int e = threadIdx.x; e < F * F; e += blockDim.x) w[e] = a.w[e];
   __syncthreads();
+  float wr[F * F];   // the taps live in registers for the whole kernel
+#pragma unroll
+  for (int e = 0; e < F * F; ++e) wr[e] = w[e];
   const int64_t nt = a.ntr * a.ntc;
   // tile iterator (thread 0), as the Jacobi body
   int64_t cur = 0, end = 0, kk = 0;
@@ -70,10 +93,20 @@ __global__ void __launch_bounds__(1024) stencil_kernel(const __grid_constant__ S
     tma_fence_proxy();
     tma_mbar_expect_tx(bars + buf, WR * WCP * 4);
     // window rows [i0-R, i0+BM+R) x cols [j0-4, j0+BN+4) of the local buffer
-    tma_load_2d(smc + buf * L::BUF, &tmw, (int)(j0 - 4), (int)(i0 - R - a.row0), bars + buf);
+    if constexpr (!L::WIDE) {
+      tma_load_2d(smc + buf * L::BUF, &tmw, (int)(j0 - 4), (int)(i0 - R - a.row0), bars + buf);
+    } else {
+#pragma unroll
+      for (int q = 0; q < L::NB; ++q)
+        tma_load_2d(smc + buf * L::BUF + q * (WR * 256 * 4), &tmw, (int)(j0 - 4 + 256 * q), (int)(i0 - R - a.row0),
+                    bars + buf);
+      tma_load_2d(smc + buf * L::BUF + L::NB * (WR * 256 * 4), &tmw8, (int)(j0 - 4 + 256 * L::NB),
+                  (int)(i0 - R - a.row0), bars + buf);
+    }
   };
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmw);
+    if constexpr (L::WIDE) tma_prefetch_desc(&tmw8);
     tma_mbar_init(bars + 0, 1);
     tma_mbar_init(bars + 1, 1);
     tma_fence_init();
@@ -95,7 +128,71 @@ __global__ void __launch_bounds__(1024) stencil_kernel(const __grid_constant__ S
     const float *win = reinterpret_cast<const float *>(smc + buf * L::BUF);
     const int64_t i0 = (a.ti0 + tile / a.ntc) * BM, j0 = (a.tj0 + tile % a.ntc) * BN;
     const int ic = a.inner_chunk;
-    if (ic == 4) {
+    if (ic == 4 && BN == 4 * MAXT && units == MAXT && MAXT <= 256) {
+      // static,4 with BN = 4 * units: unit u owns the 4-column strip c = 4u of
+      // every tile row (chunk k = r*units + u), visited top to bottom -- a
+      // sliding window of F input rows in registers: 3 LDS.128 per 4 outputs.
+      const int c = 4 * u;
+      const int64_t j = j0 + c;
+      float v[F][12];
+#pragma unroll
+      for (int p = 0; p < F - 1; ++p) {
+#pragma unroll
+        for (int q = 0; q < 3; ++q) {
+          const float4 t4 = *reinterpret_cast<const float4 *>(win + win_off<R, BM, BN>(p, c + 4 * q));
+          v[p][4 * q] = t4.x;
+          v[p][4 * q + 1] = t4.y;
+          v[p][4 * q + 2] = t4.z;
+          v[p][4 * q + 3] = t4.w;
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < BM; ++r) {
+        {   // bring in window row r + F - 1
+#pragma unroll
+          for (int q = 0; q < 3; ++q) {
+            const float4 t4 = *reinterpret_cast<const float4 *>(win + win_off<R, BM, BN>(r + F - 1, c + 4 * q));
+            v[F - 1][4 * q] = t4.x;
+            v[F - 1][4 * q + 1] = t4.y;
+            v[F - 1][4 * q + 2] = t4.z;
+            v[F - 1][4 * q + 3] = t4.w;
+          }
+        }
+        const int64_t i = i0 + r;
+        if (i >= a.lb0 && i < a.ub0 && j + 3 >= a.lb1 && j < a.ub1) {
+          float acc[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+          for (int p = 0; p < F; ++p)
+#pragma unroll
+            for (int q = 0; q < F; ++q)
+#pragma unroll
+              for (int t = 0; t < 4; ++t) acc[t] = __fmaf_rn(wr[p * F + q], v[p][4 - R + t + q], acc[t]);
+          float *dst = a.out + (i - a.row0) * a.ld + j;
+          if (j >= a.lb1 && j + 4 <= a.ub1 && ((uintptr_t)dst & 15) == 0) {
+            __stcs(reinterpret_cast<float4 *>(dst), make_float4(acc[0], acc[1], acc[2], acc[3]));
+          } else {
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              if (j + t >= a.lb1 && j + t < a.ub1) dst[t] = acc[t];
+          }
+          if (a.trace) {
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+              if (j + t >= a.lb1 && j + t < a.ub1) {
+                const int64_t idx = tile * POS + r * BN + c + t;
+                a.trace[idx] = blockIdx.x;
+                a.trace[nt * POS + idx] = u;
+                atomicAdd(a.trace + 2 * nt * POS + idx, 1);
+              }
+          }
+        }
+        // slide the window down one row
+#pragma unroll
+        for (int p = 0; p < F - 1; ++p)
+#pragma unroll
+          for (int q = 0; q < 12; ++q) v[p][q] = v[p + 1][q];
+      }
+    } else if (ic == 4) {
       for (int k = u; k * 4 < POS; k += units) {
         const int r = (k * 4) / BN, c = (k * 4) % BN;
         const int64_t i = i0 + r, j = j0 + c;
@@ -105,10 +202,9 @@ __global__ void __launch_bounds__(1024) stencil_kernel(const __grid_constant__ S
         for (int p = 0; p < F; ++p) {
           // window columns c .. c+11 = global j-4 .. j+7 as three 16-B vectors
           float v[12];
-          const float4 *rowp = reinterpret_cast<const float4 *>(win + (r + p) * WCP + c);
 #pragma unroll
           for (int q = 0; q < 3; ++q) {
-            const float4 t4 = rowp[q];
+            const float4 t4 = *reinterpret_cast<const float4 *>(win + win_off<R, BM, BN>(r + p, c + 4 * q));
             v[4 * q] = t4.x;
             v[4 * q + 1] = t4.y;
             v[4 * q + 2] = t4.z;
@@ -116,7 +212,7 @@ __global__ void __launch_bounds__(1024) stencil_kernel(const __grid_constant__ S
           }
 #pragma unroll
           for (int q = 0; q < F; ++q) {
-            const float wq = w[p * F + q];
+            const float wq = wr[p * F + q];
 #pragma unroll
             for (int t = 0; t < 4; ++t) acc[t] = __fmaf_rn(wq, v[4 - R + t + q], acc[t]);
           }
@@ -148,7 +244,7 @@ __global__ void __launch_bounds__(1024) stencil_kernel(const __grid_constant__ S
           if (i < a.lb0 || i >= a.ub0 || j < a.lb1 || j >= a.ub1) continue;
           float acc = 0.f;
           for (int p = 0; p < F; ++p)
-            for (int q = 0; q < F; ++q) acc = __fmaf_rn(w[p * F + q], win[(r + p) * WCP + c + 4 - R + q], acc);
+            for (int q = 0; q < F; ++q) acc = __fmaf_rn(w[p * F + q], win[win_off<R, BM, BN>(r + p, c + 4 - R + q)], acc);
           a.out[(i - a.row0) * a.ld + j] = acc;
           if (a.trace) {
             const int64_t idx = tile * POS + pos;
@@ -177,21 +273,27 @@ __global__ void __launch_bounds__(1024) stencil_kernel(const __grid_constant__ S
 template <int R, int BM, int BN>
 cudaError_t launch_r(const StencilArgs &a, int teams, int units, cudaStream_t s) {
   using L = SLayout<R, BM, BN>;
-  CUtensorMap tm;
+  CUtensorMap tm, tm8;
   if (!encode_tmap_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, a.in, (uint64_t)a.nx, (uint64_t)(a.ny - a.row0),
-                      (uint64_t)a.ld * 4, L::WC, L::WR, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B))
+                      (uint64_t)a.ld * 4, L::WIDE ? 256 : L::WC, L::WR, CU_TENSOR_MAP_SWIZZLE_NONE,
+                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B) ||
+      !encode_tmap_2d(&tm8, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, a.in, (uint64_t)a.nx, (uint64_t)(a.ny - a.row0),
+                      (uint64_t)a.ld * 4, 8, L::WR, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B))
     return cudaErrorInvalidValue;
-  auto k = stencil_kernel<R, BM, BN>;
+  auto k = (BN == 512 && units == 128)   ? stencil_kernel<R, BM, BN, 128>
+           : units <= 256                 ? stencil_kernel<R, BM, BN, 256>
+                                          : stencil_kernel<R, BM, BN, 1024>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
   if (e != cudaSuccess) return e;
-  k<<<teams, units, L::SMEM, s>>>(a, tm);
+  k<<<teams, units, L::SMEM, s>>>(a, tm, tm8);
   return cudaGetLastError();
 }
 
 }  // namespace
 
 bool stencil_supported(int F, int bm, int bn) {
-  return (F == 3 || F == 5 || F == 7) && ((bm == 16 && bn == 128) || (bm == 8 && bn == 64));
+  return (F == 3 || F == 5 || F == 7) &&
+         ((bm == 16 && bn == 128) || (bm == 8 && bn == 64) || (bm == 16 && bn == 512) || (bm == 16 && bn == 1024));
 }
 
 cudaError_t launch_stencil(const StencilArgs &a, int F, int bm, int bn, int teams, int units, cudaStream_t s) {
@@ -203,6 +305,12 @@ cudaError_t launch_stencil(const StencilArgs &a, int F, int bm, int bn, int team
   UPIR_ST(1, 8, 64)
   UPIR_ST(2, 8, 64)
   UPIR_ST(3, 8, 64)
+  UPIR_ST(1, 16, 512)
+  UPIR_ST(2, 16, 512)
+  UPIR_ST(3, 16, 512)
+  UPIR_ST(1, 16, 1024)
+  UPIR_ST(2, 16, 1024)
+  UPIR_ST(3, 16, 1024)
 #undef UPIR_ST
   return cudaErrorInvalidValue;
 }

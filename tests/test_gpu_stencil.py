@@ -109,3 +109,27 @@ def test_stencil_trace_mapping(ctx):
     it = ot >= 0
     assert (tr[2 * n:][it] == 1).all() and (tr[2 * n:][~it] == 0).all()
     assert (tr[:n][it] == ot[it]).all() and (tr[n:2 * n][it] == ou[it]).all()
+
+
+@pytest.mark.parametrize("tile,units", [((16, 512), 128), ((16, 1024), 256), ((16, 512), 64)])
+@pytest.mark.parametrize("F", [7, 3])
+def test_stencil_strip_tiles(ctx, tile, units, F):
+    """BN = 4 * units: each unit owns one 4-column strip of the tile (static,4),
+    computed with a sliding register window; other unit counts use the
+    generic path for the same tile."""
+    g = synth.jacobi_init(75, 1100)
+    w = weights(F)
+    out, _ = stencil_gpu(ctx, g, w, S=2, teams=5, units=units, tile=tile)
+    assert err(out, g, w, 2) <= 1e-5
+
+
+def test_stencil_strip_trace(ctx):
+    g = synth.jacobi_init(40, 600)
+    w = weights(7)
+    teams, units, tile = 3, 128, (16, 512)
+    _, tr = stencil_gpu(ctx, g, w, teams=teams, units=units, tile=tile, chunk=1, trace=True)
+    n = len(tr) // 3
+    ot, ou = oracle.tiled_owner(3, 37, 3, 597, tile[0], tile[1], oracle.STATIC, 1, teams, 4, units)
+    it = ot >= 0
+    assert (tr[2 * n:][it] == 1).all() and (tr[2 * n:][~it] == 0).all()
+    assert (tr[:n][it] == ot[it]).all() and (tr[n:2 * n][it] == ou[it]).all()
