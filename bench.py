@@ -132,6 +132,16 @@ def dist_env():
     return rank, world, local
 
 
+C2_METRIC = "GB/s per upir.loop reduction (int64+fp32 sum/max, n=2^30 per GPU)"
+
+
+def c2_config(sched, world):
+    return {"workload": "C2: int64 and fp32 sum/max reduction, n=2^30 per GPU, teams x units 592x256, "
+                        f"schedule {sched}, map to/from",
+            "teams": 592, "units": 256, "schedule": sched,
+            "l2": "inputs 12 GiB per GPU >> 126 MB L2 (no flush needed)", "parallelism": f"dp{world}"}
+
+
 # --------------------------------------------------------------------------- reference arm
 def run_reference(args):
     """The oracle (plain sequential CPU interpreter) as the reference arm, on a
@@ -160,12 +170,11 @@ def run_reference(args):
     dt = (time.perf_counter() - t0) / args.steps
     gbs = n * 12 / dt / 1e9
     print(json.dumps({
-        "impl": "reference", "metric": "reduction GB/s (int64+fp32 sum/max, n=2^30 per GPU)",
+        "impl": "reference", "metric": C2_METRIC,
         "value": gbs, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": dt * 1e3 * (1 << 30) / n, "higher_is_better": True, "scaling": "weak",
         "vs_baseline": None, "dtype": "i64+f32", "data": "synthetic",
-        "config": {"workload": "C2: int64 and fp32 sum/max reduction, n=2^30, teams x units SPMD, map to/from",
-                   "sample": "n=2^24 of the same stream"},
+        "config": dict(c2_config(args.sched or "static", world), sample="n=2^24 of the same stream per step"),
         "cpu_baseline": {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "oracle",
                          "sample": "2^24 int64 + 2^24 fp32 elements (sum and max each), scaled by bytes"},
         "e2e": {"value": gbs, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -394,15 +403,11 @@ def bench_reduce(args, U, ctx, stream, barrier, rank, world, peaks, peak_src):
     ach_f = n * 4 / (kf / 1e3) / 1e9
     peak = float(peaks["hbm_gbs"])
     return {
-        "metric": "GB/s per upir.loop reduction (int64+fp32 sum/max, n=2^30 per GPU)",
+        "metric": C2_METRIC,
         "value": None, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
         "ms_per_step": ms, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "i64+f32", "data": "synthetic",
-        "config": {"workload": "C2: int64 and fp32 sum/max reduction, n=2^30 per GPU, teams x units "
-                               f"{teams}x{units}, schedule {args.sched}, map to/from",
-                   "n_per_gpu": n, "teams": teams, "units": units, "schedule": args.sched,
-                   "l2": "inputs 12 GiB per GPU >> 126 MB L2 (no flush needed)",
-                   "parallelism": f"dp{world}"},
+        "config": dict(c2_config(args.sched, world), n_per_gpu=n),
         "roofline": {"bound": "hbm", "achieved": ach_i, "peak": peak, "unit": "GB/s",
                      "frac": ach_i / peak, "traffic": ncu_traffic("reduce_i64"),
                      "kernel": "stream_loop_kernel<RED_I64,2>", "peak_source": peak_src,
