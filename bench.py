@@ -601,6 +601,30 @@ def bench_matmul(args, U, ctx, stream, peaks, peak_src, n=8192):
     del A, B
     tflops = 2.0 * n ** 3 / (ms / 1e3) / 1e12
     peak = float(peaks.get("bf16_tflops", 1590.0))
+    # CTA pairs (cta_group::2): 74 teams of 2 CTAs = 512 units, 256 x 256 tiles
+    pair = {}
+    A2 = torch.empty(n * n, dtype=torch.bfloat16, device="cuda")
+    B2 = torch.empty(n * n, dtype=torch.bfloat16, device="cuda")
+    torch.cuda.synchronize()
+    ma2, mb2, mc = U.upir_data_adopt(ctx, A2), U.upir_data_adopt(ctx, B2), U.upir_data_adopt(ctx, C)
+    U.upir_synth_fill(ctx, ma2, 3, 3)
+    U.upir_synth_fill(ctx, mb2, 3, 4)
+    try:
+        sp = U.upir_spmd_launch(ctx, U.spmd_desc(74, 512))
+        bodyp = U.body(U.BODY_MATMUL, U.BF16, in0=ma2, in1=mb2, out=mc, ld=(n, n, n), dims=(n, n, n))
+        for _ in range(3):
+            U.upir_loop_exec(sp, loop, bodyp)
+        msp = _time_graph(U, ctx, stream, lambda: U.upir_loop_exec(sp, loop, bodyp), reps)
+        U.upir_spmd_end(sp)
+        pair = {"ms": msp, "TFLOP/s": 2.0 * n ** 3 / (msp / 1e3) / 1e12,
+                "frac": 2.0 * n ** 3 / (msp / 1e3) / 1e12 / peak,
+                "geometry": "74 teams x 512 units (CTA pairs, tcgen05.mma.cta_group::2, 256x256 tiles)"}
+    except Exception as e:
+        pair = {"error": str(e)[:200]}
+    for m in (mc, mb2, ma2):
+        U.upir_data_unmap(ctx, m)
+    U.upir_sync(ctx)
+    del A2, B2
     # fp32 inputs (3xTF32 on kind::tf32): 384 units per team
     A32 = torch.empty(n * n, dtype=torch.float32, device="cuda")
     B32 = torch.empty(n * n, dtype=torch.float32, device="cuda")
@@ -621,7 +645,7 @@ def bench_matmul(args, U, ctx, stream, peaks, peak_src, n=8192):
     fp32_tflops = 2.0 * n ** 3 / (ms32 / 1e3) / 1e12
     return {"workload": f"C4: bf16 matmul {n}^3 -> fp32, 128x256 tiles static,1 over {teams} teams x 256 units "
                         "(tcgen05.mma kind::f16, TMA SW128, TMEM accumulators)",
-            "ms": ms, "TFLOP/s": tflops, "bound": "tensor",
+            "ms": ms, "TFLOP/s": tflops, "bound": "tensor", "cta_pair_bf16": pair,
             "fp32_3xtf32": {"ms": ms32, "TFLOP/s": fp32_tflops, "tensor_TFLOP/s": 3 * fp32_tflops,
                             "peak_tf32": tf32_peak, "frac_of_tf32_over_3": fp32_tflops / (tf32_peak / 3),
                             "peak_source": peak_src + " bf16 burst x nominal tf32/bf16 ratio 1/2"},

@@ -369,11 +369,240 @@ __global__ void __launch_bounds__(Cfg<DT>::THREADS, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(TMEM_COLS));
 }
 
+// ---------------------------------------------------------------------------
+// CTA-pair variant (bf16): a TEAM is a cluster of 2 CTAs (reading c24: "team =
+// the CTA pair when cta_group::2 is used"), 2 x 256 = 512 units.  The pair
+// owns 256 x 256 output tiles: CTA r stages A rows [m0 + 128 r, +128) and B
+// columns [n0 + 128 r, +128); the leader issues tcgen05.mma.cta_group::2
+// (M = 256, N = 256) over both CTAs' shared memory; each CTA's TMEM receives
+// its 128 rows.  Both CTAs' TMA loads complete on the LEADER's full barrier
+// (cp.async.bulk.tensor ... .cta_group::2), MMA completion is multicast to
+// both CTAs' empty / tmem-full barriers, and both epilogues release the
+// accumulator on the leader's tmem-empty barrier.  B traffic per SM halves.
+constexpr int PBM = 256, PSTAGES = 6;
+constexpr int P_A = 128 * 64 * 2;              // this CTA's A rows
+constexpr int P_B = 64 * 128 * 2;              // this CTA's B columns (2 boxes)
+constexpr int P_STAGE = P_A + P_B;
+constexpr int P_SMEM = PSTAGES * P_STAGE + 1024 + 256;
+constexpr uint32_t P_IDESC = (1u << 4) | (1u << 7) | (1u << 10) | (0u << 15) | (1u << 16) |
+                             ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(PBM >> 4) << 24);
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;\n" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t map_to_cta(uint32_t smem_addr, uint32_t cta) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;\n" : "=r"(r) : "r"(smem_addr), "r"(cta));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_2d_pair(void *dst, const void *tmap, int c0, int c1, uint32_t bar_cluster) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], "
+      "[%4];\n" ::"r"(tma_smem(dst)),
+      "l"(tmap), "r"(c0), "r"(c1), "r"(bar_cluster)
+      : "memory");
+}
+__device__ __forceinline__ void mma_pair(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::f16 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(P_IDESC), "r"(accum));
+}
+__device__ __forceinline__ void commit_pair(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n" ::"r"(
+          tma_smem(bar)),
+      "h"((uint16_t)0x3)
+      : "memory");
+}
+__device__ __forceinline__ void remote_arrive(uint32_t bar_cluster) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];\n" ::"r"(bar_cluster) : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
+    matmul_pair_kernel(const __grid_constant__ MatmulArgs a, const __grid_constant__ CUtensorMap tma,
+                       const __grid_constant__ CUtensorMap tmb) {
+  extern __shared__ __align__(1024) char smem_raw[];
+  char *smem = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + PSTAGES * P_STAGE);
+  uint64_t *empty = full + PSTAGES;
+  uint64_t *tfull = empty + PSTAGES;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+
+  const int64_t ti0 = a.lb0 / PBM, tj0 = a.lb1 / BN;
+  const int64_t ntr = (a.ub0 + PBM - 1) / PBM - ti0, ntc = (a.ub1 + BN - 1) / BN - tj0;
+  const int64_t nt = ntr * ntc;
+  const int KB = (int)((a.K + 64 - 1) / 64);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tma);
+    tma_prefetch_desc(&tmb);
+    for (int st = 0; st < PSTAGES; ++st) {
+      tma_mbar_init(full + st, 1);
+      tma_mbar_init(empty + st, 1);
+    }
+    for (int st = 0; st < 2; ++st) {
+      tma_mbar_init(tfull + st, 1);
+      tma_mbar_init(tempty + st, 8);   // 4 epilogue warps x 2 CTAs (leader's copy is used)
+    }
+    tma_fence_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tma_smem(tmem_holder)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  // the pair's tile sequence (teams = pairs)
+  TileSeq seq;
+  {
+    seq.sched = a.sched;
+    seq.chunk = a.chunk;
+    seq.nt = nt;
+    seq.p = gridDim.x / 2;
+    seq.t = blockIdx.x / 2;
+    if (seq.sched == SK_STATIC_BLOCK) {
+      const int64_t q = nt / seq.p, r = nt % seq.p;
+      seq.cur = seq.t * q + (seq.t < r ? seq.t : r);
+      seq.end = seq.cur + q + (seq.t < r ? 1 : 0);
+      seq.k = 0;
+    } else {
+      seq.k = seq.t;
+      seq.cur = seq.k * seq.chunk;
+      seq.end = min(nt, seq.cur + seq.chunk);
+    }
+  }
+
+  if (warp == 0) {
+    if (lane == 0) {   // ---------------- TMA producer (both CTAs)
+      const uint32_t full_leader = map_to_cta(tma_smem(full), 0);
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t tile = seq.next(); tile >= 0; tile = seq.next()) {
+        int64_t ti, tj;
+        tile_coords(tile, ntr, ntc, ti, tj);
+        const int m0 = (int)((ti0 + ti) * PBM + 128 * rank), n0 = (int)((tj0 + tj) * BN + 128 * rank);
+        for (int kb = 0; kb < KB; ++kb) {
+          tma_mbar_wait(empty + stage, phase ^ 1);
+          char *sa = smem + stage * P_STAGE;
+          char *sb = sa + P_A;
+          if (leader) tma_mbar_expect_tx(full + stage, 2 * P_STAGE);
+          const uint32_t fb = full_leader + (uint32_t)(stage * 8);
+          tma_load_2d_pair(sa, &tma, kb * 64, m0 - (int)a.row0, fb);
+          tma_load_2d_pair(sb, &tmb, n0, kb * 64, fb);
+          tma_load_2d_pair(sb + 8192, &tmb, n0 + 64, kb * 64, fb);
+          if (++stage == PSTAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {   // ---------------- MMA issuer (leader CTA only)
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int64_t tile = seq.next(); tile >= 0; tile = seq.next(), ++local) {
+        const int acc = local & 1;
+        const uint32_t acc_phase = (uint32_t)((local >> 1) & 1);
+        tma_mbar_wait(tempty + acc, acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < KB; ++kb) {
+          tma_mbar_wait(full + stage, phase);
+          tc_fence_after();
+          const char *sa = smem + stage * P_STAGE;
+          const char *sb = sa + P_A;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t ad = smem_desc(sa + k * 32, 16, 1024);
+            const uint64_t bd = smem_desc(sb + k * 2048, 8192, 1024);
+            mma_pair(tmem_d, ad, bd, (kb | k) != 0);
+          }
+          commit_pair(empty + stage);   // both CTAs' smem stages free
+          if (++stage == PSTAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        commit_pair(tfull + acc);   // both CTAs' accumulators ready
+      }
+    }
+  } else if (warp >= 4) {   // ---------------- epilogue (both CTAs)
+    const int ew = warp & 3;
+    const uint32_t tempty_leader = map_to_cta(tma_smem(tempty), 0);
+    int local = 0;
+    for (int64_t tile = seq.next(); tile >= 0; tile = seq.next(), ++local) {
+      const int acc = local & 1;
+      const uint32_t acc_phase = (uint32_t)((local >> 1) & 1);
+      int64_t ti, tj;
+      tile_coords(tile, ntr, ntc, ti, tj);
+      const int64_t m0 = (ti0 + ti) * PBM + 128 * rank, n0 = (tj0 + tj) * BN;
+      tma_mbar_wait(tfull + acc, acc_phase);
+      tc_fence_after();
+      const int64_t row = m0 + 32 * ew + lane;
+      const bool row_ok = row >= a.lb0 && row < a.ub0;
+      float *crow = a.C + (row - a.row0) * a.ldc;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((uint32_t)(32 * ew) << 16) + (uint32_t)(acc * BN + c), r);
+        const int64_t col0 = n0 + c;
+        if (!row_ok) continue;
+        if (col0 >= a.lb1 && col0 + 32 <= a.ub1) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(crow + col0 + 8 * q),
+                         "r"(r[8 * q]), "r"(r[8 * q + 1]), "r"(r[8 * q + 2]), "r"(r[8 * q + 3]), "r"(r[8 * q + 4]),
+                         "r"(r[8 * q + 5]), "r"(r[8 * q + 6]), "r"(r[8 * q + 7])
+                         : "memory");
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; ++q)
+            if (col0 + q >= a.lb1 && col0 + q < a.ub1) crow[col0 + q] = __uint_as_float(r[q]);
+        }
+      }
+      if (a.trace && leader && ew == 0 && lane == 0) {
+        a.trace[tile] = (int32_t)(blockIdx.x / 2);
+        a.trace[nt + tile] = 0;
+        atomicAdd(a.trace + 2 * nt + tile, 1);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) remote_arrive(tempty_leader + (uint32_t)(acc * 8));
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(TMEM_COLS));
+}
+
 }  // namespace
 
 int matmul_tile_m() { return BM; }
 int matmul_tile_n() { return BN; }
 int matmul_required_units(int dtype) { return dtype == UPIR_F32 ? Cfg<UPIR_F32>::THREADS : Cfg<UPIR_BF16>::THREADS; }
+// bf16 teams may also be CTA pairs (512 units, 256-row tiles)
+bool matmul_units_ok(int dtype, int units) {
+  return units == matmul_required_units(dtype) || (dtype == UPIR_BF16 && units == 512);
+}
+int matmul_tile_m_for(int dtype, int units) { return (dtype == UPIR_BF16 && units == 512) ? PBM : BM; }
 
 bool matmul_encode_tmaps(void *tma, void *tmb, const void *A, const void *B, int dtype, int64_t M, int64_t N,
                          int64_t K, int64_t lda, int64_t ldb) {
@@ -398,6 +627,13 @@ static cudaError_t launch_dt(const MatmulArgs &a, int teams, cudaStream_t s) {
 }
 
 cudaError_t launch_matmul(const MatmulArgs &a, int dtype, int teams, int units, cudaStream_t s) {
+  if (dtype == UPIR_BF16 && units == 512) {
+    cudaError_t e = cudaFuncSetAttribute(matmul_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, P_SMEM);
+    if (e != cudaSuccess) return e;
+    matmul_pair_kernel<<<2 * teams, 256, P_SMEM, s>>>(a, *reinterpret_cast<const CUtensorMap *>(a.tmap_a),
+                                                     *reinterpret_cast<const CUtensorMap *>(a.tmap_b));
+    return cudaGetLastError();
+  }
   if (units != matmul_required_units(dtype)) return cudaErrorInvalidValue;
   if (dtype == UPIR_BF16) return launch_dt<UPIR_BF16>(a, teams, s);
   if (dtype == UPIR_F32) return launch_dt<UPIR_F32>(a, teams, s);

@@ -146,5 +146,7 @@ bool matmul_encode_tmaps(void *tma, void *tmb, const void *A, const void *B, int
 int matmul_tile_m();
 int matmul_tile_n();
 int matmul_required_units(int dtype);
+bool matmul_units_ok(int dtype, int units);
+int matmul_tile_m_for(int dtype, int units);
 
 }  // namespace upir

@@ -1212,9 +1212,10 @@ static upir_status exec_matmul(upir_spmd s, const upir_loop_desc *l, const upir_
     row0 = mA->loc_row_lo;
     rows_here = mA->loc_row_hi - mA->loc_row_lo;
   }
-  if (sd.num_units != matmul_required_units(b->dtype))
-    return fail(UPIR_E_INVALID, "the tcgen05 MATMUL body runs %d units per team for this dtype (got %d): geometry is not clamped",
-                matmul_required_units(b->dtype), sd.num_units);
+  if (!matmul_units_ok(b->dtype, sd.num_units))
+    return fail(UPIR_E_INVALID,
+                "the tcgen05 MATMUL body runs %d units per team for this dtype (bf16 also 512 = a CTA pair; got %d): "
+                "geometry is not clamped", matmul_required_units(b->dtype), sd.num_units);
   int sk;
   int64_t chunk;
   if ((st = tile_sched(l, sk, chunk)) != UPIR_OK) return st;
@@ -1240,7 +1241,7 @@ static upir_status exec_matmul(upir_spmd s, const upir_loop_desc *l, const upir_
   if (a.ub0 <= a.lb0 || a.ub1 <= a.lb1) return UPIR_OK;
   a.sched = sk;
   a.chunk = chunk;
-  const int64_t bm = matmul_tile_m(), bn = matmul_tile_n();
+  const int64_t bm = matmul_tile_m_for(b->dtype, sd.num_units), bn = matmul_tile_n();
   const int64_t nt = ((a.ub0 + bm - 1) / bm - a.lb0 / bm) * ((a.ub1 + bn - 1) / bn - a.lb1 / bn);
   if (trace) {
     if ((st = check_map(c, trace, "trace")) != UPIR_OK) return st;

@@ -30,14 +30,15 @@ def to_bf16_bits(x):
 
 
 def matmul_gpu(ctx, A, B, teams=148, policy=U.SCHED_STATIC, chunk=1, space=None, trace=False, C0=None,
-               dtype=U.BF16):
+               dtype=U.BF16, units=None):
     M, K = A.shape
     _, N = B.shape
     if dtype == U.BF16:
         a, b = to_bf16_bits(A), to_bf16_bits(B)
     else:
         a, b = np.ascontiguousarray(A, np.float32), np.ascontiguousarray(B, np.float32)
-    units = 256 if dtype == U.BF16 else 384
+    units = units or (256 if dtype == U.BF16 else 384)
+    tm_rows = 256 if units == 512 else 128
     C = np.zeros((M, N), np.float32) if C0 is None else C0.copy()
     ma = U.upir_data_map(ctx, a, U.MAP_TO)
     mb = U.upir_data_map(ctx, b, U.MAP_TO)
@@ -45,7 +46,7 @@ def matmul_gpu(ctx, A, B, teams=148, policy=U.SCHED_STATIC, chunk=1, space=None,
     lb0, ub0, lb1, ub1 = space or (0, M, 0, N)
     tr = tm = None
     if trace:
-        nt = ((ub0 + 127) // 128 - lb0 // 128) * ((ub1 + 255) // 256 - lb1 // 256)
+        nt = ((ub0 + tm_rows - 1) // tm_rows - lb0 // tm_rows) * ((ub1 + 255) // 256 - lb1 // 256)
         tr = np.zeros(3 * nt, np.int32)
         tm = U.upir_data_map(ctx, tr, U.MAP_TOFROM)
     s = U.upir_spmd_launch(ctx, U.spmd_desc(teams, units))
@@ -244,3 +245,39 @@ def test_matmul_cluster_block_rows_world1(ctx):
         U.upir_data_unmap(ctx, m)
     U.upir_sync(ctx)
     assert scaled_err(C, A, B, oracle.matmul(A, B)) <= 1e-5
+
+
+
+# ---- CTA pairs (cta_group::2): a team = 2 CTAs = 512 units, 256 x 256 tiles ----------
+@pytest.mark.parametrize("M,N,K", [(256, 256, 64), (512, 768, 256), (300, 520, 136), (1024, 1024, 1024)])
+def test_matmul_pair_parity(ctx, M, N, K):
+    A = synth.bf16_sym_as_f32(3, 0, M * K).reshape(M, K)
+    B = synth.bf16_sym_as_f32(4, 0, K * N).reshape(K, N)
+    C, _ = matmul_gpu(ctx, A, B, teams=74, units=512)
+    assert scaled_err(C, A, B, oracle.matmul(A, B)) <= 1e-5
+
+
+def test_matmul_pair_exact_and_trace(ctx):
+    rng = np.random.default_rng(8)
+    M, N, K = 768, 1024, 320
+    A = rng.integers(-2, 3, (M, K)).astype(np.float32)
+    B = rng.integers(-2, 3, (K, N)).astype(np.float32)
+    C, tr = matmul_gpu(ctx, A, B, teams=5, units=512, chunk=1, trace=True)
+    assert (C == oracle.matmul(A, B)).all()
+    nt = len(tr) // 3
+    assert (tr[2 * nt:] == 1).all()
+    assert (tr[:nt] == oracle.tile_owner(M, N, 256, 256, oracle.STATIC, 1, 5)).all()
+
+
+def test_matmul_pair_subspace(ctx):
+    M, N, K = 600, 704, 64
+    A = synth.bf16_sym_as_f32(3, 0, M * K).reshape(M, K)
+    B = synth.bf16_sym_as_f32(4, 0, K * N).reshape(K, N)
+    C0 = np.full((M, N), -7.0, np.float32)
+    C, _ = matmul_gpu(ctx, A, B, teams=3, units=512, space=(37, 590, 100, 600), C0=C0)
+    ref = oracle.matmul(A, B)
+    sub = np.s_[37:590, 100:600]
+    assert scaled_err(C[sub], A[37:590], B[:, 100:600], ref[sub]) <= 1e-5
+    mask = np.ones((M, N), bool)
+    mask[sub] = False
+    assert (C[mask] == -7.0).all()
