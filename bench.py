@@ -643,13 +643,18 @@ def bench_matmul(args, U, ctx, stream, peaks, peak_src, n=8192):
     del A32, B32
     tf32_peak = peak / 2.0      # tf32 dense = 1/2 of bf16 (nominal ratio) x measured bf16
     fp32_tflops = 2.0 * n ** 3 / (ms32 / 1e3) / 1e12
-    return {"workload": f"C4: bf16 matmul {n}^3 -> fp32, 128x256 tiles static,1 over {teams} teams x 256 units "
-                        "(tcgen05.mma kind::f16, TMA SW128, TMEM accumulators)",
-            "ms": ms, "TFLOP/s": tflops, "bound": "tensor", "cta_pair_bf16": pair,
+    # headline: the better of the single-CTA and CTA-pair realisations of the
+    # same collapse(2) loop (both parity-tested)
+    best = pair if pair.get("TFLOP/s", 0) > tflops else {"ms": ms, "TFLOP/s": tflops}
+    return {"workload": f"C4: bf16 matmul {n}^3 -> fp32 as a collapse(2) upir.loop, tile loop static,1 over "
+                        "persistent teams: 74 teams x 512 units (CTA pairs, tcgen05.mma.cta_group::2, 256x256 tiles) "
+                        f"and {teams} teams x 256 units (1 CTA, 128x256 tiles); TMA SW128, TMEM accumulators",
+            "ms": best["ms"], "TFLOP/s": best["TFLOP/s"], "bound": "tensor", "cta_pair_bf16": pair,
+            "single_cta_bf16": {"ms": ms, "TFLOP/s": tflops, "frac": tflops / peak},
             "fp32_3xtf32": {"ms": ms32, "TFLOP/s": fp32_tflops, "tensor_TFLOP/s": 3 * fp32_tflops,
                             "peak_tf32": tf32_peak, "frac_of_tf32_over_3": fp32_tflops / (tf32_peak / 3),
                             "peak_source": peak_src + " bf16 burst x nominal tf32/bf16 ratio 1/2"},
-            "roofline": {"achieved": tflops, "peak": peak, "unit": "TFLOP/s", "frac": tflops / peak,
+            "roofline": {"achieved": best["TFLOP/s"], "peak": peak, "unit": "TFLOP/s", "frac": best["TFLOP/s"] / peak,
                          "peak_source": peak_src + " bf16 burst", "traffic": ncu_traffic("matmul")}}
 
 
