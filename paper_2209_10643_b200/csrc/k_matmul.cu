@@ -593,6 +593,231 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(TMEM_COLS));
 }
 
+// CTA-pair variant for fp32 inputs (3xTF32): a team = 2 CTAs x 384 units.
+// Each CTA's TMA loads its raw fp32 A rows / B columns on ITS OWN full
+// barrier; its 4 split warps write hi / lo copies and then arrive on the
+// LEADER's ready barrier (8 arrivals per stage); the leader issues
+// tcgen05.mma.cta_group::2.kind::tf32 (M = 256, N = 256, K = 8) three times
+// per k-step.  3 stages of 64 KB (hi + lo of A and B halves) per CTA.
+constexpr int PF_STAGES = 3;
+constexpr int PF_A = 128 * 32 * 4;            // 16 KB: this CTA's A rows (one copy)
+constexpr int PF_B = 32 * 128 * 4;            // 16 KB: this CTA's B columns (4 boxes of 32)
+constexpr int PF_COPY = PF_A + PF_B;
+constexpr int PF_STAGE = 2 * PF_COPY;
+constexpr int PF_SMEM = PF_STAGES * PF_STAGE + 1024 + 256;
+constexpr uint32_t PF_IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (0u << 15) | (1u << 16) |
+                              ((uint32_t)(BN >> 3) << 17) | ((uint32_t)(PBM >> 4) << 24);
+
+__device__ __forceinline__ void mma_pair_tf32(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc, uint32_t accum) {
+  asm volatile(
+      "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+      " tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "l"(adesc), "l"(bdesc), "r"(PF_IDESC), "r"(accum));
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
+    matmul_pair_f32_kernel(const __grid_constant__ MatmulArgs a, const __grid_constant__ CUtensorMap tma,
+                           const __grid_constant__ CUtensorMap tmb) {
+  extern __shared__ __align__(1024) char smem_raw[];
+  char *smem = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
+  uint64_t *full = reinterpret_cast<uint64_t *>(smem + PF_STAGES * PF_STAGE);
+  uint64_t *empty = full + PF_STAGES;
+  uint64_t *ready = empty + PF_STAGES;
+  uint64_t *tfull = ready + PF_STAGES;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(tempty + 2);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+
+  const int64_t ti0 = a.lb0 / PBM, tj0 = a.lb1 / BN;
+  const int64_t ntr = (a.ub0 + PBM - 1) / PBM - ti0, ntc = (a.ub1 + BN - 1) / BN - tj0;
+  const int64_t nt = ntr * ntc;
+  const int KB = (int)((a.K + 32 - 1) / 32);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tma);
+    tma_prefetch_desc(&tmb);
+    for (int st = 0; st < PF_STAGES; ++st) {
+      tma_mbar_init(full + st, 1);
+      tma_mbar_init(empty + st, 1);
+      tma_mbar_init(ready + st, 8);    // 4 split warps x 2 CTAs (leader's copy is used)
+    }
+    for (int st = 0; st < 2; ++st) {
+      tma_mbar_init(tfull + st, 1);
+      tma_mbar_init(tempty + st, 8);
+    }
+    tma_fence_init();
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(tma_smem(tmem_holder)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;\n");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  TileSeq seq;
+  seq.sched = a.sched;
+  seq.chunk = a.chunk;
+  seq.nt = nt;
+  seq.p = gridDim.x / 2;
+  seq.t = blockIdx.x / 2;
+  if (seq.sched == SK_STATIC_BLOCK) {
+    const int64_t q = nt / seq.p, r = nt % seq.p;
+    seq.cur = seq.t * q + (seq.t < r ? seq.t : r);
+    seq.end = seq.cur + q + (seq.t < r ? 1 : 0);
+    seq.k = 0;
+  } else {
+    seq.k = seq.t;
+    seq.cur = seq.k * seq.chunk;
+    seq.end = min(nt, seq.cur + seq.chunk);
+  }
+
+  if (warp == 0) {
+    if (lane == 0) {   // ---------------- TMA producer (both CTAs, own full barrier)
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t tile = seq.next(); tile >= 0; tile = seq.next()) {
+        int64_t ti, tj;
+        tile_coords(tile, ntr, ntc, ti, tj);
+        const int m0 = (int)((ti0 + ti) * PBM + 128 * rank), n0 = (int)((tj0 + tj) * BN + 128 * rank);
+        for (int kb = 0; kb < KB; ++kb) {
+          tma_mbar_wait(empty + stage, phase ^ 1);
+          char *sa = smem + stage * PF_STAGE;
+          char *sb = sa + PF_A;
+          tma_mbar_expect_tx(full + stage, PF_COPY);
+          tma_load_2d(sa, &tma, kb * 32, m0 - (int)a.row0, full + stage);
+#pragma unroll
+          for (int j = 0; j < 4; ++j) tma_load_2d(sb + j * 4096, &tmb, n0 + 32 * j, kb * 32, full + stage);
+          if (++stage == PF_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && leader) {   // ---------------- MMA issuer (leader)
+      int stage = 0;
+      uint32_t phase = 0;
+      int local = 0;
+      for (int64_t tile = seq.next(); tile >= 0; tile = seq.next(), ++local) {
+        const int acc = local & 1;
+        const uint32_t acc_phase = (uint32_t)((local >> 1) & 1);
+        tma_mbar_wait(tempty + acc, acc_phase ^ 1);
+        tc_fence_after();
+        const uint32_t tmem_d = tmem_base + (uint32_t)(acc * BN);
+        for (int kb = 0; kb < KB; ++kb) {
+          tma_mbar_wait(ready + stage, phase);
+          tc_fence_after();
+          const char *hi = smem + stage * PF_STAGE;
+          const char *lo = hi + PF_COPY;
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            const uint64_t ah = smem_desc(hi + k * 32, 16, 1024);
+            const uint64_t al = smem_desc(lo + k * 32, 16, 1024);
+            const uint64_t bh = smem_desc(hi + PF_A + k * 1024, 4096, 512, LT_SW128_BASE32B);
+            const uint64_t bl = smem_desc(lo + PF_A + k * 1024, 4096, 512, LT_SW128_BASE32B);
+            mma_pair_tf32(tmem_d, al, bh, (kb | k) != 0);   // lo_a * hi_b
+            mma_pair_tf32(tmem_d, ah, bl, 1);               // hi_a * lo_b
+            mma_pair_tf32(tmem_d, ah, bh, 1);               // hi_a * hi_b
+          }
+          commit_pair(empty + stage);
+          if (++stage == PF_STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        commit_pair(tfull + acc);
+      }
+    }
+  } else if (warp >= 4 && warp < 8) {   // ---------------- epilogue (both CTAs)
+    const int ew = warp & 3;
+    const uint32_t tempty_leader = map_to_cta(tma_smem(tempty), 0);
+    int local = 0;
+    for (int64_t tile = seq.next(); tile >= 0; tile = seq.next(), ++local) {
+      const int acc = local & 1;
+      const uint32_t acc_phase = (uint32_t)((local >> 1) & 1);
+      int64_t ti, tj;
+      tile_coords(tile, ntr, ntc, ti, tj);
+      const int64_t m0 = (ti0 + ti) * PBM + 128 * rank, n0 = (tj0 + tj) * BN;
+      tma_mbar_wait(tfull + acc, acc_phase);
+      tc_fence_after();
+      const int64_t row = m0 + 32 * ew + lane;
+      const bool row_ok = row >= a.lb0 && row < a.ub0;
+      float *crow = a.C + (row - a.row0) * a.ldc;
+#pragma unroll 1
+      for (int c = 0; c < BN; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(tmem_base + ((uint32_t)(32 * ew) << 16) + (uint32_t)(acc * BN + c), r);
+        const int64_t col0 = n0 + c;
+        if (!row_ok) continue;
+        if (col0 >= a.lb1 && col0 + 32 <= a.ub1) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+            asm volatile("st.global.v8.f32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"l"(crow + col0 + 8 * q),
+                         "r"(r[8 * q]), "r"(r[8 * q + 1]), "r"(r[8 * q + 2]), "r"(r[8 * q + 3]), "r"(r[8 * q + 4]),
+                         "r"(r[8 * q + 5]), "r"(r[8 * q + 6]), "r"(r[8 * q + 7])
+                         : "memory");
+        } else {
+#pragma unroll
+          for (int q = 0; q < 32; ++q)
+            if (col0 + q >= a.lb1 && col0 + q < a.ub1) crow[col0 + q] = __uint_as_float(r[q]);
+        }
+      }
+      if (a.trace && leader && ew == 0 && lane == 0) {
+        a.trace[tile] = (int32_t)(blockIdx.x / 2);
+        a.trace[nt + tile] = 0;
+        atomicAdd(a.trace + 2 * nt + tile, 1);
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) remote_arrive(tempty_leader + (uint32_t)(acc * 8));
+    }
+  } else if (warp >= 8) {   // ---------------- 3xTF32 split of this CTA's tiles
+    const int tid = threadIdx.x - 256;
+    const uint32_t ready_leader = map_to_cta(tma_smem(ready), 0);
+    int stage = 0;
+    uint32_t phase = 0;
+    for (int64_t tile = seq.next(); tile >= 0; tile = seq.next()) {
+      for (int kb = 0; kb < KB; ++kb) {
+        tma_mbar_wait(full + stage, phase);
+        float4 *hi = reinterpret_cast<float4 *>(smem + stage * PF_STAGE);
+        float4 *lo = reinterpret_cast<float4 *>(smem + stage * PF_STAGE + PF_COPY);
+        for (int v = tid; v < PF_COPY / 16; v += 128) {
+          const float4 x = hi[v];
+          float4 h, l;
+          h.x = to_tf32(x.x);
+          h.y = to_tf32(x.y);
+          h.z = to_tf32(x.z);
+          h.w = to_tf32(x.w);
+          l.x = __fsub_rn(x.x, h.x);
+          l.y = __fsub_rn(x.y, h.y);
+          l.z = __fsub_rn(x.z, h.z);
+          l.w = __fsub_rn(x.w, h.w);
+          hi[v] = h;
+          lo[v] = l;
+        }
+        tma_fence_proxy();
+        __syncwarp();
+        if (lane == 0) remote_arrive(ready_leader + (uint32_t)(stage * 8));
+        if (++stage == PF_STAGES) {
+          stage = 0;
+          phase ^= 1;
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  if (warp == 2)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(TMEM_COLS));
+}
+
 }  // namespace
 
 int matmul_tile_m() { return BM; }
@@ -600,9 +825,12 @@ int matmul_tile_n() { return BN; }
 int matmul_required_units(int dtype) { return dtype == UPIR_F32 ? Cfg<UPIR_F32>::THREADS : Cfg<UPIR_BF16>::THREADS; }
 // bf16 teams may also be CTA pairs (512 units, 256-row tiles)
 bool matmul_units_ok(int dtype, int units) {
-  return units == matmul_required_units(dtype) || (dtype == UPIR_BF16 && units == 512);
+  return units == matmul_required_units(dtype) || (dtype == UPIR_BF16 && units == 512) ||
+         (dtype == UPIR_F32 && units == 768);
 }
-int matmul_tile_m_for(int dtype, int units) { return (dtype == UPIR_BF16 && units == 512) ? PBM : BM; }
+int matmul_tile_m_for(int dtype, int units) {
+  return ((dtype == UPIR_BF16 && units == 512) || (dtype == UPIR_F32 && units == 768)) ? PBM : BM;
+}
 
 bool matmul_encode_tmaps(void *tma, void *tmb, const void *A, const void *B, int dtype, int64_t M, int64_t N,
                          int64_t K, int64_t lda, int64_t ldb) {
@@ -632,6 +860,13 @@ cudaError_t launch_matmul(const MatmulArgs &a, int dtype, int teams, int units, 
     if (e != cudaSuccess) return e;
     matmul_pair_kernel<<<2 * teams, 256, P_SMEM, s>>>(a, *reinterpret_cast<const CUtensorMap *>(a.tmap_a),
                                                      *reinterpret_cast<const CUtensorMap *>(a.tmap_b));
+    return cudaGetLastError();
+  }
+  if (dtype == UPIR_F32 && units == 768) {
+    cudaError_t e = cudaFuncSetAttribute(matmul_pair_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PF_SMEM);
+    if (e != cudaSuccess) return e;
+    matmul_pair_f32_kernel<<<2 * teams, 384, PF_SMEM, s>>>(a, *reinterpret_cast<const CUtensorMap *>(a.tmap_a),
+                                                          *reinterpret_cast<const CUtensorMap *>(a.tmap_b));
     return cudaGetLastError();
   }
   if (units != matmul_required_units(dtype)) return cudaErrorInvalidValue;

@@ -38,7 +38,7 @@ def matmul_gpu(ctx, A, B, teams=148, policy=U.SCHED_STATIC, chunk=1, space=None,
     else:
         a, b = np.ascontiguousarray(A, np.float32), np.ascontiguousarray(B, np.float32)
     units = units or (256 if dtype == U.BF16 else 384)
-    tm_rows = 256 if units == 512 else 128
+    tm_rows = 256 if units in (512, 768) else 128
     C = np.zeros((M, N), np.float32) if C0 is None else C0.copy()
     ma = U.upir_data_map(ctx, a, U.MAP_TO)
     mb = U.upir_data_map(ctx, b, U.MAP_TO)
@@ -281,3 +281,23 @@ def test_matmul_pair_subspace(ctx):
     mask = np.ones((M, N), bool)
     mask[sub] = False
     assert (C[mask] == -7.0).all()
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 256, 32), (512, 768, 256), (300, 520, 72)])
+def test_matmul_pair_f32_parity(ctx, M, N, K):
+    A = synth.f32_sym(3, 0, M * K).reshape(M, K)
+    B = synth.f32_sym(4, 0, K * N).reshape(K, N)
+    C, _ = matmul_gpu(ctx, A, B, teams=74, units=768, dtype=U.F32)
+    assert scaled_err(C, A, B, oracle.matmul(A, B)) <= 1e-5
+
+
+def test_matmul_pair_f32_exact_and_trace(ctx):
+    rng = np.random.default_rng(12)
+    M, N, K = 512, 512, 96
+    A = rng.integers(-2, 3, (M, K)).astype(np.float32)
+    B = rng.integers(-2, 3, (K, N)).astype(np.float32)
+    C, tr = matmul_gpu(ctx, A, B, teams=3, units=768, chunk=1, trace=True, dtype=U.F32)
+    assert (C == oracle.matmul(A, B)).all()
+    nt = len(tr) // 3
+    assert (tr[2 * nt:] == 1).all()
+    assert (tr[:nt] == oracle.tile_owner(M, N, 256, 256, oracle.STATIC, 1, 3)).all()
