@@ -1,6 +1,7 @@
 """Summarise ncu reports into profiles/ (run here, on the CPU box).
 
     python tools/ncu_summary.py <round-tag> gpurun_out/prof_*.ncu-rep
+    (env UPIR_PROFILES_OUT=<dir> writes there instead of profiles/)
 
 Writes profiles/<tag>_<name>.txt (key metrics per profiled kernel launch)
 and updates profiles/traffic.json (DRAM bytes per launch, read by bench.py).
@@ -13,6 +14,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+OUT = os.environ.get("UPIR_PROFILES_OUT", os.path.join(ROOT, "profiles"))
 KEYS = [
     "gpu__time_duration.sum",
     "dram__bytes_read.sum",
@@ -64,8 +66,13 @@ def to_bytes(v, u):
 
 def main():
     tag = sys.argv[1]
-    traffic_path = os.path.join(ROOT, "profiles", "traffic.json")
-    traffic = json.load(open(traffic_path)) if os.path.exists(traffic_path) else {}
+    os.makedirs(OUT, exist_ok=True)
+    traffic_path = os.path.join(OUT, "traffic.json")
+    if not os.path.exists(traffic_path) and os.path.exists(os.path.join(ROOT, "profiles", "traffic.json")):
+        traffic_path_in = os.path.join(ROOT, "profiles", "traffic.json")
+    else:
+        traffic_path_in = traffic_path
+    traffic = json.load(open(traffic_path_in)) if os.path.exists(traffic_path_in) else {}
     for rep in sys.argv[2:]:
         name = os.path.basename(rep).replace(".ncu-rep", "").replace("prof_", "")
         launches = raw(rep)
@@ -90,12 +97,20 @@ def main():
                     key = "axpy"
                 elif "jacobi5" in kname:
                     key = "jacobi"
+                elif "matmul_pair_kernel" in kname:
+                    key = "matmul_pair"
+                elif "matmul_kernel<2>" in kname or "matmul_kernel<(int)2>" in kname:
+                    key = "matmul_f32"
                 elif "matmul" in kname:
                     key = "matmul"
+                elif "matvec" in kname:
+                    key = "matvec"
+                elif "stencil" in kname:
+                    key = "stencil7"
                 if key and key not in traffic.get("_seen_" + tag, []):
                     traffic[key] = rb + wb
                     traffic.setdefault("_seen_" + tag, []).append(key)
-        out = os.path.join(ROOT, "profiles", f"{tag}_{name}.txt")
+        out = os.path.join(OUT, f"{tag}_{name}.txt")
         with open(out, "w") as f:
             f.write("\n".join(lines) + "\n")
         print("wrote", out)
