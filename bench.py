@@ -377,7 +377,9 @@ def bench_reduce(args, U, ctx, stream, barrier, rank, world, peaks, peak_src):
     hx_f = torch.empty(e2e_n, dtype=torch.float32, pin_memory=True)
     hx_i.copy_(xi_t[:e2e_n])
     hx_f.copy_(xf_t[:e2e_n])
-    hres = np.zeros(8, np.float64)
+    # result scalars: a pinned host buffer (no per-step page registration)
+    hres_t = torch.zeros(8, dtype=torch.float64, pin_memory=True)
+    hres = np.ctypeslib.as_array(ctypes.cast(hres_t.data_ptr(), ctypes.POINTER(ctypes.c_double)), shape=(8,))
     U.upir_data_unmap(ctx, mi)
     U.upir_data_unmap(ctx, mf)
     del xi_t, xf_t
@@ -419,6 +421,15 @@ def bench_reduce(args, U, ctx, stream, barrier, rank, world, peaks, peak_src):
             e2e_step()
         barrier()
         e2e_ms = (time.perf_counter() - te0) * 1e3 / args.e2e_steps
+        if os.environ.get("UPIR_E2E_PHASES"):
+            tp = time.perf_counter()
+            m1 = U.upir_data_map(ctx, ai, U.MAP_TO)
+            U.upir_sync(ctx)
+            t_map = time.perf_counter() - tp
+            U.upir_data_unmap(ctx, m1)
+            U.upir_sync(ctx)
+            print(f"e2e phase: map(to) of {ai.nbytes / 1e9:.2f} GB in {t_map * 1e3:.1f} ms "
+                  f"= {ai.nbytes / t_map / 1e9:.1f} GB/s", file=sys.stderr)
     # the e2e path is timed by the host clock around synchronous steps (each
     # step ends in upir_sync), max over ranks below
 

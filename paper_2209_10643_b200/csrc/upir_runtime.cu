@@ -336,6 +336,9 @@ static void map_range(upir_map m, bool owned_only, size_t &host_off, size_t &dev
 // released at the first upir_sync (or finalize) after their last map is gone
 // -- the contract keeps host buffers valid until that sync.
 static void pin_host(upir_ctx c, void *host, size_t bytes) {
+  // small buffers are copied from pageable memory (the driver stages them);
+  // registering / unregistering a page per map costs more than the copy
+  if (bytes < ((size_t)1 << 20)) return;
   for (auto &r : c->registered)
     if ((char *)host >= (char *)r.ptr && (char *)host + bytes <= (char *)r.ptr + r.bytes) {
       r.users++;
