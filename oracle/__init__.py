@@ -65,6 +65,7 @@ def lib():
             "orc_tiled_owner": (i64, [i64, i64, i64, i64, i64, i64, i32, i64, i64, i64, i64, vp, vp]),
             "orc_matvec": (i32, [i64, i64, i64, i64, i64, vp, vp, vp, vp]),
             "orc_stencil2d": (i32, [i64, i64, i64, i64, vp, vp, vp]),
+            "orc_reduce_stream": (i32, [i32, i32, ctypes.c_uint64, i64, i64, vp, vp]),
         }
         for name, (res, args) in sig.items():
             f = getattr(_lib, name)
@@ -174,6 +175,16 @@ def reduce_f32(op, x, init=None, lb=0, ub=None, step=1, policy=STATIC, chunk=0, 
                               _p(parts) if want_partials else None, _p(res))
     _check(rc, "reduce_f32")
     return (float(res[0]), parts) if want_partials else float(res[0])
+
+
+def reduce_stream(op, dist, stream, start, n):
+    """Sequential reduction of elements [start, start+n) of the synthetic
+    stream, generated inside the oracle (its own copy of the recipe):
+    dist 2 = int64 (exact), dist 0 = fp32 U[0,1) (fp64 accumulation)."""
+    rf = np.zeros(1, np.float64)
+    ri = np.zeros(1, np.int64)
+    _check(lib().orc_reduce_stream(op, dist, stream, start, n, _p(rf), _p(ri)), "reduce_stream")
+    return int(ri[0]) if dist == 2 else float(rf[0])
 
 
 def world_reduce(op, rank_results):

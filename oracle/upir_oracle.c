@@ -499,3 +499,42 @@ int orc_stencil2d(int64_t ny, int64_t nx, int64_t R, int64_t S, const float *w, 
     free(a); free(b);
     return 0;
 }
+
+/* ---- full-size reductions over the synthetic input stream -----------------
+ * The oracle's own copy of the counter-based input recipe (DESIGN.md "Input
+ * recipe"; the task allows each side its own implementation of the same
+ * generator), fused with a plain sequential reduction so that 2^30 .. 2^34
+ * element references need no host array.  dist 2 = i64 U[-2^28, 2^28),
+ * dist 0 = f32 U[0,1).  Elements [start, start + n) of `stream`; result =
+ * init (+) x_start (+) ... in index order (exact int64 / fp64). */
+static uint64_t orc_mix(uint64_t z)
+{
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    return z ^ (z >> 31);
+}
+
+int orc_reduce_stream(int op, int dist, uint64_t stream, int64_t start, int64_t n, double *res_f,
+                      int64_t *res_i)
+{
+    uint64_t seed = (2209ull << 16) | stream;
+    if (dist == 2) {
+        uint64_t acc = i64_identity(op);
+        for (int64_t e = 0; e < n; ++e) {
+            uint64_t x = orc_mix(seed + ((uint64_t)(start + e) + 1ull) * 0x9E3779B97F4A7C15ull);
+            acc = i64_combine(op, acc, (int64_t)(x >> 35) - ((int64_t)1 << 28));
+        }
+        *res_i = (int64_t)acc;
+        return 0;
+    }
+    if (dist == 0) {
+        double acc = f_identity(op);
+        for (int64_t e = 0; e < n; ++e) {
+            uint64_t x = orc_mix(seed + ((uint64_t)(start + e) + 1ull) * 0x9E3779B97F4A7C15ull);
+            acc = f_combine(op, acc, (double)(x >> 40) * 0x1.0p-24);
+        }
+        *res_f = acc;
+        return 0;
+    }
+    return -1;
+}

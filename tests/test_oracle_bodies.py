@@ -298,3 +298,14 @@ def test_stencil_delta_and_shift_and_fixed_points():
     j = np.arange(40)[None, :].astype(np.float64)
     lin = (2 * i - 3 * j + 5).astype(np.float32)              # linear field, symmetric weights summing to 1
     assert (oracle.stencil2d(lin, _w7(), 4) == lin).all()
+
+
+def test_reduce_stream_matches_array_oracle():
+    # the oracle's in-place generator + reduction == generator module + array oracle
+    for start, n in ((0, 5000), (123_456, 777)):
+        xi = synth.i64_sym(6, start, n)
+        xf = synth.f32_unit(7, start, n)
+        assert oracle.reduce_stream(oracle.SUM, 2, 6, start, n) == oracle.reduce_i64(oracle.SUM, xi)
+        assert oracle.reduce_stream(oracle.MAX, 2, 6, start, n) == int(xi.max())
+        assert oracle.reduce_stream(oracle.SUM, 0, 7, start, n) == math.fsum(xf.astype(np.float64))
+        assert oracle.reduce_stream(oracle.MAX, 0, 7, start, n) == float(xf.max())
