@@ -67,6 +67,9 @@ typedef struct upir_graph_s *upir_graph;
  * 128-byte ncclUniqueId produced on rank 0 by upir_comm_unique_id and
  * broadcast by the caller (e.g. torch.distributed).  compute_stream /
  * copy_stream: cudaStream_t values to run on, 0 = library-created streams.
+ * nccl_id NULL with nranks > 1: a communicator-less world -- ranks exchange
+ * data only through peer windows (upir_peer_*; fused world reductions, fused
+ * halos, WORLD_BARRIER); NCCL-backed calls return UPIR_E_UNSUPPORTED.
  */
 typedef struct {
     int32_t rank, nranks;
@@ -155,6 +158,36 @@ upir_status upir_dist_owned_rows(int64_t n_rows, int32_t rank, int32_t nranks,
 upir_status upir_halo_plan(int64_t n_rows, int32_t halo_rows, int32_t rank, int32_t nranks,
                            int64_t out[8]);
 
+/* ---- peer windows: NVLink peer memory between ranks (CUDA IPC) ----------
+ * One process per GPU; the NVSwitch lets every GPU load/store every other
+ * GPU's memory.  upir_peer_export writes a UPIR_PEER_REC_BYTES record (a
+ * CUDA-IPC handle plus layout facts) for
+ *   map == NULL : the context's peer window (signal counters and reduction
+ *                 slots written by the other ranks), or
+ *   map != NULL : a BLOCK-distributed map's local buffer (its halo rows are
+ *                 the neighbours' peer-store targets).  A library-allocated
+ *                 buffer is moved to an exportable block on first export
+ *                 (device pointers taken earlier go stale); an adopted
+ *                 buffer must be a cudaMalloc allocation (e.g. torch).
+ * The caller moves records between ranks (e.g. all_gather_object) and calls
+ * upir_peer_import(ctx, map, r, rec) for rank r's record: windows of every
+ * rank (enables UPIR_WORLD_REDUCE in-kernel and the peer WORLD_BARRIER), map
+ * buffers of ranks r +- 1 only (enables the fused halo below).
+ *
+ * Fused halo (PAPER.md:889 send/recv between rank-adjacent slabs, fused with
+ * the sweep that produces the rows): a CLUSTER JACOBI5 loop whose out map
+ * has imported neighbour buffers stores its first / last owned output row
+ * also into the neighbours' halo rows of THEIR out buffers, and its tiles
+ * that touch halo / boundary rows wait in the kernel until both neighbours
+ * finished their previous sweep.  upir_sync(HALO) on a map written by such a
+ * sweep returns at once (the exchange already happened).  Peer-mode sweeps
+ * are collective: every rank executes the same sequence.  Unmapping a
+ * peer-attached map first waits for the neighbours' last sweep.
+ * Errors: UPIR_E_INVALID (bad record / rank / layout), UPIR_E_CUDA (IPC). */
+#define UPIR_PEER_REC_BYTES 256
+upir_status upir_peer_export(upir_ctx ctx, upir_map map, void *rec);
+upir_status upir_peer_import(upir_ctx ctx, upir_map map, int32_t peer_rank, const void *rec);
+
 /* ---- upir.spmd (Fig. 1) -------------------------------------------------
  * teams x units = CUDA grid x block (Figs. 11-12): team = CTA,
  * unit = thread, flat unit id g = team * num_units + unit.
@@ -205,6 +238,17 @@ typedef enum {
 typedef enum { UPIR_DIST_TEAMS = 1, UPIR_DIST_UNITS = 2, UPIR_DIST_TEAMS_UNITS = 3 } upir_distribute;
 
 #define UPIR_NOWAIT 1u  /* no implicit end barrier: the host does not wait */
+/* UPIR_WORLD_REDUCE: the loop's reductions are combined over all ranks as part
+ * of the loop (Fig. 7 'allreduce' with ranks as units fused into the loop's
+ * end barrier): every rank receives
+ *   init (+) P_0 (+) P_1 (+) ... (+) P_{N-1}   (ascending rank order)
+ * where P_r is rank r's combination of its units' partials (fp64 for F32,
+ * rounded once; the original value counted once).  With every rank's peer
+ * window imported the last team of each rank exchanges the partials through
+ * NVLink peer memory inside the loop kernel; otherwise (communicator only)
+ * the loop is followed by upir_reduce(WORLD).  Collective: every rank must
+ * execute the loop.  nranks == 1: no effect. */
+#define UPIR_WORLD_REDUCE 2u
 
 typedef struct {
     int32_t collapse;        /* 1..2 */

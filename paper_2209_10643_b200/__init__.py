@@ -252,3 +252,31 @@ def upir_graph_destroy(g):
 
 def upir_synth_fill(ctx, m, dist_kind, stream, index_base=0, n_rows=0, n_cols=0):
     check(lib().upir_synth_fill(ctx, m, dist_kind, stream, index_base, n_rows, n_cols))
+
+
+def upir_peer_export(ctx, m=None):
+    """Peer record (bytes) of the context window (m None) or of map m."""
+    buf = ctypes.create_string_buffer(_abi.PEER_REC_BYTES)
+    check(lib().upir_peer_export(ctx, m, buf))
+    return bytes(buf.raw)
+
+
+def upir_peer_import(ctx, m, peer_rank, rec):
+    buf = ctypes.create_string_buffer(bytes(rec), _abi.PEER_REC_BYTES)
+    check(lib().upir_peer_import(ctx, m, peer_rank, buf))
+
+
+def upir_peer_share(ctx, maps=(), group=None):
+    """Collective over torch.distributed: export this rank's window and maps,
+    all-gather the records, import every rank's window and the halo
+    neighbours' (rank +- 1) map buffers.  Host plumbing only."""
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    recs = [upir_peer_export(ctx, None)] + [upir_peer_export(ctx, m) for m in maps]
+    allr = [None] * world
+    dist.all_gather_object(allr, (rank, recs), group=group)
+    for q, rr in allr:
+        upir_peer_import(ctx, None, q, rr[0])
+        if abs(q - rank) == 1:
+            for k, m in enumerate(maps):
+                upir_peer_import(ctx, m, q, rr[k + 1])

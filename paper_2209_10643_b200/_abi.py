@@ -20,6 +20,8 @@ TARGET_GPU, TARGET_CLUSTER = 1, 2
 SCHED_STATIC, SCHED_DYNAMIC, SCHED_GUIDED, SCHED_RUNTIME, SCHED_AUTO = 0, 1, 2, 3, 4
 DIST_TEAMS, DIST_UNITS, DIST_TEAMS_UNITS = 1, 2, 3
 NOWAIT = 1
+WORLD_REDUCE = 2
+PEER_REC_BYTES = 256
 BODY_AXPY, BODY_REDUCE, BODY_JACOBI5, BODY_MATMUL, BODY_MATVEC, BODY_STENCIL2D = 0, 1, 2, 3, 4, 5
 OP_SUM, OP_MAX, OP_MIN = 0, 1, 2
 SCOPE_DEVICE, SCOPE_WORLD = 0, 1
@@ -90,6 +92,8 @@ _SIGS = {
     "upir_graph_launch": (i32, [vp, vp]),
     "upir_graph_destroy": (i32, [vp]),
     "upir_synth_fill": (i32, [vp, vp, i32, u64, i64, i64, i64]),
+    "upir_peer_export": (i32, [vp, vp, vp]),
+    "upir_peer_import": (i32, [vp, vp, i32, vp]),
 }
 
 DECLARED = tuple(_SIGS)

@@ -14,6 +14,17 @@
 // once per sweep (neighbour tiles' halos hit L2): 8 B per lattice update.
 // fp32 arithmetic with explicit __fadd_rn/__fmul_rn: no FMA contraction, so
 // the result is independent of decomposition (1 vs N GPUs bit-identical).
+//
+// Peer mode (a.win != null): the halo exchange with ranks r+-1
+// is fused into the sweep.  A unit that computes my first / last owned row
+// also stores it into the neighbour's halo row of ITS output buffer (peer
+// stores over NVLink), and the tiles that read my halo rows or write those
+// boundary rows wait -- before their TMA load is issued -- until both
+// neighbours have delivered every sweep before this one (their last team
+// bumps my counter with a .sys release after the whole sweep).  Interior
+// tiles never wait: the transfer and the neighbour skew overlap the bulk of
+// the sweep.
+#include "dev_peer.cuh"
 #include "dev_tma.cuh"
 #include "upir_internal.h"
 
@@ -107,7 +118,24 @@ __global__ void __launch_bounds__(1024) jacobi5_kernel(const __grid_constant__ J
     tma_load_2d(b + L::CEN + L::HAL, &tmh, c0 + BN, r0, bars + buf);
   };
 
+  // peer mode: sweeps this rank completed = sweeps each neighbour must have
+  // delivered before a boundary tile may read / write halo rows
+  unsigned long long gen = 0;
+  auto peer_wait = [&](int64_t tile) {
+    const int64_t i0 = (a.ti0 + tile / a.ntc) * BM;
+    bool waited = false;
+    if (a.win_up && a.halo_up_row >= i0 - 1 && a.halo_up_row <= i0 + BM) {
+      wait_geq_sys(a.win + WIN_HALO_FROM_UP, gen);
+      waited = true;
+    }
+    if (a.win_dn && a.halo_dn_row >= i0 - 1 && a.halo_dn_row <= i0 + BM) {
+      wait_geq_sys(a.win + WIN_HALO_FROM_DN, gen);
+      waited = true;
+    }
+    if (waited) fence_proxy_async_global();
+  };
   if (threadIdx.x == 0) {
+    if (a.win) gen = *reinterpret_cast<volatile unsigned long long *>(a.win + WIN_HALO_GEN);
     tma_prefetch_desc(&tmc);
     tma_prefetch_desc(&tmh);
     tma_mbar_init(bars + 0, 1);
@@ -115,7 +143,10 @@ __global__ void __launch_bounds__(1024) jacobi5_kernel(const __grid_constant__ J
     tma_fence_init();
     const int64_t t0 = next_tile(it, a, nt);
     tile_s[0] = t0;
-    if (t0 >= 0) issue(t0, 0);
+    if (t0 >= 0) {
+      if (a.win) peer_wait(t0);
+      issue(t0, 0);
+    }
   }
   __syncthreads();
 
@@ -129,7 +160,10 @@ __global__ void __launch_bounds__(1024) jacobi5_kernel(const __grid_constant__ J
     if (threadIdx.x == 0) {
       const int64_t nx = next_tile(it, a, nt);
       tile_s[buf ^ 1] = nx;
-      if (nx >= 0) issue(nx, buf ^ 1);
+      if (nx >= 0) {
+        if (a.win) peer_wait(nx);
+        issue(nx, buf ^ 1);
+      }
     }
     tma_mbar_wait(bars + buf, (unsigned)((iter >> 1) & 1));
     const int64_t ti = a.ti0 + tile / a.ntc, tj = a.tj0 + tile % a.ntc;
@@ -160,13 +194,24 @@ __global__ void __launch_bounds__(1024) jacobi5_kernel(const __grid_constant__ J
         o.z = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(up.z, dn.z), __fadd_rn(md.y, md.w)));
         o.w = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(up.w, dn.w), __fadd_rn(md.z, e3)));
         float *dst = a.out + (i - a.row0) * a.ld + j;
+        // peer mode: my boundary rows also land in the neighbour's halo row
+        float *pdst = (a.win && i == a.send_up_row && a.peer_up) ? a.peer_up + (i - a.peer_up_row0) * a.ld + j
+                                                                  : nullptr;
+        float *pdst2 = (a.win && i == a.send_dn_row && a.peer_dn) ? a.peer_dn + (i - a.peer_dn_row0) * a.ld + j
+                                                                   : nullptr;
         if (j >= a.lb1 && j + 4 <= a.ub1) {
           __stcs(reinterpret_cast<float4 *>(dst), o);
+          if (pdst) *reinterpret_cast<float4 *>(pdst) = o;
+          if (pdst2) *reinterpret_cast<float4 *>(pdst2) = o;
         } else {
           const float ov[4] = {o.x, o.y, o.z, o.w};
 #pragma unroll
           for (int q = 0; q < 4; ++q)
-            if (j + q >= a.lb1 && j + q < a.ub1) dst[q] = ov[q];
+            if (j + q >= a.lb1 && j + q < a.ub1) {
+              dst[q] = ov[q];
+              if (pdst) pdst[q] = ov[q];
+              if (pdst2) pdst2[q] = ov[q];
+            }
         }
         if constexpr (TRACE) {
 #pragma unroll
@@ -189,6 +234,10 @@ __global__ void __launch_bounds__(1024) jacobi5_kernel(const __grid_constant__ J
           const float v = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(at(r, c), at(r + 2, c)),
                                                      __fadd_rn(at(r + 1, c - 1), at(r + 1, c + 1))));
           a.out[(i - a.row0) * a.ld + j] = v;
+          if (a.win) {
+            if (i == a.send_up_row && a.peer_up) a.peer_up[(i - a.peer_up_row0) * a.ld + j] = v;
+            if (i == a.send_dn_row && a.peer_dn) a.peer_dn[(i - a.peer_dn_row0) * a.ld + j] = v;
+          }
           if constexpr (TRACE) {
             const int64_t idx = tile * POS + pos;
             a.trace[idx] = blockIdx.x;
@@ -199,6 +248,23 @@ __global__ void __launch_bounds__(1024) jacobi5_kernel(const __grid_constant__ J
       }
     }
     __syncthreads();   // buffer `buf` free; tile_s[buf ^ 1] visible
+  }
+  // peer mode: after the whole sweep (every unit's peer stores fenced), the
+  // last team counts the sweep and delivers it to both neighbours
+  if (a.win) {
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      const unsigned long long t = atomicAdd(a.win + WIN_HALO_DONE, 1ull);
+      if (t == (unsigned long long)gridDim.x - 1) {
+        a.win[WIN_HALO_DONE] = 0ull;
+        __threadfence_system();
+        const unsigned long long g = *reinterpret_cast<volatile unsigned long long *>(a.win + WIN_HALO_GEN);
+        *reinterpret_cast<volatile unsigned long long *>(a.win + WIN_HALO_GEN) = g + 1ull;
+        if (a.win_up) red_release_sys_add(a.win_up + WIN_HALO_FROM_DN, 1ull);
+        if (a.win_dn) red_release_sys_add(a.win_dn + WIN_HALO_FROM_UP, 1ull);
+      }
+    }
   }
   // dynamic: the last team resets the tile counter for the next launch
   if (a.sched == SK_DYNAMIC) {

@@ -2,6 +2,7 @@
 // upir_reduce(WORLD), and the device-side synthetic input generator.
 #include <math_constants.h>
 
+#include "dev_peer.cuh"
 #include "upir_internal.h"
 
 namespace upir {
@@ -71,6 +72,31 @@ cudaError_t launch_rank_combine(int op, int dtype, const void *gathered, int64_t
   if (blocks > 1184) blocks = 1184;
   if (blocks < 1) blocks = 1;
   rank_combine_kernel<<<(int)blocks, threads, 0, s>>>(op, dtype, gathered, count, nranks, out);
+  return cudaGetLastError();
+}
+
+// ---- peer mode: drain the neighbours' deliveries ---------------------------
+__global__ void peer_drain_kernel(unsigned long long *win, int has_up, int has_dn) {
+  const unsigned long long g = *reinterpret_cast<volatile unsigned long long *>(win + WIN_HALO_GEN);
+  if (has_up) wait_geq_sys(win + WIN_HALO_FROM_UP, g);
+  if (has_dn) wait_geq_sys(win + WIN_HALO_FROM_DN, g);
+}
+
+cudaError_t launch_peer_drain(unsigned long long *win, int has_up, int has_dn, cudaStream_t s) {
+  peer_drain_kernel<<<1, 1, 0, s>>>(win, has_up, has_dn);
+  return cudaGetLastError();
+}
+
+__global__ void peer_barrier_kernel(unsigned long long *win, int nranks) {
+  const unsigned long long e = *reinterpret_cast<volatile unsigned long long *>(win + WIN_BAR_GEN);
+  for (int q = 0; q < nranks; ++q)
+    red_release_sys_add(reinterpret_cast<unsigned long long *>(win[WIN_PEERS + q]) + WIN_BAR_CNT, 1ull);
+  wait_geq_sys(win + WIN_BAR_CNT, (e + 1ull) * (unsigned long long)nranks);
+  *reinterpret_cast<volatile unsigned long long *>(win + WIN_BAR_GEN) = e + 1ull;
+}
+
+cudaError_t launch_peer_barrier(unsigned long long *win, int nranks, cudaStream_t s) {
+  peer_barrier_kernel<<<1, 1, 0, s>>>(win, nranks);
   return cudaGetLastError();
 }
 

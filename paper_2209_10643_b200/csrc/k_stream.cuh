@@ -26,6 +26,7 @@
 
 #include <type_traits>
 
+#include "dev_peer.cuh"
 #include "sched.cuh"
 
 namespace upir {
@@ -652,7 +653,35 @@ __device__ void reduce_epilogue(const StreamArgs &a, Acc<BODY, NRED> &acc, bool 
       v[r] = x;
     }
     block_tree(v);
-    if (threadIdx.x == 0) {
+    if (threadIdx.x == 0 && a.wwin) {
+      // upir.sync allreduce fused into the loop's end barrier: publish this
+      // rank's partials into every rank's window (slot [parity][rank][r]),
+      // signal, wait for all ranks, combine init (+) P_0 (+) ... in ascending
+      // rank order.  Parity double-buffering: a rank can only be one world
+      // reduction ahead of any other (it waits for all of them each time).
+      unsigned long long *win = a.wwin;
+      const unsigned long long e = *reinterpret_cast<volatile unsigned long long *>(win + WIN_WR_GEN);
+      const int par = (int)(e & 1ull);
+      for (int q = 0; q < a.wranks; ++q) {
+        unsigned long long *pw = reinterpret_cast<unsigned long long *>(win[WIN_PEERS + q]);
+#pragma unroll
+        for (int r = 0; r < NRED; ++r)
+          st_relaxed_sys(pw + WIN_WR_SLOTS + (par * WIN_MAX_RANKS + a.wrank) * 2 + r, to_bits(v[r]));
+      }
+      for (int q = 0; q < a.wranks; ++q)
+        red_release_sys_add(reinterpret_cast<unsigned long long *>(win[WIN_PEERS + q]) + WIN_WR_CNT, 1ull);
+      wait_geq_sys(win + WIN_WR_CNT, (e + 1ull) * (unsigned long long)a.wranks);
+#pragma unroll
+      for (int r = 0; r < NRED; ++r) {
+        const RedSpec &rs = a.red[r];
+        W x = from_bits(rs.init_bits);
+        for (int q = 0; q < a.wranks; ++q)
+          x = comb(rs.op, x, from_bits(ld_relaxed_sys(win + WIN_WR_SLOTS + (par * WIN_MAX_RANKS + q) * 2 + r)));
+        if constexpr (BODY == SB_RED_I64) *reinterpret_cast<long long *>(rs.result) = x;
+        else *reinterpret_cast<float *>(rs.result) = (float)x;
+      }
+      *reinterpret_cast<volatile unsigned long long *>(win + WIN_WR_GEN) = e + 1ull;
+    } else if (threadIdx.x == 0) {
 #pragma unroll
       for (int r = 0; r < NRED; ++r) {
         const RedSpec &rs = a.red[r];

@@ -17,6 +17,26 @@ enum PathKind : int32_t {
   PATH_STAGED = 1    // warp-cooperative cp.async staging of 128/64-B unit segments
 };
 
+// ---- peer window (one per context; exported to the other ranks by CUDA IPC) --
+// 64-bit words.  Remote ranks write the counters / slots of THIS window over
+// NVLink; the peer table holds this rank's mapped pointers to every rank's
+// window (entry `rank` = the local window).
+enum WinWord : int32_t {
+  WIN_HALO_FROM_UP = 0,   // sweeps delivered by rank - 1 (monotonic)
+  WIN_HALO_FROM_DN = 1,   // sweeps delivered by rank + 1
+  WIN_HALO_GEN = 2,       // peer-mode sweeps this rank completed
+  WIN_HALO_DONE = 3,      // last-team ticket of a peer-mode sweep
+  WIN_WR_CNT = 8,         // world-reduce arrivals (monotonic, N per reduction)
+  WIN_WR_GEN = 9,         // world reductions this rank completed
+  WIN_BAR_CNT = 10,       // peer-barrier arrivals (monotonic, N per barrier)
+  WIN_BAR_GEN = 11,       // peer barriers this rank completed
+  WIN_WR_SLOTS = 16,      // [2 parity][WIN_MAX_RANKS][2 reductions] partials
+  WIN_PEERS = 512,        // [WIN_MAX_RANKS] mapped window pointers
+  WIN_WORDS = 576
+};
+constexpr int WIN_MAX_RANKS = 64;
+constexpr size_t WIN_BYTES = 8192;
+
 // Streaming bodies.
 enum StreamBody : int32_t { SB_RED_I64 = 0, SB_RED_F32 = 1, SB_AXPY = 2 };
 
@@ -50,6 +70,10 @@ struct StreamArgs {
   RedSpec red[2];
   unsigned long long *slots;   // [gridDim.x][2] team partials (8-byte words)
   unsigned int *done;          // last-team ticket (self-resetting)
+  // world reduction fused into the epilogue (UPIR_WORLD_REDUCE): local peer
+  // window or null; the last team combines init (+) P_0 (+) ... (+) P_{N-1}
+  unsigned long long *wwin;
+  int32_t wrank, wranks;
   // trace: [team[T], unit[T], hits[T]] int32, or null
   int32_t *trace;
 };
@@ -65,6 +89,11 @@ size_t staged_smem_bytes(int body, int units, int segv, int nst);
 // the ordered combine of gathered per-rank partials (upir_reduce WORLD).
 cudaError_t launch_reduce_array(int op, int dtype, const void *in, int64_t count, void *out,
                                 unsigned long long *slots, unsigned int *done, cudaStream_t s);
+// Peer mode: wait until both neighbours delivered every sweep this rank
+// completed (before a peer-attached buffer is read back or released).
+cudaError_t launch_peer_drain(unsigned long long *win, int has_up, int has_dn, cudaStream_t s);
+// Barrier over all ranks through the peer windows (communicator-less worlds).
+cudaError_t launch_peer_barrier(unsigned long long *win, int nranks, cudaStream_t s);
 cudaError_t launch_rank_combine(int op, int dtype, const void *gathered, int64_t count,
                                 int nranks, void *out, cudaStream_t s);
 
@@ -88,6 +117,13 @@ struct JacobiArgs {
   unsigned long long *dyn_counter;
   unsigned int *done;
   int32_t *trace;       // [team | unit | hits] planes of ntiles*BM*BN int32, or null
+  // fused halo exchange with ranks r-1 / r+1 (peer mode): null win = off
+  unsigned long long *win;          // local peer window
+  unsigned long long *win_up, *win_dn;  // neighbours' windows (null at the ends)
+  float *peer_up, *peer_dn;         // neighbours' OUT buffers (local row 0)
+  int64_t peer_up_row0, peer_dn_row0;
+  int64_t send_up_row, send_dn_row;  // my first / last owned row (-1: none)
+  int64_t halo_up_row, halo_dn_row;  // my halo rows read from the neighbours (-1: none)
 };
 bool jacobi_supported_tile(int bm, int bn);
 // tmc / tmh: CUtensorMap (128 B) of the input buffer with boxes {BN, BM+2}

@@ -72,6 +72,13 @@ struct upir_map_s {
   int64_t elem_offset;           // global element index of local element 0
   int64_t elem_bytes;
   bool pinned = false;     // took a user count on a registration
+  // peer mode (fused halo): exported from a cudaMalloc block; neighbours'
+  // buffers mapped by CUDA IPC ([0] = rank - 1, [1] = rank + 1)
+  bool ipc_alloc = false;
+  void *peer_base[2] = {nullptr, nullptr};
+  float *peer_dev[2] = {nullptr, nullptr};
+  int64_t peer_row0[2] = {0, 0};
+  bool halo_fused = false;  // last written by a peer-mode sweep: halos already exchanged
 };
 
 struct upir_event_s {
@@ -116,6 +123,10 @@ struct upir_ctx_s {
   std::vector<upir_spmd> regions;
   cudaError_t sticky = cudaSuccess;
   bool capturing = false;
+  // peer window (WinWord layout) and the other ranks' windows mapped by IPC
+  unsigned long long *win = nullptr;
+  unsigned long long *peer_win[WIN_MAX_RANKS] = {};
+  void *peer_win_base[WIN_MAX_RANKS] = {};
   // statistics
   int64_t h2d_bytes = 0, d2h_bytes = 0, launches = 0;
 };
@@ -155,7 +166,6 @@ extern "C" upir_status upir_init(int cuda_device, const upir_world *world, upir_
                 prop.major, prop.minor);
   if (world && (world->nranks < 1 || world->rank < 0 || world->rank >= world->nranks))
     return fail(UPIR_E_INVALID, "bad world rank %d / nranks %d", world->rank, world->nranks);
-  if (world && world->nranks > 1 && !world->nccl_id) return fail(UPIR_E_INVALID, "nranks > 1 needs an nccl_id");
   CUDA_TRY(cudaSetDevice(cuda_device));
   upir_ctx c = new upir_ctx_s();
   c->device = cuda_device;
@@ -192,7 +202,19 @@ extern "C" upir_status upir_init(int cuda_device, const upir_world *world, upir_
   c->dyn = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(c->done) + 64);
   if (cudaMalloc(&c->one, 64) != cudaSuccess) return cleanup(fail(UPIR_E_OOM, "workspace allocation failed"));
   if (ensure_slots(c, (size_t)1 << 16) != UPIR_OK) return cleanup(UPIR_E_OOM);
-  if (c->nranks > 1) {
+  // peer window: plain cudaMalloc block (CUDA-IPC exportable), zeroed; its own
+  // entry of the peer table points at itself
+  if (cudaMalloc(&c->win, WIN_BYTES) != cudaSuccess || cudaMemset(c->win, 0, WIN_BYTES) != cudaSuccess)
+    return cleanup(fail(UPIR_E_OOM, "peer window allocation failed"));
+  if (c->rank < WIN_MAX_RANKS) {
+    c->peer_win[c->rank] = c->win;
+    unsigned long long self = (unsigned long long)(uintptr_t)c->win;
+    if (cudaMemcpy(c->win + WIN_PEERS + c->rank, &self, 8, cudaMemcpyHostToDevice) != cudaSuccess)
+      return cleanup(fail(UPIR_E_CUDA, "peer window init failed"));
+  }
+  // nccl_id NULL with nranks > 1: a communicator-less world -- only the peer
+  // window paths (fused world reduction / halo, peer barrier) exchange data
+  if (c->nranks > 1 && world->nccl_id) {
     ncclUniqueId id;
     memcpy(&id, world->nccl_id, sizeof id);
     ncclResult_t r = ncclCommInitRank(&c->comm, c->nranks, id, c->rank);
@@ -236,6 +258,9 @@ extern "C" upir_status upir_finalize(upir_ctx c) {
   upir_status st = sticky_check(c);
   for (auto &r : c->registered) cudaHostUnregister(r.ptr);
   for (auto s : c->regions) delete s;
+  for (int q = 0; q < WIN_MAX_RANKS; ++q)
+    if (c->peer_win_base[q]) cudaIpcCloseMemHandle(c->peer_win_base[q]);
+  cudaFree(c->win);
   if (c->comm) ncclCommDestroy(c->comm);
   cudaFree(c->slots);
   cudaFree(c->done);
@@ -387,6 +412,8 @@ static upir_status copy_to_compute(upir_ctx c) {
   CUDA_TRY(cudaEventDestroy(ev));
   return UPIR_OK;
 }
+static upir_status peer_release(upir_ctx c, upir_map m);
+
 static upir_status compute_to_copy(upir_ctx c) {
   cudaEvent_t ev;
   CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -478,6 +505,8 @@ extern "C" upir_status upir_data_unmap(upir_ctx c, upir_map m) {
   if (!m->owned) {
     auto it = std::find(c->adopted.begin(), c->adopted.end(), m);
     if (it == c->adopted.end()) return fail(UPIR_E_INVALID, "map not live");
+    upir_status pst = peer_release(c, m);
+    if (pst != UPIR_OK) return pst;
     c->adopted.erase(it);
     delete m;
     return sticky_check(c);
@@ -485,7 +514,9 @@ extern "C" upir_status upir_data_unmap(upir_ctx c, upir_map m) {
   auto it = c->present.find(m->host);
   if (it == c->present.end() || it->second != m) return fail(UPIR_E_INVALID, "map not live");
   if (--m->refcount > 0) return UPIR_OK;
-  upir_status st = compute_to_copy(c);
+  upir_status st = peer_release(c, m);
+  if (st != UPIR_OK) return st;
+  st = compute_to_copy(c);
   if (st != UPIR_OK) return st;
   if (m->kind == UPIR_MAP_FROM || m->kind == UPIR_MAP_TOFROM) {   // data_movement backward
     size_t ho, dof, len;
@@ -493,7 +524,12 @@ extern "C" upir_status upir_data_unmap(upir_ctx c, upir_map m) {
     CUDA_TRY(cudaMemcpyAsync((char *)m->host + ho, (char *)m->dev + dof, len, cudaMemcpyDeviceToHost, c->copy));
     c->d2h_bytes += (int64_t)len;
   }
-  CUDA_TRY(cudaFreeAsync(m->dev, c->copy));   // mm_deallocator
+  if (m->ipc_alloc) {   // exported block: plain free once the copy is done
+    CUDA_TRY(cudaStreamSynchronize(c->copy));
+    CUDA_TRY(cudaFree(m->dev));
+  } else {
+    CUDA_TRY(cudaFreeAsync(m->dev, c->copy));   // mm_deallocator
+  }
   if (m->pinned) unpin_host(c, m->host);
   c->present.erase(it);
   delete m;
@@ -546,6 +582,163 @@ extern "C" upir_status upir_data_device_ptr(upir_map m, void **dptr, int64_t *lo
   if (dptr) *dptr = m->dev;
   if (local_elems) *local_elems = m->elems_local;
   if (global_offset) *global_offset = m->elem_offset;
+  return UPIR_OK;
+}
+
+// ------------------------------------------------------------------ peer windows (CUDA IPC)
+static upir_status check_map(upir_ctx c, upir_map m, const char *what);
+// A record carries one CUDA-IPC handle plus the layout facts the importer
+// checks; the caller moves records between ranks (e.g. torch.distributed).
+namespace {
+struct PeerRec {
+  uint32_t magic;            // PEER_MAGIC
+  uint32_t kind;             // 0 = context window, 1 = map buffer
+  int32_t rank, nranks;
+  cudaIpcMemHandle_t handle;
+  int64_t offset;            // byte offset of the buffer inside the exported allocation
+  int64_t loc_row_lo, row_elems, elem_bytes, n_rows;
+  int32_t halo_rows, pad;
+};
+static_assert(sizeof(PeerRec) <= UPIR_PEER_REC_BYTES, "peer record size");
+constexpr uint32_t PEER_MAGIC = 0x52495055u;   // "UPIR"
+}  // namespace
+
+// Allocation base of a device pointer (driver cuMemGetAddressRange).
+static bool alloc_base(void *p, void **base) {
+  typedef CUresult (*Fn)(CUdeviceptr *, size_t *, CUdeviceptr);
+  static Fn fn = nullptr;
+  if (!fn) {
+    cudaDriverEntryPointQueryResult q;
+    void *f = nullptr;
+    if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess || !f)
+      return false;
+    fn = reinterpret_cast<Fn>(f);
+  }
+  CUdeviceptr b = 0;
+  size_t sz = 0;
+  if (fn(&b, &sz, (CUdeviceptr)(uintptr_t)p) != CUDA_SUCCESS) return false;
+  *base = (void *)(uintptr_t)b;
+  return true;
+}
+
+static bool world_ready(upir_ctx c) {
+  if (c->nranks > WIN_MAX_RANKS) return false;
+  for (int q = 0; q < c->nranks; ++q)
+    if (!c->peer_win[q]) return false;
+  return true;
+}
+
+extern "C" upir_status upir_peer_export(upir_ctx c, upir_map m, void *rec) {
+  if (!c || !rec) return fail(UPIR_E_INVALID, "NULL argument");
+  cudaSetDevice(c->device);
+  PeerRec r;
+  memset(&r, 0, sizeof r);
+  r.magic = PEER_MAGIC;
+  r.rank = c->rank;
+  r.nranks = c->nranks;
+  if (!m) {
+    r.kind = 0;
+    CUDA_TRY(cudaIpcGetMemHandle(&r.handle, c->win));
+  } else {
+    upir_status st = check_map(c, m, "map");
+    if (st != UPIR_OK) return st;
+    if (m->dist.pattern != UPIR_PATTERN_BLOCK)
+      return fail(UPIR_E_INVALID, "peer export needs a BLOCK-distributed map (its halo rows are the peers' targets)");
+    if (c->capturing) return fail(UPIR_E_INVALID, "peer export during graph capture");
+    if (m->owned && !m->ipc_alloc) {
+      // stream-ordered pool blocks are not IPC-exportable: move the buffer to
+      // a plain cudaMalloc block (device pointers taken earlier go stale)
+      CUDA_TRY(cudaStreamSynchronize(c->compute));
+      CUDA_TRY(cudaStreamSynchronize(c->copy));
+      void *nb = nullptr;
+      const size_t alloc = std::max<size_t>(256, (m->dev_bytes + 255) / 256 * 256);
+      if (cudaMalloc(&nb, alloc) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(UPIR_E_OOM, "peer buffer of %zu bytes", alloc);
+      }
+      CUDA_TRY(cudaMemcpy(nb, m->dev, m->dev_bytes, cudaMemcpyDeviceToDevice));
+      CUDA_TRY(cudaFreeAsync(m->dev, c->copy));
+      CUDA_TRY(cudaStreamSynchronize(c->copy));
+      m->dev = nb;
+      m->ipc_alloc = true;
+    }
+    void *base = m->dev;
+    if (!m->owned && !alloc_base(m->dev, &base)) return fail(UPIR_E_CUDA, "cannot resolve the allocation of an adopted buffer");
+    CUDA_TRY(cudaIpcGetMemHandle(&r.handle, base));
+    r.kind = 1;
+    r.offset = (int64_t)((char *)m->dev - (char *)base);
+    r.loc_row_lo = m->loc_row_lo;
+    r.row_elems = m->dist.row_elems;
+    r.elem_bytes = m->dist.elem_bytes;
+    r.n_rows = m->dist.n_rows;
+    r.halo_rows = m->dist.halo_rows;
+  }
+  memset(rec, 0, UPIR_PEER_REC_BYTES);
+  memcpy(rec, &r, sizeof r);
+  return UPIR_OK;
+}
+
+extern "C" upir_status upir_peer_import(upir_ctx c, upir_map m, int32_t peer, const void *rec) {
+  if (!c || !rec) return fail(UPIR_E_INVALID, "NULL argument");
+  PeerRec r;
+  memcpy(&r, rec, sizeof r);
+  if (r.magic != PEER_MAGIC) return fail(UPIR_E_INVALID, "not a peer record");
+  if (peer < 0 || peer >= c->nranks || r.rank != peer || r.nranks != c->nranks)
+    return fail(UPIR_E_INVALID, "peer record of rank %d/%d imported as rank %d/%d", r.rank, r.nranks, peer, c->nranks);
+  cudaSetDevice(c->device);
+  if (!m) {
+    if (r.kind != 0) return fail(UPIR_E_INVALID, "record is not a context window");
+    if (peer >= WIN_MAX_RANKS) return fail(UPIR_E_UNSUPPORTED, "peer windows support at most %d ranks", WIN_MAX_RANKS);
+    if (peer == c->rank || c->peer_win[peer]) return UPIR_OK;
+    void *p = nullptr;
+    CUDA_TRY(cudaIpcOpenMemHandle(&p, r.handle, cudaIpcMemLazyEnablePeerAccess));
+    c->peer_win_base[peer] = p;
+    c->peer_win[peer] = reinterpret_cast<unsigned long long *>((char *)p + r.offset);
+    const unsigned long long v = (unsigned long long)(uintptr_t)c->peer_win[peer];
+    CUDA_TRY(cudaMemcpy(c->win + WIN_PEERS + peer, &v, 8, cudaMemcpyHostToDevice));
+    return UPIR_OK;
+  }
+  upir_status st = check_map(c, m, "map");
+  if (st != UPIR_OK) return st;
+  if (r.kind != 1) return fail(UPIR_E_INVALID, "record is not a map buffer");
+  if (m->dist.pattern != UPIR_PATTERN_BLOCK || r.n_rows != m->dist.n_rows || r.row_elems != m->dist.row_elems ||
+      r.elem_bytes != m->dist.elem_bytes)
+    return fail(UPIR_E_INVALID, "peer map layout differs from this map's");
+  const int side = peer == c->rank - 1 ? 0 : (peer == c->rank + 1 ? 1 : -1);
+  if (side < 0) return fail(UPIR_E_INVALID, "map buffers are imported from the halo neighbours (rank +- 1) only");
+  if (m->peer_base[side]) {
+    CUDA_TRY(cudaStreamSynchronize(c->compute));
+    cudaIpcCloseMemHandle(m->peer_base[side]);
+    m->peer_base[side] = nullptr;
+    m->peer_dev[side] = nullptr;
+  }
+  void *p = nullptr;
+  CUDA_TRY(cudaIpcOpenMemHandle(&p, r.handle, cudaIpcMemLazyEnablePeerAccess));
+  m->peer_base[side] = p;
+  m->peer_dev[side] = reinterpret_cast<float *>((char *)p + r.offset);
+  m->peer_row0[side] = r.loc_row_lo;
+  return UPIR_OK;
+}
+
+// Before a peer-attached buffer is read back or released: the neighbours'
+// last sweeps (which store into its halo rows) must have been delivered, and
+// this rank's kernels must be done with the neighbours' buffers.
+static upir_status peer_release(upir_ctx c, upir_map m) {
+  if (!m->peer_base[0] && !m->peer_base[1] && !m->ipc_alloc) return UPIR_OK;
+  const bool up = c->rank > 0 && c->peer_win[c->rank - 1];
+  const bool dn = c->rank + 1 < c->nranks && c->rank + 1 < WIN_MAX_RANKS && c->peer_win[c->rank + 1];
+  if (up || dn) {
+    cudaError_t e = launch_peer_drain(c->win, up, dn, c->compute);
+    if (e != cudaSuccess) return fail(UPIR_E_CUDA, "peer drain launch failed: %s", cudaGetErrorString(e));
+  }
+  CUDA_TRY(cudaStreamSynchronize(c->compute));
+  for (int side = 0; side < 2; ++side)
+    if (m->peer_base[side]) {
+      cudaIpcCloseMemHandle(m->peer_base[side]);
+      m->peer_base[side] = nullptr;
+      m->peer_dev[side] = nullptr;
+    }
   return UPIR_OK;
 }
 
@@ -878,6 +1071,31 @@ static upir_status exec_stream(upir_spmd s, const upir_loop_desc *l, const upir_
       memcpy(&a.red[r].init_bits, &v, 8);
     }
   }
+  // UPIR_WORLD_REDUCE: upir.sync allreduce fused into the loop (peer windows),
+  // else the loop with the original value applied on rank 0 only, followed
+  // by upir_reduce(WORLD) (NCCL) on each result -- the same combination
+  bool world_after = false;
+  if ((l->flags & UPIR_WORLD_REDUCE) && c->nranks > 1 && n_reds > 0) {
+    if (world_ready(c)) {
+      a.wwin = c->win;
+      a.wrank = c->rank;
+      a.wranks = c->nranks;
+    } else if (c->comm) {
+      world_after = true;
+      if (c->rank != 0)
+        for (int r = 0; r < n_reds; ++r) {
+          if (reds[r].dtype == UPIR_I64) {
+            int64_t v = reds[r].op == UPIR_OP_SUM ? 0 : (reds[r].op == UPIR_OP_MAX ? INT64_MIN : INT64_MAX);
+            a.red[r].init_bits = (uint64_t)v;
+          } else {
+            double v = reds[r].op == UPIR_OP_SUM ? 0.0 : (reds[r].op == UPIR_OP_MAX ? -HUGE_VAL : HUGE_VAL);
+            memcpy(&a.red[r].init_bits, &v, 8);
+          }
+        }
+    } else {
+      return fail(UPIR_E_INVALID, "UPIR_WORLD_REDUCE needs every rank's peer window (upir_peer_import) or a communicator");
+    }
+  }
   a.trace = trace ? (int32_t *)trace->dev : nullptr;
   // long per-unit chunks: 256-bit loads, 4 in flight; AXPY aligns each unit's
   // main loop to whole 128-B lines so its stores complete lines (measured best
@@ -950,6 +1168,11 @@ static upir_status exec_stream(upir_spmd s, const upir_loop_desc *l, const upir_
                                      sd.num_teams, sd.num_units, smem, a, c->compute);
   if (e != cudaSuccess) return fail(UPIR_E_CUDA, "loop kernel launch failed: %s", cudaGetErrorString(e));
   c->launches++;
+  if (world_after)
+    for (int r = 0; r < n_reds; ++r) {
+      st = upir_reduce(c, reds[r].op, reds[r].dtype, reds[r].dev_result, 1, reds[r].dev_result, UPIR_SCOPE_WORLD);
+      if (st != UPIR_OK) return st;
+    }
   return UPIR_OK;
 }
 
@@ -968,6 +1191,7 @@ extern "C" upir_status upir_loop_exec(upir_spmd s, const upir_loop_desc *l, cons
   if (st != UPIR_OK) return st;
   if (c->sticky != cudaSuccess) return sticky_check(c);
   cudaSetDevice(c->device);
+  if (b->out) b->out->halo_fused = false;   // set again by a peer-mode sweep
   switch (b->kind) {
     case UPIR_BODY_AXPY:
     case UPIR_BODY_REDUCE: st = exec_stream(s, l, b, reds, n_reds, trace); break;
@@ -1014,6 +1238,9 @@ static upir_status exec_jacobi(upir_spmd s, const upir_loop_desc *l, const upir_
   int64_t lb0 = l->lb[0], ub0 = l->ub[0], lb1 = l->lb[1], ub1 = l->ub[1];
   if (lb0 < 1 || ub0 > ny - 1 || lb1 < 1 || ub1 > ld - 1)
     return fail(UPIR_E_INVALID, "JACOBI5 iteration space must lie in the grid interior [1,ny-1) x [1,ld-1)");
+  // peer mode: the out map has imported neighbour buffers (fused halo)
+  const upir_map mo = b->out;
+  const bool peer = sd.target == UPIR_TARGET_CLUSTER && c->nranks > 1 && (mo->peer_dev[0] || mo->peer_dev[1]);
   if (sd.target == UPIR_TARGET_CLUSTER && c->nranks > 1) {
     upir_map m = b->in0;
     if (m->dist.pattern != UPIR_PATTERN_BLOCK) return fail(UPIR_E_INVALID, "cluster JACOBI5 needs BLOCK-distributed maps");
@@ -1025,6 +1252,30 @@ static upir_status exec_jacobi(upir_spmd s, const upir_loop_desc *l, const upir_
                 (long long)ub0, (long long)row0, (long long)(row0 + rows_local));
   JacobiArgs a;
   memset(&a, 0, sizeof a);
+  if (peer) {
+    int64_t plan[8];
+    if ((st = upir_halo_plan(mo->dist.n_rows, mo->dist.halo_rows, c->rank, c->nranks, plan)) != UPIR_OK) return st;
+    a.send_up_row = a.send_dn_row = a.halo_up_row = a.halo_dn_row = -1;
+    if (plan[1] > plan[0]) {   // exchange with rank - 1: send row lo, read halo row lo - 1
+      if (!mo->peer_dev[0] || !c->peer_win[c->rank - 1])
+        return fail(UPIR_E_INVALID, "peer-mode JACOBI5: rank %d's buffer / window not imported", c->rank - 1);
+      a.win_up = c->peer_win[c->rank - 1];
+      a.peer_up = mo->peer_dev[0];
+      a.peer_up_row0 = mo->peer_row0[0];
+      a.send_up_row = plan[0];
+      a.halo_up_row = plan[0] - 1;
+    }
+    if (plan[5] > plan[4]) {   // exchange with rank + 1: send row hi - 1, read halo row hi
+      if (!mo->peer_dev[1] || c->rank + 1 >= WIN_MAX_RANKS || !c->peer_win[c->rank + 1])
+        return fail(UPIR_E_INVALID, "peer-mode JACOBI5: rank %d's buffer / window not imported", c->rank + 1);
+      a.win_dn = c->peer_win[c->rank + 1];
+      a.peer_dn = mo->peer_dev[1];
+      a.peer_dn_row0 = mo->peer_row0[1];
+      a.send_dn_row = plan[5] - 1;
+      a.halo_dn_row = plan[5];
+    }
+    a.win = c->win;
+  }
   a.out = reinterpret_cast<float *>(b->out->dev);
   a.ld = ld;
   a.row0 = row0;
@@ -1032,11 +1283,16 @@ static upir_status exec_jacobi(upir_spmd s, const upir_loop_desc *l, const upir_
   a.ub0 = ub0;
   a.lb1 = lb1;
   a.ub1 = ub1;
-  if (ub0 <= lb0 || ub1 <= lb1) return UPIR_OK;   // empty iteration space
-  a.ti0 = lb0 / bm;
-  a.tj0 = lb1 / bn;
-  a.ntr = (ub0 + bm - 1) / bm - a.ti0;
-  a.ntc = (ub1 + bn - 1) / bn - a.tj0;
+  const bool empty = ub0 <= lb0 || ub1 <= lb1;
+  if (empty && !peer) return UPIR_OK;   // empty iteration space
+  if (!empty) {
+    a.ti0 = lb0 / bm;
+    a.tj0 = lb1 / bn;
+    a.ntr = (ub0 + bm - 1) / bm - a.ti0;
+    a.ntc = (ub1 + bn - 1) / bn - a.tj0;
+  } else {
+    a.ntc = 1;   // no tiles; the sweep still delivers to the neighbours
+  }
   int sk;
   int64_t chunk;
   if ((st = tile_sched(l, sk, chunk)) != UPIR_OK) return st;
@@ -1061,6 +1317,7 @@ static upir_status exec_jacobi(upir_spmd s, const upir_loop_desc *l, const upir_
   cudaError_t e = launch_jacobi_tma(a, &tmc, &tmh, sd.num_teams, sd.num_units, bm, bn, trace != nullptr, c->compute);
   if (e != cudaSuccess) return fail(UPIR_E_CUDA, "JACOBI5 launch failed: %s", cudaGetErrorString(e));
   c->launches++;
+  if (peer) mo->halo_fused = true;
   return UPIR_OK;
 }
 static upir_status exec_stencil(upir_spmd s, const upir_loop_desc *l, const upir_body *b, upir_map trace) {
@@ -1317,6 +1574,7 @@ extern "C" upir_status upir_reduce(upir_ctx c, int32_t op, int32_t dtype, const 
     c->scratch_bytes = need;
   }
   if (c->nranks > 1) {
+    if (!c->comm) return fail(UPIR_E_UNSUPPORTED, "upir_reduce(WORLD) needs a communicator (or UPIR_WORLD_REDUCE on a loop)");
     NCCL_TRY(ncclAllGather(dev_in, c->scratch, (size_t)count, dtype == UPIR_I64 ? ncclInt64 : ncclFloat32, c->comm,
                            c->compute));
   } else {
@@ -1332,6 +1590,9 @@ static upir_status halo_exchange(upir_ctx c, upir_map m, cudaStream_t strm) {
   if (m->dist.pattern != UPIR_PATTERN_BLOCK || m->dist.halo_rows < 1)
     return fail(UPIR_E_INVALID, "HALO needs a BLOCK-distributed map with halo_rows >= 1");
   if (c->nranks == 1) return UPIR_OK;
+  if (m->halo_fused) return UPIR_OK;   // exchanged inside the peer-mode sweep that wrote it
+  if (!c->comm)
+    return fail(UPIR_E_UNSUPPORTED, "communicator-less world: halos move only inside peer-mode sweeps");
   int64_t plan[8];
   upir_status st = upir_halo_plan(m->dist.n_rows, m->dist.halo_rows, c->rank, c->nranks, plan);
   if (st != UPIR_OK) return st;
@@ -1373,7 +1634,14 @@ extern "C" upir_status upir_sync(upir_ctx c, int32_t kind, upir_map halo_map, up
       upir_status st = upir_sync(c, UPIR_SYNC_BARRIER, nullptr, nullptr);
       if (st != UPIR_OK) return st;
       if (c->nranks > 1) {
-        NCCL_TRY(ncclAllReduce(c->one, c->one, 1, ncclInt32, ncclSum, c->comm, c->compute));
+        if (c->comm) {
+          NCCL_TRY(ncclAllReduce(c->one, c->one, 1, ncclInt32, ncclSum, c->comm, c->compute));
+        } else if (world_ready(c)) {
+          cudaError_t e = launch_peer_barrier(c->win, c->nranks, c->compute);
+          if (e != cudaSuccess) return fail(UPIR_E_CUDA, "peer barrier launch failed: %s", cudaGetErrorString(e));
+        } else {
+          return fail(UPIR_E_UNSUPPORTED, "WORLD_BARRIER needs a communicator or every rank's peer window");
+        }
         CUDA_TRY(cudaStreamSynchronize(c->compute));
       }
       return UPIR_OK;

@@ -1,0 +1,141 @@
+"""Worker processes of the peer-window tests (test harness only).
+
+Each worker is one rank of a communicator-less world (nccl_id NULL): the
+ranks share ONE GPU here (the only one this environment has), so the CUDA-IPC
+peer mappings, the .sys-scope signals and the in-kernel waits run exactly as
+between GPUs, with the ranks' kernels time-sliced instead of concurrent.
+Records move over a gloo process group; results go to .npy files.
+"""
+import os
+
+import numpy as np
+
+
+def _setup(rank, world, port):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    import torch.distributed as dist
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2209_10643_b200 as U
+    ctx = U.upir_init(0, rank, world, None)
+    return dist, U, ctx
+
+
+def world_reduce_worker(rank, world, port, out_dir, n, reps, use_graph):
+    dist, U, ctx = _setup(rank, world, port)
+    import torch
+
+    import synth
+    xi = synth.i64_sym(6, 0, n)
+    xf = synth.f32_unit(7, 0, n)
+    U.upir_peer_share(ctx)
+    mi = U.upir_data_map(ctx, xi, U.MAP_TO)
+    mf = U.upir_data_map(ctx, xf, U.MAP_TO)
+    res = torch.zeros(4 * reps, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    base = res.data_ptr()
+    s = U.upir_spmd_launch(ctx, U.spmd_desc(37, 96, U.TARGET_CLUSTER))
+    loop_i = U.loop_desc(0, n, policy=U.SCHED_STATIC, chunk=2, flags=U.WORLD_REDUCE)
+    loop_f = U.loop_desc(0, n, policy=U.SCHED_DYNAMIC, chunk=64, flags=U.WORLD_REDUCE)
+    init_i = np.array([7], np.int64)
+    init_f = np.array([0.5], np.float32)
+
+    def rep(k):
+        o = base + 32 * k
+        U.upir_loop_exec(s, loop_i, U.body(U.BODY_REDUCE, U.I64, in0=mi),
+                         [U.reduction(U.OP_SUM, U.I64, o, init=init_i), U.reduction(U.OP_MAX, U.I64, o + 8)])
+        U.upir_loop_exec(s, loop_f, U.body(U.BODY_REDUCE, U.F32, in0=mf),
+                         [U.reduction(U.OP_SUM, U.F32, o + 16, init=init_f), U.reduction(U.OP_MAX, U.F32, o + 24)])
+
+    if use_graph:
+        U.upir_graph_begin(ctx)
+        for k in range(reps):
+            rep(k)
+        g = U.upir_graph_end(ctx)
+        U.upir_graph_launch(ctx, g)
+        U.upir_sync(ctx)
+        U.upir_graph_launch(ctx, g)   # replay: the generation counters advance on the device
+        U.upir_sync(ctx)
+        U.upir_graph_destroy(g)
+    else:
+        for k in range(reps):
+            rep(k)
+    U.upir_spmd_end(s)
+    U.upir_sync(ctx, U.SYNC_WORLD_BARRIER)
+    raw = res.cpu().numpy().view(np.int64).reshape(reps, 4)
+    out = np.zeros((reps, 4), np.float64)
+    for k in range(reps):
+        out[k, 0] = float(raw[k, 0])
+        out[k, 1] = float(raw[k, 1])
+        out[k, 2] = float(np.frombuffer(raw[k, 2].tobytes()[:4], np.float32)[0])
+        out[k, 3] = float(np.frombuffer(raw[k, 3].tobytes()[:4], np.float32)[0])
+    np.save(os.path.join(out_dir, f"wr_{rank}.npy"), out)
+    np.save(os.path.join(out_dir, f"wri_{rank}.npy"), raw[:, :2].copy())
+    U.upir_data_unmap(ctx, mf)
+    U.upir_data_unmap(ctx, mi)
+    U.upir_sync(ctx)
+    U.upir_finalize(ctx)
+    dist.destroy_process_group()
+
+
+def jacobi_worker(rank, world, port, out_dir, ny, nx, S, tile, use_graph, adopt):
+    dist, U, ctx = _setup(rank, world, port)
+    import torch
+
+    import synth
+    g = synth.jacobi_init(ny, nx)
+    d = U.dist(ny, nx, 4, halo_rows=1)
+    a, b = g.copy(), g.copy()
+    keep = []
+    if adopt:
+        # torch-owned device grids (cudaMalloc-backed): local rows incl. halos
+        lo, hi = U.upir_dist_owned_rows(ny, rank, world)
+        r0, r1 = max(0, lo - 1), min(ny, hi + 1)
+        ta = torch.from_numpy(g[r0:r1].copy()).cuda()
+        tb = torch.from_numpy(g[r0:r1].copy()).cuda()
+        torch.cuda.synchronize()
+        keep = [ta, tb]
+        ma = U.upir_data_adopt(ctx, ta, d, nbytes=g.nbytes)
+        mb = U.upir_data_adopt(ctx, tb, d, nbytes=g.nbytes)
+    else:
+        ma = U.upir_data_map(ctx, a, U.MAP_TOFROM, d)
+        mb = U.upir_data_map(ctx, b, U.MAP_TOFROM, d)
+    U.upir_peer_share(ctx, [ma, mb])
+    s = U.upir_spmd_launch(ctx, U.spmd_desc(5, 128, U.TARGET_CLUSTER))
+    loop = U.loop_desc([1, 1], [ny - 1, nx - 1], tile=list(tile), distribute=U.DIST_TEAMS, inner_chunk=4)
+    bodies = [U.body(U.BODY_JACOBI5, U.F32, in0=ma, out=mb, ld=(nx, 0, 0), dims=(ny, 0, 0)),
+              U.body(U.BODY_JACOBI5, U.F32, in0=mb, out=ma, ld=(nx, 0, 0), dims=(ny, 0, 0))]
+
+    def sweeps(k0, count):
+        for k in range(k0, k0 + count):
+            U.upir_loop_exec(s, loop, bodies[k % 2])
+            U.upir_sync(ctx, U.SYNC_HALO, halo_map=bodies[k % 2].out)   # fused: returns at once
+
+    if use_graph:
+        assert S % 4 == 0
+        U.upir_graph_begin(ctx)
+        sweeps(0, S // 2)
+        gr = U.upir_graph_end(ctx)
+        U.upir_graph_launch(ctx, gr)
+        U.upir_graph_launch(ctx, gr)
+        U.upir_graph_destroy(gr)
+    else:
+        sweeps(0, S)
+    U.upir_spmd_end(s)
+    lo, hi = U.upir_dist_owned_rows(ny, rank, world)
+    if adopt:
+        U.upir_sync(ctx)
+        fin = (keep[0] if S % 2 == 0 else keep[1]).cpu().numpy()
+        r0 = max(0, lo - 1)
+        own = fin[lo - r0:hi - r0].copy()
+        U.upir_data_unmap(ctx, mb)
+        U.upir_data_unmap(ctx, ma)
+    else:
+        U.upir_data_unmap(ctx, mb)
+        U.upir_data_unmap(ctx, ma)
+        U.upir_sync(ctx)
+        own = (a if S % 2 == 0 else b)[lo:hi].copy()
+    np.save(os.path.join(out_dir, f"jac_{rank}.npy"), own)
+    U.upir_sync(ctx, U.SYNC_WORLD_BARRIER)
+    U.upir_finalize(ctx)
+    dist.destroy_process_group()

@@ -1,0 +1,98 @@
+"""Peer-window paths (NVLink peer memory between ranks) at world sizes 2 and
+3, with the ranks as separate processes sharing the one GPU of this
+environment (see tests/peer_worker.py):
+
+* UPIR_WORLD_REDUCE -- upir.sync allreduce fused into the loop kernel:
+  every rank gets init (+) the global reduction; int64 and fp32 max
+  bit-exact against the oracle, fp32 sum within 1e-5 * sum|x| (north_star);
+  repeated and graph-replayed reductions (generation / parity logic).
+* Fused halo -- peer-mode JACOBI5 sweeps store boundary rows into the
+  neighbours' halo rows and wait in-kernel for the neighbours' previous
+  sweep; the assembled grid after S sweeps matches the fp64 oracle within
+  1e-5 * max|ref| and is bit-identical to the one-rank sweep of the same
+  kernel (decomposition invariance, reading c16).
+"""
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+import oracle
+import paper_2209_10643_b200 as U
+import peer_worker
+import synth
+
+pytestmark = pytest.mark.gpu
+
+
+def _port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _spawn(fn, world, *args):
+    mp.spawn(fn, args=(world, _port()) + args, nprocs=world, join=True)
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("world,use_graph", [(2, False), (3, False), (2, True)])
+def test_fused_world_reduce(upir, tmp_path, world, use_graph):
+    n, reps = 300_007, 3
+    _spawn(peer_worker.world_reduce_worker, world, str(tmp_path), n, reps, use_graph)
+    xi = synth.i64_sym(6, 0, n)
+    xf = synth.f32_unit(7, 0, n)
+    want_si = oracle.world_reduce(oracle.SUM, [7, oracle.reduce_i64(oracle.SUM, xi)])
+    want_mi = int(xi.max())
+    want_sf = 0.5 + oracle.reduce_f32(oracle.SUM, xf)
+    want_mf = float(xf.max())
+    for r in range(world):
+        raw = np.load(tmp_path / f"wri_{r}.npy")
+        got = np.load(tmp_path / f"wr_{r}.npy")
+        for k in range(reps):
+            assert int(raw[k, 0]) == want_si, (r, k)
+            assert int(raw[k, 1]) == want_mi, (r, k)
+            assert abs(got[k, 2] - want_sf) <= 1e-5 * want_sf, (r, k)
+            assert got[k, 3] == want_mf, (r, k)
+    # every rank holds the identical combination (ascending rank order)
+    ref = np.load(tmp_path / "wr_0.npy")
+    for r in range(1, world):
+        assert (np.load(tmp_path / f"wr_{r}.npy") == ref).all()
+
+
+def _jacobi_one_rank(g, S, tile):
+    ny, nx = g.shape
+    ctx = U.upir_init(0)
+    a, b = g.copy(), g.copy()
+    ma = U.upir_data_map(ctx, a, U.MAP_TOFROM)
+    mb = U.upir_data_map(ctx, b, U.MAP_TOFROM)
+    s = U.upir_spmd_launch(ctx, U.spmd_desc(5, 128))
+    loop = U.loop_desc([1, 1], [ny - 1, nx - 1], tile=list(tile), distribute=U.DIST_TEAMS, inner_chunk=4)
+    for k in range(S):
+        src, dst = (ma, mb) if k % 2 == 0 else (mb, ma)
+        U.upir_loop_exec(s, loop, U.body(U.BODY_JACOBI5, U.F32, in0=src, out=dst, ld=(nx, 0, 0), dims=(ny, 0, 0)))
+    U.upir_spmd_end(s)
+    U.upir_data_unmap(ctx, mb)
+    U.upir_data_unmap(ctx, ma)
+    U.upir_sync(ctx)
+    U.upir_finalize(ctx)
+    return a if S % 2 == 0 else b
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("world,ny,nx,S,tile,use_graph,adopt", [
+    (2, 70, 132, 6, (8, 64), False, False),
+    (3, 61, 200, 5, (8, 64), False, False),
+    (2, 67, 264, 8, (16, 256), True, False),
+    (2, 70, 132, 4, (8, 64), False, True),
+])
+def test_fused_halo_jacobi(upir, tmp_path, world, ny, nx, S, tile, use_graph, adopt):
+    _spawn(peer_worker.jacobi_worker, world, str(tmp_path), ny, nx, S, tile, use_graph, adopt)
+    g = synth.jacobi_init(ny, nx)
+    got = np.concatenate([np.load(tmp_path / f"jac_{r}.npy") for r in range(world)])
+    assert got.shape == (ny, nx)
+    ref = oracle.jacobi5(g, S)
+    assert np.abs(got - ref).max() <= 1e-5 * np.abs(ref).max()
+    one = _jacobi_one_rank(g, S, tile)
+    assert (got == one).all()
