@@ -240,17 +240,30 @@ def run_upir(args):
     import paper_2209_10643_b200 as U
 
     rank, world, local = dist_env()
+    # test hook (not a bench configuration): every rank on cuda:0, gloo for
+    # the host plumbing, a communicator-less upir world (peer windows only) --
+    # exercises the N > 1 code of this script on a one-GPU box
+    shared = os.environ.get("UPIR_BENCH_SHARED_GPU") == "1"
+    if shared:
+        local = 0
+        os.environ["LOCAL_RANK"] = "0"
     torch.cuda.set_device(local)
     numa_cpus = pin_to_gpu_numa(local)
     pg = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if shared:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         pg = dist
         _PG[0] = dist
-        idb = [U.upir_comm_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(idb, src=0)
-        ctx = U.upir_init(local, rank=rank, nranks=world, nccl_id=idb[0])
+        if shared:
+            ctx = U.upir_init(local, rank=rank, nranks=world, nccl_id=None)
+        else:
+            idb = [U.upir_comm_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(idb, src=0)
+            ctx = U.upir_init(local, rank=rank, nranks=world, nccl_id=idb[0])
     else:
         ctx = U.upir_init(local)
     stream = torch.cuda.ExternalStream(U.upir_ctx_stream(ctx, 0))
@@ -326,8 +339,12 @@ def bench_reduce(args, U, ctx, stream, barrier, rank, world, peaks, peak_src):
     base = res_t.data_ptr()
     reds_i = [U.reduction(U.OP_SUM, U.I64, base + 0), U.reduction(U.OP_MAX, U.I64, base + 8)]
     reds_f = [U.reduction(U.OP_SUM, U.F32, base + 16), U.reduction(U.OP_MAX, U.F32, base + 24)]
-    loop_i = U.loop_desc(0, n, policy=pol, chunk=ci)
-    loop_f = U.loop_desc(0, n, policy=pol, chunk=cf)
+    peer = use_peer(world)
+    if peer:
+        U.upir_peer_share(ctx)
+    wflag = U.WORLD_REDUCE if peer else 0
+    loop_i = U.loop_desc(0, n, policy=pol, chunk=ci, flags=wflag)
+    loop_f = U.loop_desc(0, n, policy=pol, chunk=cf, flags=wflag)
     spmd = U.upir_spmd_launch(ctx, U.spmd_desc(teams, units))
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
 
@@ -341,7 +358,7 @@ def bench_reduce(args, U, ctx, stream, barrier, rank, world, peaks, peak_src):
         U.upir_loop_exec(spmd, loop_f, U.body(U.BODY_REDUCE, U.F32, in0=mf), reds_f)
         if e:
             e[2].record(stream)
-        if world > 1:
+        if world > 1 and not peer:
             U.upir_reduce(ctx, U.OP_SUM, U.I64, base + 0, 1, base + 32, U.SCOPE_WORLD)
             U.upir_reduce(ctx, U.OP_MAX, U.I64, base + 8, 1, base + 40, U.SCOPE_WORLD)
             U.upir_reduce(ctx, U.OP_SUM, U.F32, base + 16, 1, base + 48, U.SCOPE_WORLD)
@@ -398,11 +415,13 @@ def bench_reduce(args, U, ctx, stream, barrier, rank, world, peaks, peak_src):
         mr = U.upir_data_map(ctx, hres, U.MAP_FROM)
         rp, _, _ = U.upir_data_device_ptr(mr)
         s = U.upir_spmd_launch(ctx, U.spmd_desc(teams, units))
-        U.upir_loop_exec(s, U.loop_desc(0, e2e_n, policy=pol, chunk=ci), U.body(U.BODY_REDUCE, U.I64, in0=m1),
+        U.upir_loop_exec(s, U.loop_desc(0, e2e_n, policy=pol, chunk=ci, flags=wflag),
+                         U.body(U.BODY_REDUCE, U.I64, in0=m1),
                          [U.reduction(U.OP_SUM, U.I64, rp + 0), U.reduction(U.OP_MAX, U.I64, rp + 8)])
-        U.upir_loop_exec(s, U.loop_desc(0, e2e_n, policy=pol, chunk=cf), U.body(U.BODY_REDUCE, U.F32, in0=m2),
+        U.upir_loop_exec(s, U.loop_desc(0, e2e_n, policy=pol, chunk=cf, flags=wflag),
+                         U.body(U.BODY_REDUCE, U.F32, in0=m2),
                          [U.reduction(U.OP_SUM, U.F32, rp + 16), U.reduction(U.OP_MAX, U.F32, rp + 24)])
-        if world > 1:
+        if world > 1 and not peer:
             for k, (op, dt) in enumerate(((U.OP_SUM, U.I64), (U.OP_MAX, U.I64), (U.OP_SUM, U.F32),
                                           (U.OP_MAX, U.F32))):
                 U.upir_reduce(ctx, op, dt, rp + 8 * k, 1, rp + 32 + 8 * k, U.SCOPE_WORLD)
@@ -723,12 +742,16 @@ def bench_reduce34(args, U, ctx, stream, barrier, rank, world, peaks, peak_src):
     reds = [U.reduction(U.OP_SUM, U.I64, base), U.reduction(U.OP_MAX, U.I64, base + 8)]
     spmd = U.upir_spmd_launch(ctx, U.spmd_desc(148 * 4, 256, U.TARGET_CLUSTER))
     pol = {"static": U.SCHED_STATIC, "static1": U.SCHED_STATIC, "dynamic": U.SCHED_DYNAMIC}[args.sched]
-    loop = U.loop_desc(0, n, policy=pol, chunk=0 if args.sched == "static" else 2)
+    peer = use_peer(world)
+    if peer:
+        U.upir_peer_share(ctx)
+    loop = U.loop_desc(0, n, policy=pol, chunk=0 if args.sched == "static" else 2,
+                       flags=U.WORLD_REDUCE if world > 1 else 0)
 
     def step():
+        # world > 1: the allreduce is part of the loop (in-kernel over peer
+        # windows, or upir_reduce(WORLD) after it with UPIR_PEER=0)
         U.upir_loop_exec(spmd, loop, U.body(U.BODY_REDUCE, U.I64, in0=m), reds)
-        U.upir_reduce(ctx, U.OP_SUM, U.I64, base, 1, base + 16, U.SCOPE_WORLD)
-        U.upir_reduce(ctx, U.OP_MAX, U.I64, base + 8, 1, base + 24, U.SCOPE_WORLD)
 
     for _ in range(args.warmup):
         step()
@@ -752,7 +775,8 @@ def bench_reduce34(args, U, ctx, stream, barrier, rank, world, peaks, peak_src):
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "i64", "data": "synthetic",
         "config": {"workload": f"C5a: int64 sum+max over n=2^{int(math.log2(n))} BLOCK-distributed over {world} "
-                               f"GPU(s), 592x256 per GPU, schedule {args.sched}, upir_reduce(WORLD)",
+                               f"GPU(s), 592x256 per GPU, schedule {args.sched}, "
+                               f"world reduction {'fused in-kernel (peer windows)' if peer else 'NCCL'}",
                    "n_global": n, "parallelism": f"dp{world}", "l2": "inputs >> L2"},
         "roofline": {"bound": "hbm", "achieved": per_rank_gbs, "peak": peak, "unit": "GB/s",
                      "frac": per_rank_gbs / peak, "traffic": ncu_traffic("reduce_i64_1"),
@@ -765,6 +789,27 @@ def bench_reduce34(args, U, ctx, stream, barrier, rank, world, peaks, peak_src):
 
 
 _PG = [None]
+
+
+_PEER_OK = [None]
+
+
+def use_peer(world):
+    """N > 1: exchange through NVLink peer windows (fused world reduction /
+    fused halo) unless UPIR_PEER=0 selects the NCCL path, or some rank's GPU
+    cannot map another's memory (decided collectively, so all ranks agree)."""
+    if world == 1 or os.environ.get("UPIR_PEER", "1") == "0":
+        return False
+    if _PEER_OK[0] is None:
+        import torch
+        me = torch.cuda.current_device()
+        ok = all(torch.cuda.can_device_access_peer(me, d) for d in range(torch.cuda.device_count()) if d != me)
+        t = torch.tensor([1 if ok else 0], dtype=torch.int32)
+        if os.environ.get("UPIR_BENCH_SHARED_GPU") != "1":
+            t = t.cuda()
+        _PG[0].all_reduce(t, op=_PG[0].ReduceOp.MIN)
+        _PEER_OK[0] = bool(t.item())
+    return _PEER_OK[0]
 
 
 def pg_of():
@@ -787,6 +832,9 @@ def bench_jacobi32k(args, U, ctx, stream, barrier, rank, world, peaks, peak_src,
     ma, mb = U.upir_data_adopt(ctx, a_t, d), U.upir_data_adopt(ctx, b_t, d)
     U.upir_synth_fill(ctx, ma, 4, 5, 0, n, n)
     U.upir_synth_fill(ctx, mb, 4, 5, 0, n, n)
+    peer = use_peer(world)
+    if peer:   # fused halo: boundary rows stored into the neighbours' halos inside each sweep
+        U.upir_peer_share(ctx, [ma, mb])
     teams = int(os.environ.get("UPIR_JACOBI_TEAMS", 444))
     bm, bn = (int(v) for v in os.environ.get("UPIR_JACOBI_TILE", "16x256").split("x"))
     loop = U.loop_desc([1, 1], [n - 1, n - 1], tile=[bm, bn], policy=U.SCHED_STATIC, chunk=1,
@@ -798,7 +846,8 @@ def bench_jacobi32k(args, U, ctx, stream, barrier, rank, world, peaks, peak_src,
     def sweeps():
         for k in range(S):
             src, body = bodies[k % 2]
-            U.upir_sync(ctx, U.SYNC_HALO, halo_map=src)
+            if not peer:
+                U.upir_sync(ctx, U.SYNC_HALO, halo_map=src)
             U.upir_loop_exec(s, loop, body)
 
     U.upir_graph_begin(ctx)
@@ -830,7 +879,8 @@ def bench_jacobi32k(args, U, ctx, stream, barrier, rank, world, peaks, peak_src,
         "n_gpus": world, "steps": reps, "warmup": 1, "ms_per_step": ms, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
         "config": {"workload": f"C5b: Jacobi 5-point {n}x{n} fp32, {S} sweeps as one CUDA graph, BLOCK row slabs "
-                               f"over {world} GPU(s) with 1-row halos (upir_sync HALO before each sweep), tiles "
+                               f"over {world} GPU(s) with 1-row halos "
+                               f"({'fused peer stores in each sweep' if peer else 'upir_sync HALO before each sweep'}), tiles "
                                f"{bm}x{bn} static,1 over {teams} teams",
                    "parallelism": f"dp{world}", "l2": "2 x 4 GiB grids >> L2"},
         "roofline": {"bound": "hbm", "achieved": per_rank_gbs, "peak": peak, "unit": "GB/s",
