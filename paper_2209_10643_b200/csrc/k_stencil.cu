@@ -23,8 +23,16 @@ struct SLayout {
   // columns plus one of 8, each landing as its own dense [WR][box] block
   static constexpr bool WIDE = WC > 256;
   static constexpr int NB = WIDE ? (WC - 8) / 256 : 0;
-  static constexpr int BUF = ((WR * WC * 4) + 127) / 128 * 128;
-  static constexpr int SMEM = 2 * BUF + 256 + F * F * 4 + 128;
+  // strip layout (BN = 4 * units): one dense [WR][SW] block per warp holding
+  // the warp's 128 output columns plus 4 halo columns each side
+  static constexpr int SW = 136, NS = BN / 128;
+  static constexpr int SBLK = (WR * SW * 4 + 127) / 128 * 128;   // TMA destinations are 128-B aligned
+  static constexpr int STX = WR * SW * 4 * (NS > 0 ? NS : 1);    // bytes one strip window delivers
+  static constexpr int GBUF = WR * WC * 4, SBUF = SBLK * (NS > 0 ? NS : 1);
+  static constexpr int BUF = (((GBUF > SBUF ? GBUF : SBUF)) + 127) / 128 * 128;
+  // pipeline depth (window buffers)
+  static constexpr int NST = 2;   // 3 stages measured slower: they cost a resident CTA per SM
+  static constexpr int SMEM = NST * BUF + 256 + F * F * 4 + 128;
 };
 
 // smem offset (floats) of window (row, col) -- col a multiple of 4 for vectors
@@ -45,15 +53,18 @@ __device__ __forceinline__ int win_off(int row, int col) {
 template <int R, int BM, int BN, int MAXT>
 __global__ void __launch_bounds__(MAXT) stencil_kernel(const __grid_constant__ StencilArgs a,
                                                        const __grid_constant__ CUtensorMap tmw,
-                                                       const __grid_constant__ CUtensorMap tmw8) {
+                                                       const __grid_constant__ CUtensorMap tmw8,
+                                                       const __grid_constant__ CUtensorMap tms) {
   // window column c holds global column j0 - 4 + c (4-aligned so that a
   // unit's taps are read as 16-B vectors)
   using L = SLayout<R, BM, BN>;
   constexpr int F = L::F, WR = L::WR, WCP = L::WC;
   extern __shared__ __align__(128) char smc[];
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smc + 2 * L::BUF);
-  volatile long long *tile_s = reinterpret_cast<volatile long long *>(smc + 2 * L::BUF + 16);
-  float *w = reinterpret_cast<float *>(smc + 2 * L::BUF + 256);
+  constexpr int NST = L::NST;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smc + NST * L::BUF);
+  // bars: full[NST] (TMA landed / end marker), empty[NST] (every warp done with the buffer)
+  volatile long long *tile_s = reinterpret_cast<volatile long long *>(smc + NST * L::BUF + 64);
+  float *w = reinterpret_cast<float *>(smc + NST * L::BUF + 256);
   __shared__ unsigned s_last;
   const int units = blockDim.x, u = threadIdx.x;
   for (int e = threadIdx.x; e < F * F; e += blockDim.x) w[e] = a.w[e];
@@ -88,9 +99,20 @@ __global__ void __launch_bounds__(MAXT) stencil_kernel(const __grid_constant__ S
     return cur++;
   };
   constexpr int POS = BM * BN;
+  // strip path: static,4 with BN = 4 * units -- unit u owns columns 4u..4u+3
+  // (traced runs take the generic static,4 path: same position -> unit map)
+  const bool strip = a.inner_chunk == 4 && BN == 4 * units && BN % 128 == 0 && MAXT <= 256 && !a.trace;
   auto issue = [&](int64_t tile, int buf) {
     const int64_t i0 = (a.ti0 + tile / a.ntc) * BM, j0 = (a.tj0 + tile % a.ntc) * BN;
     tma_fence_proxy();
+    if (strip) {
+      tma_mbar_expect_tx(bars + buf, L::STX);
+#pragma unroll 1
+      for (int w = 0; w < L::NS; ++w)
+        tma_load_2d(smc + buf * L::BUF + w * L::SBLK, &tms, (int)(j0 - 4 + 128 * w), (int)(i0 - R - a.row0),
+                    bars + buf);
+      return;
+    }
     tma_mbar_expect_tx(bars + buf, WR * WCP * 4);
     // window rows [i0-R, i0+BM+R) x cols [j0-4, j0+BN+4) of the local buffer
     if constexpr (!L::WIDE) {
@@ -107,90 +129,119 @@ __global__ void __launch_bounds__(MAXT) stencil_kernel(const __grid_constant__ S
   if (threadIdx.x == 0) {
     tma_prefetch_desc(&tmw);
     if constexpr (L::WIDE) tma_prefetch_desc(&tmw8);
-    tma_mbar_init(bars + 0, 1);
-    tma_mbar_init(bars + 1, 1);
+    if (strip) tma_prefetch_desc(&tms);
+#pragma unroll
+    for (int b = 0; b < NST; ++b) {
+      tma_mbar_init(bars + b, 1);
+      tma_mbar_init(bars + NST + b, (units + 31) >> 5);
+    }
     tma_fence_init();
-    const int64_t t0 = next_tile();
-    tile_s[0] = t0;
-    if (t0 >= 0) issue(t0, 0);
   }
   __syncthreads();
+  // Producer / consumer ring of NST window buffers without CTA-wide
+  // barriers: thread 0 claims tiles NST - 1 ahead and loads each into the
+  // buffer every warp has released (empty barrier); the warps wait only for
+  // their data (full barrier).  A tile id < 0 ends the loop (its full
+  // barrier completed by a plain arrive).
+  int64_t prod = 0;   // thread 0: id of the tile it produced last
+  auto produce = [&](int slot, bool wait_empty, unsigned parity) {
+    const int64_t nx = next_tile();
+    if (wait_empty) tma_mbar_wait(bars + NST + slot, parity);
+    tile_s[slot] = nx;
+    if (nx >= 0) issue(nx, slot);
+    else tma_mbar_arrive(bars + slot);
+    prod = nx;
+  };
+  if (threadIdx.x == 0)
+    for (int k = 0; k < NST - 1 && prod >= 0; ++k) produce(k, false, 0);
   for (int iter = 0;; ++iter) {
-    const int buf = iter & 1;
+    const int buf = iter % NST;
+    if (threadIdx.x == 0 && prod >= 0) {
+      // tile of iteration iter + NST - 1 into the buffer iteration iter - 1 used
+      const int slot = (iter + NST - 1) % NST;
+      produce(slot, iter >= 1, (unsigned)(((iter - 1) / NST) & 1));
+    }
+    tma_mbar_wait(bars + buf, (unsigned)((iter / NST) & 1));
     const int64_t tile = tile_s[buf];
     if (tile < 0) break;
-    if (threadIdx.x == 0) {
-      const int64_t nx = next_tile();
-      tile_s[buf ^ 1] = nx;
-      if (nx >= 0) issue(nx, buf ^ 1);
-    }
-    tma_mbar_wait(bars + buf, (unsigned)((iter >> 1) & 1));
     const float *win = reinterpret_cast<const float *>(smc + buf * L::BUF);
     const int64_t i0 = (a.ti0 + tile / a.ntc) * BM, j0 = (a.tj0 + tile % a.ntc) * BN;
     const int ic = a.inner_chunk;
-    if (ic == 4 && BN == 4 * MAXT && units == MAXT && MAXT <= 256) {
+    if (strip) {
       // static,4 with BN = 4 * units: unit u owns the 4-column strip c = 4u of
-      // every tile row (chunk k = r*units + u), visited top to bottom -- a
-      // sliding window of F input rows in registers: 3 LDS.128 per 4 outputs.
+      // every tile row (chunk k = r*units + u), visited top to bottom in
+      // blocks of H output rows.  The H + F - 1 input rows of a block stream
+      // through registers once (3 LDS.128 each) and each feeds the output
+      // rows it touches: H x 4 independent accumulator chains in flight, and
+      // the unrolled block body (H * F * F * 4 FFMA, weights in uniform
+      // registers) stays inside the 32 KB L1.5 instruction cache -- a fully
+      // unrolled tile does not (measured: 'no instruction' stalls).
+      // Per output the taps accumulate in the order filter row 0..F-1,
+      // column 0..F-1 from 0 -- the same sequence as the other paths.
+      constexpr int H = 4;   // H = 8 measured slower (code size, registers)
+      static_assert(BM % H == 0, "tile height must be a multiple of the row block");
       const int c = 4 * u;
       const int64_t j = j0 + c;
-      float v[F][12];
+      const bool jok = j + 3 >= a.lb1 && j < a.ub1;
+      // this unit's columns in its warp's strip block: compile-time offsets per (row, vector)
+      const float *sbase = win + (u >> 5) * (L::SBLK / 4) + (u & 31) * 4;
+      // a tile inside the iteration space with aligned rows stores without checks
+      const int64_t ld = a.ld;
+      float *dst0 = a.out + (i0 - a.row0) * ld + j;
+      const bool interior = i0 >= a.lb0 && i0 + BM <= a.ub0 && j0 >= a.lb1 && j0 + BN <= a.ub1 && (ld & 3) == 0 &&
+                            ((uintptr_t)a.out & 15) == 0;
+#pragma unroll 1
+      for (int r0 = 0; r0 < BM; r0 += H) {
+        float acc[H][4];
 #pragma unroll
-      for (int p = 0; p < F - 1; ++p) {
+        for (int h = 0; h < H; ++h)
 #pragma unroll
-        for (int q = 0; q < 3; ++q) {
-          const float4 t4 = *reinterpret_cast<const float4 *>(win + win_off<R, BM, BN>(p, c + 4 * q));
-          v[p][4 * q] = t4.x;
-          v[p][4 * q + 1] = t4.y;
-          v[p][4 * q + 2] = t4.z;
-          v[p][4 * q + 3] = t4.w;
-        }
-      }
+          for (int t = 0; t < 4; ++t) acc[h][t] = 0.f;
 #pragma unroll
-      for (int r = 0; r < BM; ++r) {
-        {   // bring in window row r + F - 1
+        for (int p = 0; p < H + F - 1; ++p) {   // window row r0 + p
+          float v[12];
 #pragma unroll
           for (int q = 0; q < 3; ++q) {
-            const float4 t4 = *reinterpret_cast<const float4 *>(win + win_off<R, BM, BN>(r + F - 1, c + 4 * q));
-            v[F - 1][4 * q] = t4.x;
-            v[F - 1][4 * q + 1] = t4.y;
-            v[F - 1][4 * q + 2] = t4.z;
-            v[F - 1][4 * q + 3] = t4.w;
+            const float4 t4 = *reinterpret_cast<const float4 *>(sbase + (r0 + p) * L::SW + 4 * q);
+            v[4 * q] = t4.x;
+            v[4 * q + 1] = t4.y;
+            v[4 * q + 2] = t4.z;
+            v[4 * q + 3] = t4.w;
           }
-        }
-        const int64_t i = i0 + r;
-        if (i >= a.lb0 && i < a.ub0 && j + 3 >= a.lb1 && j < a.ub1) {
-          float acc[4] = {0.f, 0.f, 0.f, 0.f};
+          // q outermost: the H x 4 chains of this input row interleave (each
+          // output still takes its taps in (filter row, column) order)
 #pragma unroll
-          for (int p = 0; p < F; ++p)
+          for (int q = 0; q < F; ++q)
 #pragma unroll
-            for (int q = 0; q < F; ++q)
+            for (int h = 0; h < H; ++h) {
+              const int pp = p - h;   // filter row feeding block row h
+              if (pp >= 0 && pp < F) {
 #pragma unroll
-              for (int t = 0; t < 4; ++t) acc[t] = __fmaf_rn(wr[p * F + q], v[p][4 - R + t + q], acc[t]);
-          float *dst = a.out + (i - a.row0) * a.ld + j;
-          if (j >= a.lb1 && j + 4 <= a.ub1 && ((uintptr_t)dst & 15) == 0) {
-            __stcs(reinterpret_cast<float4 *>(dst), make_float4(acc[0], acc[1], acc[2], acc[3]));
-          } else {
-#pragma unroll
-            for (int t = 0; t < 4; ++t)
-              if (j + t >= a.lb1 && j + t < a.ub1) dst[t] = acc[t];
-          }
-          if (a.trace) {
-#pragma unroll
-            for (int t = 0; t < 4; ++t)
-              if (j + t >= a.lb1 && j + t < a.ub1) {
-                const int64_t idx = tile * POS + r * BN + c + t;
-                a.trace[idx] = blockIdx.x;
-                a.trace[nt * POS + idx] = u;
-                atomicAdd(a.trace + 2 * nt * POS + idx, 1);
+                for (int t = 0; t < 4; ++t) acc[h][t] = __fmaf_rn(wr[pp * F + q], v[4 - R + t + q], acc[h][t]);
               }
+            }
+        }
+        float *dstb = dst0 + r0 * ld;
+        if (interior) {
+#pragma unroll
+          for (int h = 0; h < H; ++h)
+            __stcs(reinterpret_cast<float4 *>(dstb + h * ld), make_float4(acc[h][0], acc[h][1], acc[h][2], acc[h][3]));
+        } else {
+#pragma unroll
+          for (int h = 0; h < H; ++h) {
+            const int64_t i = i0 + r0 + h;
+            if (jok && i >= a.lb0 && i < a.ub0) {
+              float *dst = dstb + h * ld;
+              if (j >= a.lb1 && j + 4 <= a.ub1 && ((uintptr_t)dst & 15) == 0) {
+                __stcs(reinterpret_cast<float4 *>(dst), make_float4(acc[h][0], acc[h][1], acc[h][2], acc[h][3]));
+              } else {
+#pragma unroll
+                for (int t = 0; t < 4; ++t)
+                  if (j + t >= a.lb1 && j + t < a.ub1) dst[t] = acc[h][t];
+              }
+            }
           }
         }
-        // slide the window down one row
-#pragma unroll
-        for (int p = 0; p < F - 1; ++p)
-#pragma unroll
-          for (int q = 0; q < 12; ++q) v[p][q] = v[p + 1][q];
       }
     } else if (ic == 4) {
       for (int k = u; k * 4 < POS; k += units) {
@@ -255,7 +306,8 @@ __global__ void __launch_bounds__(MAXT) stencil_kernel(const __grid_constant__ S
         }
       }
     }
-    __syncthreads();   // buffer `buf` free; tile_s[buf ^ 1] visible
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) tma_mbar_arrive(bars + NST + buf);   // this warp is done with `buf`
   }
   if (a.sched == SK_DYNAMIC) {
     if (threadIdx.x == 0) {
@@ -273,7 +325,10 @@ __global__ void __launch_bounds__(MAXT) stencil_kernel(const __grid_constant__ S
 template <int R, int BM, int BN>
 cudaError_t launch_r(const StencilArgs &a, int teams, int units, cudaStream_t s) {
   using L = SLayout<R, BM, BN>;
-  CUtensorMap tm, tm8;
+  CUtensorMap tm, tm8, tms;
+  if (!encode_tmap_2d(&tms, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, a.in, (uint64_t)a.nx, (uint64_t)(a.ny - a.row0),
+                      (uint64_t)a.ld * 4, L::SW, L::WR, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B))
+    return cudaErrorInvalidValue;
   if (!encode_tmap_2d(&tm, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, a.in, (uint64_t)a.nx, (uint64_t)(a.ny - a.row0),
                       (uint64_t)a.ld * 4, L::WIDE ? 256 : L::WC, L::WR, CU_TENSOR_MAP_SWIZZLE_NONE,
                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B) ||
@@ -285,7 +340,7 @@ cudaError_t launch_r(const StencilArgs &a, int teams, int units, cudaStream_t s)
                                           : stencil_kernel<R, BM, BN, 1024>;
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
   if (e != cudaSuccess) return e;
-  k<<<teams, units, L::SMEM, s>>>(a, tm, tm8);
+  k<<<teams, units, L::SMEM, s>>>(a, tm, tm8, tms);
   return cudaGetLastError();
 }
 
@@ -293,7 +348,9 @@ cudaError_t launch_r(const StencilArgs &a, int teams, int units, cudaStream_t s)
 
 bool stencil_supported(int F, int bm, int bn) {
   return (F == 3 || F == 5 || F == 7) &&
-         ((bm == 16 && bn == 128) || (bm == 8 && bn == 64) || (bm == 16 && bn == 512) || (bm == 16 && bn == 1024));
+         ((bm == 16 && bn == 128) || (bm == 8 && bn == 64) || (bm == 16 && bn == 512) || (bm == 16 && bn == 1024) ||
+          (bm == 8 && bn == 512) || (bm == 8 && bn == 1024) || (bm == 8 && bn == 256) || (bm == 4 && bn == 512) ||
+          (bm == 4 && bn == 256));
 }
 
 cudaError_t launch_stencil(const StencilArgs &a, int F, int bm, int bn, int teams, int units, cudaStream_t s) {
@@ -311,6 +368,21 @@ cudaError_t launch_stencil(const StencilArgs &a, int F, int bm, int bn, int team
   UPIR_ST(1, 16, 1024)
   UPIR_ST(2, 16, 1024)
   UPIR_ST(3, 16, 1024)
+  UPIR_ST(1, 8, 512)
+  UPIR_ST(2, 8, 512)
+  UPIR_ST(3, 8, 512)
+  UPIR_ST(1, 8, 1024)
+  UPIR_ST(2, 8, 1024)
+  UPIR_ST(3, 8, 1024)
+  UPIR_ST(1, 8, 256)
+  UPIR_ST(2, 8, 256)
+  UPIR_ST(3, 8, 256)
+  UPIR_ST(1, 4, 512)
+  UPIR_ST(2, 4, 512)
+  UPIR_ST(3, 4, 512)
+  UPIR_ST(1, 4, 256)
+  UPIR_ST(2, 4, 256)
+  UPIR_ST(3, 4, 256)
 #undef UPIR_ST
   return cudaErrorInvalidValue;
 }

@@ -1331,7 +1331,7 @@ static upir_status exec_stencil(upir_spmd s, const upir_loop_desc *l, const upir
   const int R = (int)(F - 1) / 2;
   const int bm = (int)l->tile[0], bn = (int)l->tile[1];
   if (!stencil_supported((int)F, bm, bn))
-    return fail(UPIR_E_UNSUPPORTED, "STENCIL2D: filter size %lld / tile %dx%d not built (F 3/5/7, tiles 16x128, 8x64)",
+    return fail(UPIR_E_UNSUPPORTED, "STENCIL2D: filter size %lld / tile %dx%d not built (F 3/5/7, tiles 16x128, 8x64, 16x512, 16x1024, 8x512, 8x1024)",
                 (long long)F, bm, bn);
   if ((int64_t)b->in1->dev_bytes < F * F * 4) return fail(UPIR_E_INVALID, "weights map needs F*F fp32");
   if (ld % 4 != 0) return fail(UPIR_E_UNSUPPORTED, "STENCIL2D row pitch must be a multiple of 4 elements (TMA stride)");

@@ -111,8 +111,9 @@ def test_stencil_trace_mapping(ctx):
     assert (tr[:n][it] == ot[it]).all() and (tr[n:2 * n][it] == ou[it]).all()
 
 
-@pytest.mark.parametrize("tile,units", [((16, 512), 128), ((16, 1024), 256), ((16, 512), 64)])
-@pytest.mark.parametrize("F", [7, 3])
+@pytest.mark.parametrize("tile,units", [((16, 512), 128), ((16, 1024), 256), ((16, 512), 64), ((8, 512), 128),
+                                        ((8, 1024), 256), ((16, 128), 32)])
+@pytest.mark.parametrize("F", [7, 5, 3])
 def test_stencil_strip_tiles(ctx, tile, units, F):
     """BN = 4 * units: each unit owns one 4-column strip of the tile (static,4),
     computed with a sliding register window; other unit counts use the
@@ -123,10 +124,11 @@ def test_stencil_strip_tiles(ctx, tile, units, F):
     assert err(out, g, w, 2) <= 1e-5
 
 
-def test_stencil_strip_trace(ctx):
+@pytest.mark.parametrize("tile,units", [((16, 512), 128), ((8, 1024), 256)])
+def test_stencil_strip_trace(ctx, tile, units):
     g = synth.jacobi_init(40, 600)
     w = weights(7)
-    teams, units, tile = 3, 128, (16, 512)
+    teams = 3
     _, tr = stencil_gpu(ctx, g, w, teams=teams, units=units, tile=tile, chunk=1, trace=True)
     n = len(tr) // 3
     ot, ou = oracle.tiled_owner(3, 37, 3, 597, tile[0], tile[1], oracle.STATIC, 1, teams, 4, units)
