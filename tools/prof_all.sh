@@ -12,7 +12,7 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:matm
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:matmul_pair_kernel -s 3 -c 1 -o gpurun_out/prof_matmul_pair -f $B > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:matmul_kernel -s 6 -c 1 -o gpurun_out/prof_matmul_f32 -f $B > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:matvec -s 3 -c 1 -o gpurun_out/prof_matvec -f $B > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:stencil_kernel -s 13 -c 1 -o gpurun_out/prof_stencil7 -f $B > /dev/null 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:stencil_kernel -s 55 -c 1 -o gpurun_out/prof_stencil7 -f $B > /dev/null 2>&1
 UPIR_PROFILES_OUT=gpurun_out/profiles python tools/ncu_summary.py $TAG gpurun_out/prof_*.ncu-rep
 mkdir -p /tmp/ncu_keep && mv gpurun_out/prof_*.ncu-rep /tmp/ncu_keep/
 cp /tmp/ncu_keep/prof_matmul_pair.ncu-rep /tmp/ncu_keep/prof_jacobi.ncu-rep gpurun_out/ 2>/dev/null
