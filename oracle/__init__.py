@@ -54,6 +54,8 @@ def lib():
             "orc_delinearize": (None, [i32, vp, i64, vp]),
             "orc_schedule_chunks": (i64, [i32, i64, i64, i64, i64, vp, vp, i64]),
             "orc_owner_map": (i32, [i32, i64, i64, i64, vp]),
+            "orc_schedule_chunks_simd": (i64, [i32, i64, i64, i64, i64, i64, vp, vp, i64]),
+            "orc_owner_map_simd": (i32, [i32, i64, i64, i64, i64, vp]),
             "orc_axpy": (i32, [i64, i64, i64, i64, dbl, vp, vp, vp]),
             "orc_reduce_i64": (i32, [i32, i64, i64, i64, i64, i32, i64, i64, vp, i64, vp, vp]),
             "orc_reduce_f32": (i32, [i32, i64, i64, i64, i64, i32, i64, i64, vp, dbl, vp, vp]),
@@ -96,12 +98,14 @@ def delinearize(T, t):
 
 
 # ---- o2/o3 ------------------------------------------------------------------
-def schedule_chunks(policy, chunk, T, p, u):
+def schedule_chunks(policy, chunk, T, p, u, simdlen=1):
+    """Chunks [lo, hi) of unit u (o2/o3); simdlen > 1: the schedule of the
+    SIMD groups of simdlen iterations (reading c33)."""
     cap = 1
     while True:
         lo = np.zeros(cap, dtype=np.int64)
         hi = np.zeros(cap, dtype=np.int64)
-        n = lib().orc_schedule_chunks(policy, chunk, T, p, u, _p(lo), _p(hi), cap)
+        n = lib().orc_schedule_chunks_simd(policy, chunk, simdlen, T, p, u, _p(lo), _p(hi), cap)
         if n < 0:
             raise ValueError("invalid schedule")
         if n <= cap:
@@ -109,9 +113,9 @@ def schedule_chunks(policy, chunk, T, p, u):
         cap = n
 
 
-def owner_map(policy, chunk, T, p):
+def owner_map(policy, chunk, T, p, simdlen=1):
     owner = np.zeros(max(T, 1), dtype=np.int64)
-    _check(lib().orc_owner_map(policy, chunk, T, p, _p(owner)), "owner_map")
+    _check(lib().orc_owner_map_simd(policy, chunk, simdlen, T, p, _p(owner)), "owner_map")
     return owner[:T]
 
 

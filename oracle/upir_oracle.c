@@ -154,10 +154,39 @@ int64_t orc_schedule_chunks(int policy, int64_t chunk, int64_t T, int64_t p,
     return -1;
 }
 
+/* loop_parallel simd(simdlen(s)) combined with worksharing (PAPER.md:638,
+ * 647-648 'simd' / 'simdlen'; reading c33): the loop is strip-mined into
+ * ceil(T/s) SIMD groups of s consecutive iterations (the last one ragged),
+ * the worksharing schedule distributes the GROUPS (a chunk of c iterations
+ * becomes ceil(c/s) groups -- OpenMP's simd schedule modifier, chunk
+ * s*ceil(c/s)), and a unit executes each group as one s-lane vector.  The
+ * chunks below are the expansion of the group chunks back to iterations. */
+int64_t orc_schedule_chunks_simd(int policy, int64_t chunk, int64_t simdlen, int64_t T, int64_t p,
+                                 int64_t u, int64_t *lo, int64_t *hi, int64_t cap)
+{
+    if (simdlen <= 1) return orc_schedule_chunks(policy, chunk, T, p, u, lo, hi, cap);
+    if (T < 0) return -1;
+    int64_t s = simdlen;
+    int64_t Tg = (T + s - 1) / s;
+    int64_t cg = chunk <= 0 ? chunk : (chunk + s - 1) / s;
+    int64_t n = orc_schedule_chunks(policy, cg, Tg, p, u, lo, hi, cap);
+    for (int64_t k = 0; k < n && k < cap; ++k) {
+        lo[k] = lo[k] * s;
+        hi[k] = hi[k] * s < T ? hi[k] * s : T;
+    }
+    return n;
+}
+
 /* Executor of every normalised iteration t in [0,T): owner[t] = unit id in
  * [0,p), obtained by running the interpreter loop nest of the schedule
  * (for u ascending, for chunk of u, for t in chunk).  Returns 0, or -1. */
+int orc_owner_map_simd(int policy, int64_t chunk, int64_t simdlen, int64_t T, int64_t p, int64_t *owner);
 int orc_owner_map(int policy, int64_t chunk, int64_t T, int64_t p, int64_t *owner)
+{
+    return orc_owner_map_simd(policy, chunk, 1, T, p, owner);
+}
+
+int orc_owner_map_simd(int policy, int64_t chunk, int64_t simdlen, int64_t T, int64_t p, int64_t *owner)
 {
     int64_t cap = 1 << 16;
     int64_t *lo = (int64_t *)malloc(sizeof(int64_t) * (size_t)cap);
@@ -165,14 +194,14 @@ int orc_owner_map(int policy, int64_t chunk, int64_t T, int64_t p, int64_t *owne
     if (!lo || !hi) { free(lo); free(hi); return -1; }
     for (int64_t t = 0; t < T; ++t) owner[t] = -1;
     for (int64_t u = 0; u < p; ++u) {
-        int64_t n = orc_schedule_chunks(policy, chunk, T, p, u, lo, hi, cap);
+        int64_t n = orc_schedule_chunks_simd(policy, chunk, simdlen, T, p, u, lo, hi, cap);
         if (n < 0) { free(lo); free(hi); return -1; }
         if (n > cap) {  /* grow and redo */
             free(lo); free(hi); cap = n;
             lo = (int64_t *)malloc(sizeof(int64_t) * (size_t)cap);
             hi = (int64_t *)malloc(sizeof(int64_t) * (size_t)cap);
             if (!lo || !hi) { free(lo); free(hi); return -1; }
-            n = orc_schedule_chunks(policy, chunk, T, p, u, lo, hi, cap);
+            n = orc_schedule_chunks_simd(policy, chunk, simdlen, T, p, u, lo, hi, cap);
         }
         for (int64_t c = 0; c < n; ++c)
             for (int64_t t = lo[c]; t < hi[c]; ++t) {

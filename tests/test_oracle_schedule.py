@@ -203,3 +203,79 @@ def test_tiled_owner_bruteforce():
     assert t == len(team)
     # every iteration appears exactly once
     assert (team >= 0).sum() == (ub0 - lb0) * (ub1 - lb1)
+
+
+# ---- simd(simdlen) combined with worksharing (reading c33) -------------------------
+SIMD_CASES = [(T, p, s) for T in (0, 1, 7, 64, 100, 1001) for p in (1, 3, 8) for s in (2, 4, 8)]
+
+
+@pytest.mark.parametrize("T,p,s", SIMD_CASES)
+def test_simd_static_chunk_is_openmp_simd_modifier(T, p, s):
+    # OpenMP 4.5 2.7.1 'simd' schedule modifier: chunk_size becomes
+    # simd_width * ceil(chunk_size / simd_width) -- a plain static,c' schedule
+    for c in (1, 3, 5, 8, 13):
+        c2 = s * math.ceil(c / s)
+        for u in range(p):
+            assert oracle.schedule_chunks(oracle.STATIC, c, T, p, u, simdlen=s) == \
+                oracle.schedule_chunks(oracle.STATIC, c2, T, p, u)
+
+
+@pytest.mark.parametrize("T,p,s", SIMD_CASES)
+def test_simd_dynamic_partition_and_default_chunk(T, p, s):
+    # chunk partition of dynamic,c under simd = that of dynamic,s*ceil(c/s);
+    # the default chunk (1 iteration) becomes one SIMD group of s iterations
+    for c, c2 in ((0, s), (1, s), (5, s * math.ceil(5 / s))):
+        got = sorted(ch for u in range(p) for ch in oracle.schedule_chunks(oracle.DYNAMIC, c, T, p, u, simdlen=s))
+        want = [(k, min(k + c2, T)) for k in range(0, T, c2)]
+        assert got == want
+
+
+@pytest.mark.parametrize("T,p,s", SIMD_CASES)
+def test_simd_static_block_over_groups(T, p, s):
+    # brute force of the strip-mined block rule: G = ceil(T/s) groups, the
+    # first G mod p units own one group more; boundaries are multiples of s
+    G = -(-T // s)
+    q, r = divmod(G, p)
+    for u in range(p):
+        g0 = u * q + min(u, r)
+        g1 = g0 + q + (1 if u < r else 0)
+        want = [(g0 * s, min(g1 * s, T))] if g1 > g0 else []
+        assert oracle.schedule_chunks(oracle.STATIC, 0, T, p, u, simdlen=s) == want
+    if T % (s * p) == 0:   # groups split evenly: the plain block rule
+        for u in range(p):
+            assert oracle.schedule_chunks(oracle.STATIC, 0, T, p, u, simdlen=s) == \
+                oracle.schedule_chunks(oracle.STATIC, 0, T, p, u)
+
+
+@pytest.mark.parametrize("T,p,s", SIMD_CASES)
+def test_simd_every_policy_partitions_on_group_boundaries(T, p, s):
+    for pol, c in ((oracle.STATIC, 0), (oracle.STATIC, 3), (oracle.DYNAMIC, 2), (oracle.GUIDED, 0),
+                   (oracle.GUIDED, 5)):
+        owner = oracle.owner_map(pol, c, T, p, simdlen=s)
+        assert (owner >= 0).all() and (owner < p).all()
+        # each SIMD group (s consecutive iterations) is executed by one unit
+        for g0 in range(0, T, s):
+            assert len(set(owner[g0:g0 + s].tolist())) == 1
+        chunks = [ch for u in range(p) for ch in oracle.schedule_chunks(pol, c, T, p, u, simdlen=s)]
+        assert all(a % s == 0 and (b % s == 0 or b == T) for a, b in chunks)
+
+
+@pytest.mark.parametrize("T,p,s", [(1000, 3, 4), (4099, 8, 8), (17, 5, 2)])
+def test_simd_guided_group_sizes(T, p, s):
+    # guided over groups: chunk = max(ceil(remaining groups / p), ceil(c/s)) groups
+    c = 6
+    chunks = sorted(ch for u in range(p) for ch in oracle.schedule_chunks(oracle.GUIDED, c, T, p, u, simdlen=s))
+    G, g = -(-T // s), 0
+    for a, b in chunks:
+        assert a == g * s
+        n = max(-(-(G - g) // p), -(-c // s))
+        n = min(n, G - g)
+        assert b == min((g + n) * s, T)
+        g += n
+    assert g == G
+
+
+def test_simdlen_one_is_plain():
+    for pol, c in ((oracle.STATIC, 0), (oracle.STATIC, 7), (oracle.DYNAMIC, 3), (oracle.GUIDED, 2)):
+        for u in range(4):
+            assert oracle.schedule_chunks(pol, c, 99, 4, u, simdlen=1) == oracle.schedule_chunks(pol, c, 99, 4, u)
