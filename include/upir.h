@@ -260,8 +260,19 @@ typedef struct {
     int32_t inner_policy;    /* upir_sched, tiled nests only */
     int64_t inner_chunk;
     uint32_t flags;
-    uint32_t reserved;
+    uint32_t simdlen;        /* loop_parallel simd(simdlen); 0 or 1 = none (see below) */
 } upir_loop_desc;
+/* simd(simdlen(s)) with worksharing (reading c33):
+ * the loop the units execute is strip-mined into SIMD groups of s
+ * consecutive iterations (the last one ragged) and the schedule distributes
+ * whole groups -- chunk c becomes s*ceil(c/s) (OpenMP's simd schedule
+ * modifier; dynamic / guided default: one group), static without chunk is
+ * the block rule over ceil(T/s) groups, CLUSTER loops split groups over
+ * ranks -- and a unit executes each group as one s-lane vector.  Applies to
+ * the 1-D loops (AXPY, REDUCE, MATVEC rows), to the intra-tile position loop
+ * of tiled nests (JACOBI5, STENCIL2D: inner_chunk becomes s*ceil(c/s)) and to
+ * MATVEC's k-loop under distribute(teams); MATMUL's intra-tile work is a
+ * tensor-core operation already (no observable effect).  s <= 4096. */
 
 /* Loop bodies (the kernels of the paper's evaluation):
  *  AXPY    : y[i] = y[i] + alpha * x[i]    (Figs. 9/11)

@@ -35,7 +35,7 @@ def spmd_desc(num_teams, num_units, target=_abi.TARGET_GPU):
 
 
 def loop_desc(lb, ub, step=None, policy=_abi.SCHED_STATIC, chunk=0, distribute=_abi.DIST_TEAMS_UNITS,
-              tile=None, inner_policy=_abi.SCHED_STATIC, inner_chunk=0, flags=0):
+              tile=None, inner_policy=_abi.SCHED_STATIC, inner_chunk=0, flags=0, simdlen=0):
     lb = list(lb) if isinstance(lb, (list, tuple)) else [lb]
     ub = list(ub) if isinstance(ub, (list, tuple)) else [ub]
     n = len(lb)
@@ -51,6 +51,7 @@ def loop_desc(lb, ub, step=None, policy=_abi.SCHED_STATIC, chunk=0, distribute=_
     d.inner_policy = inner_policy
     d.inner_chunk = inner_chunk
     d.flags = flags
+    d.simdlen = simdlen
     return d
 
 

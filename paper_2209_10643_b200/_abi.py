@@ -48,7 +48,7 @@ class SpmdDesc(ctypes.Structure):
 class LoopDesc(ctypes.Structure):
     _fields_ = [("collapse", i32), ("policy", i32), ("lb", i64 * 3), ("ub", i64 * 3),
                 ("step", i64 * 3), ("tile", i64 * 3), ("chunk", i64), ("distribute", i32),
-                ("inner_policy", i32), ("inner_chunk", i64), ("flags", u32), ("reserved", u32)]
+                ("inner_policy", i32), ("inner_chunk", i64), ("flags", u32), ("simdlen", u32)]
 
 
 class Body(ctypes.Structure):

@@ -11,6 +11,7 @@
 //                            runs its row's k-loop sequentially.
 // HBM-bound: 4 B of A per multiply-add.  fp32 loads, fp32 FMA with four
 // independent accumulators per unit, fixed-order warp/team tree.
+#include "sched.cuh"
 #include "upir_internal.h"
 
 namespace upir {
@@ -34,9 +35,7 @@ __device__ __forceinline__ int64_t next_row(RowIter &it, const MatvecArgs &a, in
   if (a.sched == SK_STATIC_BLOCK) {
     if (it.started) return -1;
     it.started = true;
-    const int64_t q = T / p, r = T % p;
-    it.cur = t * q + (t < r ? t : r);
-    it.end = it.cur + q + (t < r ? 1 : 0);
+    block_range(T, a.simd, p, t, it.cur, it.end);   // groups of a.simd rows (c33)
   } else if (a.sched == SK_STATIC_CHUNK) {
     const int64_t kk = it.started ? it.k + p : t;
     it.started = true;

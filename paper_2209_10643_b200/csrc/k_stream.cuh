@@ -735,7 +735,7 @@ __global__ void __launch_bounds__(1024) stream_loop_kernel(const __grid_constant
       run(guided ? guided_work(b, nchunks, a.gtab, u) : ticket_work(b, a.ticket_m, a.T, a.chunk, u));
     }
   } else {
-    run(static_work(a.sched, a.T, a.chunk, u));
+    run(static_work(a.sched, a.T, a.chunk, u, a.simd));
   }
   reduce_epilogue<BODY, NRED>(a, acc, NRED > 0 || a.sched == SK_DYNAMIC || a.sched == SK_GUIDED);
 }

@@ -61,13 +61,27 @@ __device__ __forceinline__ UnitIds unit_ids(int distribute) {
   return u;
 }
 
-__device__ __forceinline__ LaneWork static_work(int sched, int64_t T, int64_t c, const UnitIds &u) {
+// Static block over SIMD groups of s iterations (simdlen, reading c33):
+// unit g owns groups [g*q + min(g,r), +q + (g<r)) of G = ceil(T/s); s = 1 is
+// the plain block rule.  Returns [start, end) in iterations.
+__device__ __forceinline__ void block_range(int64_t T, int64_t s, int64_t p, int64_t g, int64_t &start,
+                                            int64_t &end) {
+  const int64_t G = s > 1 ? (T + s - 1) / s : T;
+  const int64_t q = G / p, r = G % p;
+  const int64_t g0 = g * q + (g < r ? g : r);
+  const int64_t g1 = g0 + q + (g < r ? 1 : 0);
+  start = s > 1 ? g0 * s : g0;
+  end = s > 1 ? (g1 * s < T ? g1 * s : T) : g1;
+  if (end < start) end = start;
+}
+
+__device__ __forceinline__ LaneWork static_work(int sched, int64_t T, int64_t c, const UnitIds &u, int64_t s = 1) {
   LaneWork w{0, 0, 0, 1, nullptr};
   if (!u.active || T <= 0) return w;
   if (sched == SK_STATIC_BLOCK) {
-    const int64_t q = T / u.p, r = T % u.p;
-    const int64_t start = u.g * q + (u.g < r ? u.g : r);
-    const int64_t len = q + (u.g < r ? 1 : 0);
+    int64_t start, end;
+    block_range(T, s, u.p, u.g, start, end);
+    const int64_t len = end - start;
     w.lo0 = start;
     w.c = len > 0 ? len : 1;
     w.nk = len > 0 ? 1 : 0;

@@ -65,6 +65,7 @@ struct StreamArgs {
   float alpha;
   int64_t safe_lo, safe_hi;  // elements [safe_lo, safe_hi) may be read as 16-B vectors
   int32_t dvar;              // DIRECT long-chunk load variant (0: 4x16 B, 1: 4x32 B, 2: 2x32 B, 3: 8x16 B)
+  int64_t simd;              // static block: SIMD group size (simdlen, reading c33), 1 = none
   // reductions
   int32_t nred;
   RedSpec red[2];
@@ -159,6 +160,7 @@ struct MatvecArgs {
   unsigned long long *dyn_counter;
   unsigned int *done;
   int32_t *trace;               // [team | unit | hits] x T, or null
+  int64_t simd;                 // static block over SIMD groups of this many rows (1 = none)
 };
 cudaError_t launch_matvec(const MatvecArgs &a, int teams, int units, cudaStream_t s);
 

@@ -113,7 +113,7 @@ struct upir_ctx_s {
   // guided-schedule boundary table cache (T, p, c) -> device table
   int64_t *gtab = nullptr;
   size_t gtab_cap = 0;
-  int64_t g_T = -1, g_p = -1, g_c = -1, g_n = 0;
+  int64_t g_T = -1, g_p = -1, g_c = -1, g_s = -1, g_n = 0;
   // present table: host pointer -> map
   std::map<void *, upir_map> present;
   std::vector<upir_map> adopted;
@@ -861,11 +861,17 @@ static int body_dtype_ok(int kind, int dtype) {
   return 0;
 }
 
+// simd(simdlen) (reading c33): SIMD group size, and a chunk rounded up to
+// whole groups (OpenMP's simd schedule modifier).
+static int64_t simd_of(const upir_loop_desc *l) { return l->simdlen > 1 ? (int64_t)l->simdlen : 1; }
+static int64_t simd_chunk(int64_t c, int64_t s) { return s > 1 && c > 0 ? (c + s - 1) / s * s : c; }
+
 static upir_status validate_loop(const upir_spmd_desc *sd, const upir_loop_desc *l, int kind, int dtype,
                                  const upir_reduction *reds, int n_reds) {
   upir_status st = validate_spmd(sd);
   if (st != UPIR_OK) return st;
   if (!l) return fail(UPIR_E_INVALID, "loop descriptor is NULL");
+  if (l->simdlen > 4096) return fail(UPIR_E_INVALID, "simdlen %u outside [0, 4096]", l->simdlen);
   int64_t T;
   st = upir_loop_normalize(l, &T, nullptr);
   if (st != UPIR_OK) return st;
@@ -966,23 +972,27 @@ static const char *env_path() {
 
 // Guided chunk boundaries b_0 = 0, b_{g+1} = b_g + max(ceil((T - b_g)/p), c)
 // (PAPER.md:644 'guided'), cached on the device per (T, p, c).
-static upir_status guided_table(upir_ctx c, int64_t T, int64_t p, int64_t ch, const int64_t **tab, int64_t *nc) {
-  if (c->g_T == T && c->g_p == p && c->g_c == ch) {
+static upir_status guided_table(upir_ctx c, int64_t T, int64_t p, int64_t ch, int64_t simd, const int64_t **tab,
+                                int64_t *nc) {
+  if (c->g_T == T && c->g_p == p && c->g_c == ch && c->g_s == simd) {
     *tab = c->gtab;
     *nc = c->g_n;
     return UPIR_OK;
   }
   if (c->capturing) return fail(UPIR_E_INVALID, "guided table must be built before graph capture");
+  // chunk sequence over the G = ceil(T/s) SIMD groups (s = 1: iterations),
+  // boundaries scaled back to iterations (reading c33)
   std::vector<int64_t> b;
   b.push_back(0);
+  const int64_t G = (T + simd - 1) / simd, chg = (ch + simd - 1) / simd;
   int64_t start = 0;
-  while (start < T) {
-    const int64_t rem = T - start;
+  while (start < G) {
+    const int64_t rem = G - start;
     int64_t len = (rem + p - 1) / p;
-    if (len < ch) len = ch;
+    if (len < chg) len = chg;
     if (len > rem) len = rem;
     start += len;
-    b.push_back(start);
+    b.push_back(std::min(start * simd, T));
   }
   const size_t bytes = b.size() * sizeof(int64_t);
   CUDA_TRY(cudaStreamSynchronize(c->compute));
@@ -995,6 +1005,7 @@ static upir_status guided_table(upir_ctx c, int64_t T, int64_t p, int64_t ch, co
   c->g_T = T;
   c->g_p = p;
   c->g_c = ch;
+  c->g_s = simd;
   c->g_n = (int64_t)b.size() - 1;
   *tab = c->gtab;
   *nc = c->g_n;
@@ -1010,11 +1021,16 @@ static upir_status exec_stream(upir_spmd s, const upir_loop_desc *l, const upir_
   int sk;
   int64_t chunk;
   resolve_sched(l->policy, l->chunk, sk, chunk);
+  const int64_t simd = simd_of(l);
+  if (sk != SK_GUIDED) chunk = simd_chunk(chunk, simd);   // guided: rounded in its table
   int64_t lb = l->lb[0], step = l->step[0];
-  // cluster target: block-distribute the normalised space over ranks (c20)
+  // cluster target: block-distribute the normalised space over ranks (c20),
+  // whole SIMD groups per rank (c33)
   if (sd.target == UPIR_TARGET_CLUSTER && c->nranks > 1) {
     int64_t klo, khi;
-    upir_dist_owned_rows(T, c->rank, c->nranks, &klo, &khi);
+    upir_dist_owned_rows((T + simd - 1) / simd, c->rank, c->nranks, &klo, &khi);
+    klo = std::min(klo * simd, T);
+    khi = std::min(khi * simd, T);
     lb = lb + klo * step;
     T = khi - klo;
   }
@@ -1050,6 +1066,7 @@ static upir_status exec_stream(upir_spmd s, const upir_loop_desc *l, const upir_
   a.sched = sk;
   a.distribute = l->distribute;
   a.chunk = sk == SK_STATIC_BLOCK ? 1 : chunk;
+  a.simd = simd;
   a.in0 = vx.base_shifted;
   a.out = body == SB_AXPY ? vy.base_shifted : nullptr;
   a.alpha = (float)b->alpha;
@@ -1108,7 +1125,7 @@ static upir_status exec_stream(upir_spmd s, const upir_loop_desc *l, const upir_
                          : l->distribute == UPIR_DIST_UNITS ? sd.num_units
                          : (int64_t)sd.num_teams * sd.num_units;
   if (sk == SK_GUIDED) {
-    st = guided_table(c, T, p_sched, chunk, &a.gtab, &a.gchunks);
+    st = guided_table(c, T, p_sched, chunk, simd, &a.gtab, &a.gchunks);
     if (st != UPIR_OK) return st;
     a.dyn_counter = c->dyn;
   }
@@ -1126,7 +1143,7 @@ static upir_status exec_stream(upir_spmd s, const upir_loop_desc *l, const upir_
   const int64_t p = l->distribute == UPIR_DIST_TEAMS ? sd.num_teams
                    : l->distribute == UPIR_DIST_UNITS ? sd.num_units
                    : (int64_t)sd.num_teams * sd.num_units;
-  int64_t unit_chunk = sk == SK_STATIC_BLOCK ? (T + p - 1) / p : chunk;
+  int64_t unit_chunk = sk == SK_STATIC_BLOCK ? ((T + simd - 1) / simd + p - 1) / p * simd : chunk;
   // the staged path is warp-cooperative: it needs whole warps
   const bool can_stage = (step == 1 || step == -1) && vx.aligned16 && (body != SB_AXPY || vy.aligned16) &&
                          sd.num_units % 32 == 0;
@@ -1298,7 +1315,7 @@ static upir_status exec_jacobi(upir_spmd s, const upir_loop_desc *l, const upir_
   if ((st = tile_sched(l, sk, chunk)) != UPIR_OK) return st;
   a.sched = sk;
   a.chunk = chunk;
-  a.inner_chunk = (int)l->inner_chunk;
+  a.inner_chunk = (int)simd_chunk(l->inner_chunk, simd_of(l));   // intra-tile SIMD groups (c33)
   a.dyn_counter = c->dyn;
   a.done = c->done;
   if (trace) {
@@ -1373,7 +1390,7 @@ static upir_status exec_stencil(upir_spmd s, const upir_loop_desc *l, const upir
   if ((st = tile_sched(l, sk, chunk)) != UPIR_OK) return st;
   a.sched = sk;
   a.chunk = chunk;
-  a.inner_chunk = (int)l->inner_chunk;
+  a.inner_chunk = (int)simd_chunk(l->inner_chunk, simd_of(l));   // intra-tile SIMD groups (c33)
   a.dyn_counter = c->dyn;
   a.done = c->done;
   if (trace) {
@@ -1411,8 +1428,14 @@ static upir_status exec_matvec(upir_spmd s, const upir_loop_desc *l, const upir_
   if (sk == SK_DYNAMIC && l->distribute != UPIR_DIST_TEAMS)
     return fail(UPIR_E_UNSUPPORTED, "dynamic MATVEC rows are scheduled over teams only");
   if (sk == SK_STATIC_BLOCK) chunk = 1;
+  // simd (c33): the loop the units execute -- the k-loop under
+  // distribute(teams), else the row loop
+  const int64_t simd = simd_of(l);
+  const bool simd_rows = l->distribute != UPIR_DIST_TEAMS;
+  if (simd_rows && sk != SK_STATIC_BLOCK) chunk = simd_chunk(chunk, simd);
   MatvecArgs a;
   memset(&a, 0, sizeof a);
+  a.simd = simd_rows ? simd : 1;
   a.A = (const float *)b->in0->dev;
   a.x = (const float *)b->in1->dev;
   a.y = (float *)b->out->dev;
@@ -1423,7 +1446,7 @@ static upir_status exec_matvec(upir_spmd s, const upir_loop_desc *l, const upir_
   a.sched = sk;
   a.chunk = chunk;
   a.distribute = l->distribute;
-  a.inner_chunk = l->inner_chunk > 0 ? (int)l->inner_chunk : 4;
+  a.inner_chunk = (int)simd_chunk(l->inner_chunk > 0 ? l->inner_chunk : 4, simd_rows ? 1 : simd);
   a.dyn_counter = c->dyn;
   a.done = c->done;
   if (trace) {

@@ -29,7 +29,7 @@ def dev_scalar(dtype):
 
 
 def run_reduce(ctx, x, ops, teams, units, policy=U.SCHED_STATIC, chunk=0, distribute=U.DIST_TEAMS_UNITS,
-               lb=0, ub=None, step=1, inits=None, trace=False):
+               lb=0, ub=None, step=1, inits=None, trace=False, simdlen=0):
     """Map x (host numpy int64/float32) TO the device, run a REDUCE loop with the
     given reductions, return (results, trace arrays or None)."""
     dtype = U.I64 if x.dtype == np.int64 else U.F32
@@ -38,7 +38,7 @@ def run_reduce(ctx, x, ops, teams, units, policy=U.SCHED_STATIC, chunk=0, distri
     outs = [dev_scalar(dtype) for _ in ops]
     inits = inits or [None] * len(ops)
     reds = [U.reduction(op, dtype, o, init=i) for op, o, i in zip(ops, outs, inits)]
-    loop = U.loop_desc(lb, ub, step, policy=policy, chunk=chunk, distribute=distribute)
+    loop = U.loop_desc(lb, ub, step, policy=policy, chunk=chunk, distribute=distribute, simdlen=simdlen)
     T, _ = U.upir_loop_normalize(loop)
     tr = tm = None
     if trace:
@@ -59,14 +59,14 @@ def run_reduce(ctx, x, ops, teams, units, policy=U.SCHED_STATIC, chunk=0, distri
 
 
 def run_axpy(ctx, a, x, y, teams, units, policy=U.SCHED_STATIC, chunk=0, distribute=U.DIST_TEAMS_UNITS,
-             lb=0, ub=None, step=1, sum_=False, trace=False):
+             lb=0, ub=None, step=1, sum_=False, trace=False, simdlen=0):
     ub = len(y) if ub is None else ub
     yy = y.copy()
     mx = U.upir_data_map(ctx, x, U.MAP_TO)
     my = U.upir_data_map(ctx, yy, U.MAP_TOFROM)
     out = dev_scalar(U.F32)
     reds = [U.reduction(U.OP_SUM, U.F32, out)] if sum_ else None
-    loop = U.loop_desc(lb, ub, step, policy=policy, chunk=chunk, distribute=distribute)
+    loop = U.loop_desc(lb, ub, step, policy=policy, chunk=chunk, distribute=distribute, simdlen=simdlen)
     T, _ = U.upir_loop_normalize(loop)
     tr = tm = None
     if trace:

@@ -27,7 +27,7 @@ def ctx(upir):
 
 
 def jacobi_gpu(ctx, g, S, teams=8, units=256, tile=(32, 256), policy=U.SCHED_STATIC, chunk=1, ic=4,
-               space=None, graph=False, trace=False):
+               space=None, graph=False, trace=False, simdlen=0):
     """Run S ping-pong sweeps; returns (grid after S sweeps, trace or None)."""
     ny, nx = g.shape
     a, b = g.copy(), g.copy()
@@ -35,7 +35,7 @@ def jacobi_gpu(ctx, g, S, teams=8, units=256, tile=(32, 256), policy=U.SCHED_STA
     mb = U.upir_data_map(ctx, b, U.MAP_TOFROM)
     (lb0, ub0, lb1, ub1) = space or (1, ny - 1, 1, nx - 1)
     loop = U.loop_desc([lb0, lb1], [ub0, ub1], tile=list(tile), policy=policy, chunk=chunk,
-                       distribute=U.DIST_TEAMS, inner_chunk=ic)
+                       distribute=U.DIST_TEAMS, inner_chunk=ic, simdlen=simdlen)
     s = U.upir_spmd_launch(ctx, U.spmd_desc(teams, units))
     tr = tm = None
     if trace:

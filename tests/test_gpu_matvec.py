@@ -20,7 +20,7 @@ def ctx(upir):
 
 
 def matvec_gpu(ctx, A, x, teams, units, distribute=U.DIST_TEAMS, policy=U.SCHED_STATIC, chunk=0, ic=4,
-               lb=0, ub=None, trace=False):
+               lb=0, ub=None, trace=False, simdlen=0):
     M, K = A.shape
     ub = M if ub is None else ub
     y = np.full(M, -3.0, np.float32)
@@ -31,7 +31,7 @@ def matvec_gpu(ctx, A, x, teams, units, distribute=U.DIST_TEAMS, policy=U.SCHED_
     tm = U.upir_data_map(ctx, tr, U.MAP_TOFROM) if trace else None
     s = U.upir_spmd_launch(ctx, U.spmd_desc(teams, units))
     try:
-        U.upir_loop_exec(s, U.loop_desc(lb, ub, policy=policy, chunk=chunk, distribute=distribute, inner_chunk=ic),
+        U.upir_loop_exec(s, U.loop_desc(lb, ub, policy=policy, chunk=chunk, distribute=distribute, inner_chunk=ic, simdlen=simdlen),
                          U.body(U.BODY_MATVEC, U.F32, in0=ma, in1=mx, out=my, ld=(K, 0, 0), dims=(K, M, 0)),
                          trace=tm)
     finally:

@@ -24,7 +24,7 @@ def weights(F, seed=9):
 
 
 def stencil_gpu(ctx, g, w, S=1, teams=16, units=256, tile=(16, 128), policy=U.SCHED_STATIC, chunk=1, ic=4,
-                trace=False):
+                trace=False, simdlen=0):
     ny, nx = g.shape
     F = w.shape[0]
     R = (F - 1) // 2
@@ -32,7 +32,7 @@ def stencil_gpu(ctx, g, w, S=1, teams=16, units=256, tile=(16, 128), policy=U.SC
     ma, mb, mw = U.upir_data_map(ctx, a, U.MAP_TOFROM), U.upir_data_map(ctx, b, U.MAP_TOFROM), \
         U.upir_data_map(ctx, np.ascontiguousarray(w), U.MAP_TO)
     loop = U.loop_desc([R, R], [ny - R, nx - R], tile=list(tile), policy=policy, chunk=chunk,
-                       distribute=U.DIST_TEAMS, inner_chunk=ic)
+                       distribute=U.DIST_TEAMS, inner_chunk=ic, simdlen=simdlen)
     tr = tm = None
     if trace:
         nt = ((ny - R + tile[0] - 1) // tile[0] - R // tile[0]) * ((nx - R + tile[1] - 1) // tile[1] - R // tile[1])
