@@ -111,3 +111,12 @@ def test_validation_error_paths():
 def test_failed_validation_sets_message():
     assert _st(U.spmd_desc(1, 2000), U.loop_desc(0, 1), U.BODY_REDUCE, [U.reduction(0, U.I64, 0)]) == U.E_INVALID
     assert "num_units" in U.upir_last_error()
+
+
+def test_simdlen_validation_host():
+    """simdlen (reading c33) is validated without a device."""
+    ok = U.loop_desc(0, 100, simdlen=8)
+    U.upir_loop_validate(U.spmd_desc(1, 32), ok, U.BODY_REDUCE, [U.reduction(U.OP_SUM, U.I64, 0)])
+    bad = U.loop_desc(0, 100, simdlen=5000)
+    with pytest.raises(U.UpirError):
+        U.upir_loop_validate(U.spmd_desc(1, 32), bad, U.BODY_REDUCE, [U.reduction(U.OP_SUM, U.I64, 0)])

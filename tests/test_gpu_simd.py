@@ -118,10 +118,3 @@ def test_simd_matvec_rows(ctx, policy, chunk):
     # distribute(teams): SIMD groups of the k-loop (values only)
     y2, _ = matvec_gpu(ctx, A, x, 7, 64, distribute=U.DIST_TEAMS, ic=3, simdlen=8)
     matvec_check(y2, A, x)
-
-
-def test_simdlen_validation(ctx):
-    loop = U.loop_desc(0, 100, simdlen=5000)
-    with pytest.raises(U.UpirError):
-        U.upir_loop_validate(U.spmd_desc(1, 32), loop, U.BODY_REDUCE,
-                             [U.reduction(U.OP_SUM, U.I64, 0)])
