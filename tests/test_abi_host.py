@@ -115,8 +115,8 @@ def test_failed_validation_sets_message():
 
 def test_simdlen_validation_host():
     """simdlen (reading c33) is validated without a device."""
+    reds = [U.reduction(U.OP_SUM, U.I64, 0)]
     ok = U.loop_desc(0, 100, simdlen=8)
-    U.upir_loop_validate(U.spmd_desc(1, 32), ok, U.BODY_REDUCE, [U.reduction(U.OP_SUM, U.I64, 0)])
+    assert U.upir_loop_validate(U.spmd_desc(1, 32), ok, U.BODY_REDUCE, reds) == U.OK
     bad = U.loop_desc(0, 100, simdlen=5000)
-    with pytest.raises(U.UpirError):
-        U.upir_loop_validate(U.spmd_desc(1, 32), bad, U.BODY_REDUCE, [U.reduction(U.OP_SUM, U.I64, 0)])
+    assert U.upir_loop_validate(U.spmd_desc(1, 32), bad, U.BODY_REDUCE, reds) == U.E_INVALID
