@@ -594,11 +594,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(256, 1)
 }
 
 // CTA-pair variant for fp32 inputs (3xTF32): a team = 2 CTAs x 384 units.
-// Each CTA's TMA loads its raw fp32 A rows / B columns on ITS OWN full
-// barrier; its 4 split warps write hi / lo copies and then arrive on the
-// LEADER's ready barrier (8 arrivals per stage); the leader issues
+// The operands arrive pre-split (tf32_split_kernel: hi = rna_tf32(x),
+// lo = x - hi, one elementwise pass over A and B before the loop kernel), so
+// both CTAs' TMA loads of the hi and lo tiles (.cta_group::2) complete on
+// the LEADER's full barrier and no shared-memory rewrite competes with the
+// tensor core for shared-memory bandwidth; the leader issues
 // tcgen05.mma.cta_group::2.kind::tf32 (M = 256, N = 256, K = 8) three times
 // per k-step.  3 stages of 64 KB (hi + lo of A and B halves) per CTA.
+// Warps 8..11 of the 384-unit team have no role in this variant.
 constexpr int PF_STAGES = 3;
 constexpr int PF_A = 128 * 32 * 4;            // 16 KB: this CTA's A rows (one copy)
 constexpr int PF_B = 32 * 128 * 4;            // 16 KB: this CTA's B columns (4 boxes of 32)
@@ -617,7 +620,8 @@ __device__ __forceinline__ void mma_pair_tf32(uint32_t tmem_d, uint64_t adesc, u
 
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     matmul_pair_f32_kernel(const __grid_constant__ MatmulArgs a, const __grid_constant__ CUtensorMap tma,
-                           const __grid_constant__ CUtensorMap tmb) {
+                           const __grid_constant__ CUtensorMap tmb, const __grid_constant__ CUtensorMap tmal,
+                           const __grid_constant__ CUtensorMap tmbl) {
   extern __shared__ __align__(1024) char smem_raw[];
   char *smem = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + PF_STAGES * PF_STAGE);
@@ -638,10 +642,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tma);
     tma_prefetch_desc(&tmb);
+    tma_prefetch_desc(&tmal);
+    tma_prefetch_desc(&tmbl);
     for (int st = 0; st < PF_STAGES; ++st) {
       tma_mbar_init(full + st, 1);
       tma_mbar_init(empty + st, 1);
-      tma_mbar_init(ready + st, 8);    // 4 split warps x 2 CTAs (leader's copy is used)
     }
     for (int st = 0; st < 2; ++st) {
       tma_mbar_init(tfull + st, 1);
@@ -677,7 +682,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   }
 
   if (warp == 0) {
-    if (lane == 0) {   // ---------------- TMA producer (both CTAs, own full barrier)
+    if (lane == 0) {   // ---------------- TMA producer (both CTAs -> the leader's full barrier)
+      const uint32_t full_leader = map_to_cta(tma_smem(full), 0);
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t tile = seq.next(); tile >= 0; tile = seq.next()) {
@@ -686,12 +692,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         const int m0 = (int)((ti0 + ti) * PBM + 128 * rank), n0 = (int)((tj0 + tj) * BN + 128 * rank);
         for (int kb = 0; kb < KB; ++kb) {
           tma_mbar_wait(empty + stage, phase ^ 1);
-          char *sa = smem + stage * PF_STAGE;
+          char *sa = smem + stage * PF_STAGE;   // hi copy: A, B; lo copy at + PF_COPY
           char *sb = sa + PF_A;
-          tma_mbar_expect_tx(full + stage, PF_COPY);
-          tma_load_2d(sa, &tma, kb * 32, m0 - (int)a.row0, full + stage);
+          if (leader) tma_mbar_expect_tx(full + stage, 2 * PF_STAGE);
+          const uint32_t fb = full_leader + (uint32_t)(stage * 8);
+          tma_load_2d_pair(sa, &tma, kb * 32, m0 - (int)a.row0, fb);
+          tma_load_2d_pair(sa + PF_COPY, &tmal, kb * 32, m0 - (int)a.row0, fb);
 #pragma unroll
-          for (int j = 0; j < 4; ++j) tma_load_2d(sb + j * 4096, &tmb, n0 + 32 * j, kb * 32, full + stage);
+          for (int j = 0; j < 4; ++j) {
+            tma_load_2d_pair(sb + j * 4096, &tmb, n0 + 32 * j, kb * 32, fb);
+            tma_load_2d_pair(sb + PF_COPY + j * 4096, &tmbl, n0 + 32 * j, kb * 32, fb);
+          }
           if (++stage == PF_STAGES) {
             stage = 0;
             phase ^= 1;
@@ -711,7 +722,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + (uint32_t)(acc * BN);
         for (int kb = 0; kb < KB; ++kb) {
-          tma_mbar_wait(ready + stage, phase);
+          tma_mbar_wait(full + stage, phase);
           tc_fence_after();
           const char *hi = smem + stage * PF_STAGE;
           const char *lo = hi + PF_COPY;
@@ -777,39 +788,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
       __syncwarp();
       if (lane == 0) remote_arrive(tempty_leader + (uint32_t)(acc * 8));
     }
-  } else if (warp >= 8) {   // ---------------- 3xTF32 split of this CTA's tiles
-    const int tid = threadIdx.x - 256;
-    const uint32_t ready_leader = map_to_cta(tma_smem(ready), 0);
-    int stage = 0;
-    uint32_t phase = 0;
-    for (int64_t tile = seq.next(); tile >= 0; tile = seq.next()) {
-      for (int kb = 0; kb < KB; ++kb) {
-        tma_mbar_wait(full + stage, phase);
-        float4 *hi = reinterpret_cast<float4 *>(smem + stage * PF_STAGE);
-        float4 *lo = reinterpret_cast<float4 *>(smem + stage * PF_STAGE + PF_COPY);
-        for (int v = tid; v < PF_COPY / 16; v += 128) {
-          const float4 x = hi[v];
-          float4 h, l;
-          h.x = to_tf32(x.x);
-          h.y = to_tf32(x.y);
-          h.z = to_tf32(x.z);
-          h.w = to_tf32(x.w);
-          l.x = __fsub_rn(x.x, h.x);
-          l.y = __fsub_rn(x.y, h.y);
-          l.z = __fsub_rn(x.z, h.z);
-          l.w = __fsub_rn(x.w, h.w);
-          hi[v] = h;
-          lo[v] = l;
-        }
-        tma_fence_proxy();
-        __syncwarp();
-        if (lane == 0) remote_arrive(ready_leader + (uint32_t)(stage * 8));
-        if (++stage == PF_STAGES) {
-          stage = 0;
-          phase ^= 1;
-        }
-      }
-    }
   }
   tc_fence_before();
   cluster_sync_all();
@@ -818,7 +796,41 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;\n" ::"r"(tmem_base), "r"(TMEM_COLS));
 }
 
+// 3xTF32 operand split (pair variant): hi = rna_tf32(x), lo = x - hi, over
+// n elements (16-B vectors, scalar tail).
+__global__ void tf32_split_kernel(const float *__restrict__ src, float *__restrict__ hi, float *__restrict__ lo,
+                                  int64_t n) {
+  const int64_t n4 = n / 4, stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const float4 x = __ldcs(reinterpret_cast<const float4 *>(src) + i);
+    float4 h, l;
+    h.x = to_tf32(x.x);
+    h.y = to_tf32(x.y);
+    h.z = to_tf32(x.z);
+    h.w = to_tf32(x.w);
+    l.x = __fsub_rn(x.x, h.x);
+    l.y = __fsub_rn(x.y, h.y);
+    l.z = __fsub_rn(x.z, h.z);
+    l.w = __fsub_rn(x.w, h.w);
+    reinterpret_cast<float4 *>(hi)[i] = h;
+    reinterpret_cast<float4 *>(lo)[i] = l;
+  }
+  for (int64_t i = 4 * n4 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const float h = to_tf32(src[i]);
+    hi[i] = h;
+    lo[i] = __fsub_rn(src[i], h);
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_tf32_split(const float *src, float *hi, float *lo, int64_t n, int num_sms, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  const int64_t blocks = std::min<int64_t>((int64_t)num_sms * 4, (n / 4 + 255) / 256 + 1);
+  tf32_split_kernel<<<(int)blocks, 256, 0, s>>>(src, hi, lo, n);
+  return cudaGetLastError();
+}
+bool matmul_f32_presplit(int units) { return units == 768; }
 
 int matmul_tile_m() { return BM; }
 int matmul_tile_n() { return BN; }
@@ -865,8 +877,11 @@ cudaError_t launch_matmul(const MatmulArgs &a, int dtype, int teams, int units, 
   if (dtype == UPIR_F32 && units == 768) {
     cudaError_t e = cudaFuncSetAttribute(matmul_pair_f32_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, PF_SMEM);
     if (e != cudaSuccess) return e;
+    if (!a.tmap_a2 || !a.tmap_b2) return cudaErrorInvalidValue;   // needs the pre-split lo operands
     matmul_pair_f32_kernel<<<2 * teams, 384, PF_SMEM, s>>>(a, *reinterpret_cast<const CUtensorMap *>(a.tmap_a),
-                                                          *reinterpret_cast<const CUtensorMap *>(a.tmap_b));
+                                                          *reinterpret_cast<const CUtensorMap *>(a.tmap_b),
+                                                          *reinterpret_cast<const CUtensorMap *>(a.tmap_a2),
+                                                          *reinterpret_cast<const CUtensorMap *>(a.tmap_b2));
     return cudaGetLastError();
   }
   if (units != matmul_required_units(dtype)) return cudaErrorInvalidValue;

@@ -177,7 +177,11 @@ struct MatmulArgs {
   unsigned long long *dyn_counter;
   int32_t *trace;               // tile -> team owner (tile granularity) or null
   void *tmap_a, *tmap_b;        // host CUtensorMaps (passed by value at launch)
+  void *tmap_a2, *tmap_b2;      // 3xTF32 pair variant: maps of the pre-split lo operands (a/b = hi)
 };
+// 3xTF32 pre-split of an fp32 operand (pair variant): hi = rna_tf32(x), lo = x - hi.
+cudaError_t launch_tf32_split(const float *src, float *hi, float *lo, int64_t n, int num_sms, cudaStream_t s);
+bool matmul_f32_presplit(int units);
 cudaError_t launch_matmul(const MatmulArgs &a, int dtype, int teams, int units, cudaStream_t s);
 bool matmul_encode_tmaps(void *tma, void *tmb, const void *A, const void *B, int dtype,
                          int64_t M, int64_t N, int64_t K, int64_t lda, int64_t ldb);

@@ -1531,12 +1531,39 @@ static upir_status exec_matmul(upir_spmd s, const upir_loop_desc *l, const upir_
     if ((int64_t)trace->dev_bytes < 3 * nt * 4) return fail(UPIR_E_INVALID, "trace map needs 3*ntiles int32");
     a.trace = (int32_t *)trace->dev;
   }
-  alignas(64) CUtensorMap ta, tb;
-  if (!matmul_encode_tmaps(&ta, &tb, a.A, a.B, b->dtype, rows_here, N, K, lda, ldb))
+  alignas(64) CUtensorMap ta, tb, ta2, tb2;
+  // 3xTF32 on CTA pairs: split A and B into tf32 hi / lo copies first (one
+  // elementwise pass each, stream-ordered scratch), the loop kernel streams
+  // both copies with TMA
+  const bool presplit = b->dtype == UPIR_F32 && matmul_f32_presplit(sd.num_units);
+  float *scratch = nullptr;
+  const int64_t nA = (rows_here - 1) * lda + K, nB = (K - 1) * ldb + N;
+  if (presplit) {
+    const size_t bytes = (size_t)(2 * (nA + nB) + 64) * 4;
+    CUDA_TRY(cudaMallocAsync((void **)&scratch, bytes, c->compute));
+    float *ahi = scratch, *alo = ahi + ((nA + 31) / 32) * 32, *bhi = alo + ((nA + 31) / 32) * 32,
+          *blo = bhi + ((nB + 31) / 32) * 32;
+    cudaError_t e1 = launch_tf32_split((const float *)a.A, ahi, alo, nA, c->num_sms, c->compute);
+    cudaError_t e2 = launch_tf32_split((const float *)a.B, bhi, blo, nB, c->num_sms, c->compute);
+    if (e1 != cudaSuccess || e2 != cudaSuccess) {
+      cudaFreeAsync(scratch, c->compute);
+      return fail(UPIR_E_CUDA, "3xTF32 split launch failed: %s", cudaGetErrorString(e1 != cudaSuccess ? e1 : e2));
+    }
+    c->launches += 2;
+    if (!matmul_encode_tmaps(&ta, &tb, ahi, bhi, b->dtype, rows_here, N, K, lda, ldb) ||
+        !matmul_encode_tmaps(&ta2, &tb2, alo, blo, b->dtype, rows_here, N, K, lda, ldb)) {
+      cudaFreeAsync(scratch, c->compute);
+      return fail(UPIR_E_CUDA, "cuTensorMapEncodeTiled failed for MATMUL operands");
+    }
+    a.tmap_a2 = &ta2;
+    a.tmap_b2 = &tb2;
+  } else if (!matmul_encode_tmaps(&ta, &tb, a.A, a.B, b->dtype, rows_here, N, K, lda, ldb)) {
     return fail(UPIR_E_CUDA, "cuTensorMapEncodeTiled failed for MATMUL operands");
+  }
   a.tmap_a = &ta;
   a.tmap_b = &tb;
   cudaError_t e = launch_matmul(a, b->dtype, sd.num_teams, sd.num_units, c->compute);
+  if (scratch) cudaFreeAsync(scratch, c->compute);   // stream-ordered: after the loop kernel
   if (e != cudaSuccess) return fail(UPIR_E_CUDA, "MATMUL launch failed: %s", cudaGetErrorString(e));
   c->launches++;
   return UPIR_OK;
