@@ -18,7 +18,8 @@
 //                 -> registers -> fp32 C with 256-bit stores (masked at ragged
 //                 edges).
 // bf16 inputs, fp32 accumulation (kind::f16); fp32 inputs via 3xTF32
-// (kind::tf32, warps 8..11 split each staged tile into hi/lo in shared memory).
+// (kind::tf32) over operands pre-split into tf32 hi / lo copies by
+// tf32_split_kernel (warps 8..11 of the 384-unit team have no role).
 // Ragged M/N/K are handled by TMA zero fill (loads) and masks (stores).
 #include "dev_tma.cuh"
 #include "upir_internal.h"
@@ -27,10 +28,11 @@ namespace upir {
 namespace {
 
 // Per-dtype configuration.  BF16: kind::f16, K = 16 per MMA, 64-deep stages.
-// F32 (3xTF32): kind::tf32, K = 8 per MMA, 32-deep stages; each fp32 operand
-// tile is split in shared memory into hi = rna_tf32(x) and lo = x - hi by 4
-// transform warps, and D += lo_a*hi_b + hi_a*lo_b + hi_a*hi_b (small terms
-// first), which keeps the fp32 result within the 1e-5 bar.
+// F32 (3xTF32): kind::tf32, K = 8 per MMA, 32-deep stages; each stage holds
+// the hi = rna_tf32(x) and lo = x - hi copies of the operand tiles (split
+// once in HBM by tf32_split_kernel), and D += lo_a*hi_b + hi_a*lo_b +
+// hi_a*hi_b (small terms first), which keeps the fp32 result within the
+// 1e-5 bar.
 template <int DT>
 struct Cfg;
 template <>
@@ -59,7 +61,7 @@ struct MLayout {
   static constexpr int COPY = A_BYTES + B_BYTES;                  // A + B of one split copy
   static constexpr int STAGE = COPY * C::NSPLIT;
   static constexpr int SMEM = C::STAGES * STAGE + 1024 + 256;
-  static constexpr int TX = COPY;                                 // bytes TMA delivers per stage
+  static constexpr int TX = COPY * C::NSPLIT;                     // bytes TMA delivers per stage
 };
 
 // UMMA shared-memory layout types (descriptor bits [61,64))
@@ -170,7 +172,10 @@ struct TileSeq {
 template <int DT>
 __global__ void __launch_bounds__(Cfg<DT>::THREADS, 1)
     matmul_kernel(const __grid_constant__ MatmulArgs a, const __grid_constant__ CUtensorMap tma,
-                  const __grid_constant__ CUtensorMap tmb) {
+                  const __grid_constant__ CUtensorMap tmb, const __grid_constant__ CUtensorMap tmal,
+                  const __grid_constant__ CUtensorMap tmbl) {
+  // F32: tma / tmb map the pre-split hi operands, tmal / tmbl the lo ones
+  // (tf32_split_kernel); BF16 ignores tmal / tmbl.
   using C = Cfg<DT>;
   using L = MLayout<DT>;
   constexpr int BK = C::BK, STAGES = C::STAGES;
@@ -178,8 +183,7 @@ __global__ void __launch_bounds__(Cfg<DT>::THREADS, 1)
   char *smem = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + STAGES * L::STAGE);
   uint64_t *empty = full + STAGES;
-  uint64_t *ready = empty + STAGES;          // F32: split done
-  uint64_t *tfull = ready + STAGES;
+  uint64_t *tfull = empty + 2 * STAGES;      // (a reserved barrier slot per stage in between)
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -195,7 +199,6 @@ __global__ void __launch_bounds__(Cfg<DT>::THREADS, 1)
     for (int s = 0; s < STAGES; ++s) {
       tma_mbar_init(full + s, 1);
       tma_mbar_init(empty + s, 1);
-      tma_mbar_init(ready + s, 4);
     }
     for (int s = 0; s < 2; ++s) {
       tma_mbar_init(tfull + s, 1);
@@ -217,7 +220,7 @@ __global__ void __launch_bounds__(Cfg<DT>::THREADS, 1)
   seq.init(a.sched, a.chunk, nt);
 
   if (warp == 0) {
-    if (lane == 0) {   // ---------------- TMA producer (raw operand tiles -> copy 0)
+    if (lane == 0) {   // ---------------- TMA producer (operand tiles; F32: hi -> copy 0, lo -> copy 1)
       int stage = 0;
       uint32_t phase = 0;
       for (int64_t tile = seq.next(); tile >= 0; tile = seq.next()) {
@@ -233,6 +236,12 @@ __global__ void __launch_bounds__(Cfg<DT>::THREADS, 1)
 #pragma unroll
           for (int j = 0; j < BN / L::BOXN; ++j)
             tma_load_2d(sb + j * L::B_BOX, &tmb, n0 + L::BOXN * j, kb * BK, full + stage);
+          if constexpr (DT == UPIR_F32) {
+            tma_load_2d(sa + L::COPY, &tmal, kb * BK, m0 - (int)a.row0, full + stage);
+#pragma unroll
+            for (int j = 0; j < BN / L::BOXN; ++j)
+              tma_load_2d(sb + L::COPY + j * L::B_BOX, &tmbl, n0 + L::BOXN * j, kb * BK, full + stage);
+          }
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -252,8 +261,7 @@ __global__ void __launch_bounds__(Cfg<DT>::THREADS, 1)
         tc_fence_after();
         const uint32_t tmem_d = tmem_base + (uint32_t)(acc * BN);
         for (int kb = 0; kb < KB; ++kb) {
-          if constexpr (DT == UPIR_BF16) tma_mbar_wait(full + stage, phase);
-          else tma_mbar_wait(ready + stage, phase);
+          tma_mbar_wait(full + stage, phase);
           tc_fence_after();
           const char *hi = smem + stage * L::STAGE;
 #pragma unroll
@@ -326,40 +334,6 @@ __global__ void __launch_bounds__(Cfg<DT>::THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) tma_mbar_arrive(tempty + acc);
-    }
-  } else if constexpr (DT == UPIR_F32) {
-    if (warp >= 8) {   // ---------------- 3xTF32 split: copy0 <- hi, copy1 <- lo (elementwise)
-      const int tid = threadIdx.x - 256;   // 0..127
-      int stage = 0;
-      uint32_t phase = 0;
-      for (int64_t tile = seq.next(); tile >= 0; tile = seq.next()) {
-        for (int kb = 0; kb < KB; ++kb) {
-          tma_mbar_wait(full + stage, phase);
-          float4 *hi = reinterpret_cast<float4 *>(smem + stage * L::STAGE);
-          float4 *lo = reinterpret_cast<float4 *>(smem + stage * L::STAGE + L::COPY);
-          for (int v = tid; v < L::COPY / 16; v += 128) {
-            const float4 x = hi[v];
-            float4 h, l;
-            h.x = to_tf32(x.x);
-            h.y = to_tf32(x.y);
-            h.z = to_tf32(x.z);
-            h.w = to_tf32(x.w);
-            l.x = __fsub_rn(x.x, h.x);
-            l.y = __fsub_rn(x.y, h.y);
-            l.z = __fsub_rn(x.z, h.z);
-            l.w = __fsub_rn(x.w, h.w);
-            hi[v] = h;
-            lo[v] = l;
-          }
-          tma_fence_proxy();   // generic smem writes -> visible to the tensor-core (async) proxy
-          __syncwarp();
-          if (lane == 0) tma_mbar_arrive(ready + stage);
-          if (++stage == STAGES) {
-            stage = 0;
-            phase ^= 1;
-          }
-        }
-      }
     }
   }
   tc_fence_before();
@@ -626,8 +600,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(384, 1)
   char *smem = reinterpret_cast<char *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~(uintptr_t)1023);
   uint64_t *full = reinterpret_cast<uint64_t *>(smem + PF_STAGES * PF_STAGE);
   uint64_t *empty = full + PF_STAGES;
-  uint64_t *ready = empty + PF_STAGES;
-  uint64_t *tfull = ready + PF_STAGES;
+  uint64_t *tfull = empty + 2 * PF_STAGES;   // (a reserved barrier slot per stage in between)
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_holder = reinterpret_cast<uint32_t *>(tempty + 2);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -830,7 +803,7 @@ cudaError_t launch_tf32_split(const float *src, float *hi, float *lo, int64_t n,
   tf32_split_kernel<<<(int)blocks, 256, 0, s>>>(src, hi, lo, n);
   return cudaGetLastError();
 }
-bool matmul_f32_presplit(int units) { return units == 768; }
+bool matmul_f32_presplit(int) { return true; }   // both fp32 variants stream pre-split operands
 
 int matmul_tile_m() { return BM; }
 int matmul_tile_n() { return BN; }
@@ -861,8 +834,12 @@ static cudaError_t launch_dt(const MatmulArgs &a, int teams, cudaStream_t s) {
   using L = MLayout<DT>;
   cudaError_t e = cudaFuncSetAttribute(matmul_kernel<DT>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
   if (e != cudaSuccess) return e;
-  matmul_kernel<DT><<<teams, Cfg<DT>::THREADS, L::SMEM, s>>>(a, *reinterpret_cast<const CUtensorMap *>(a.tmap_a),
-                                                             *reinterpret_cast<const CUtensorMap *>(a.tmap_b));
+  const CUtensorMap &ta = *reinterpret_cast<const CUtensorMap *>(a.tmap_a);
+  const CUtensorMap &tb = *reinterpret_cast<const CUtensorMap *>(a.tmap_b);
+  if (DT == UPIR_F32 && (!a.tmap_a2 || !a.tmap_b2)) return cudaErrorInvalidValue;   // needs the pre-split lo operands
+  const CUtensorMap &ta2 = DT == UPIR_F32 ? *reinterpret_cast<const CUtensorMap *>(a.tmap_a2) : ta;
+  const CUtensorMap &tb2 = DT == UPIR_F32 ? *reinterpret_cast<const CUtensorMap *>(a.tmap_b2) : tb;
+  matmul_kernel<DT><<<teams, Cfg<DT>::THREADS, L::SMEM, s>>>(a, ta, tb, ta2, tb2);
   return cudaGetLastError();
 }
 
