@@ -31,7 +31,7 @@ struct SLayout {
   static constexpr int GBUF = WR * WC * 4, SBUF = SBLK * (NS > 0 ? NS : 1);
   static constexpr int BUF = (((GBUF > SBUF ? GBUF : SBUF)) + 127) / 128 * 128;
   // pipeline depth (window buffers)
-  static constexpr int NST = 2;   // 3 stages measured slower: they cost a resident CTA per SM
+  static constexpr int NST = 2;   // 3 stages measured slower (they cost resident CTAs per SM)
   static constexpr int SMEM = NST * BUF + 256 + F * F * 4 + 128;
 };
 
@@ -50,8 +50,11 @@ __device__ __forceinline__ int win_off(int row, int col) {
 
 // MAXT: the team size the kernel is compiled for (256 lets the 49 taps stay
 // in registers; 1024 caps registers at 64 for teams of up to 1024 units).
-template <int R, int BM, int BN, int MAXT>
-__global__ void __launch_bounds__(MAXT) stencil_kernel(const __grid_constant__ StencilArgs a,
+// PW: teams of up to 256 units get one extra warp whose lane 0 is a
+// dedicated TMA producer (it executes no iterations); larger teams produce
+// from thread 0 between its own tiles.
+template <int R, int BM, int BN, int MAXT, bool PW = (MAXT <= 256)>
+__global__ void __launch_bounds__(MAXT + (PW ? 32 : 0)) stencil_kernel(const __grid_constant__ StencilArgs a,
                                                        const __grid_constant__ CUtensorMap tmw,
                                                        const __grid_constant__ CUtensorMap tmw8,
                                                        const __grid_constant__ CUtensorMap tms) {
@@ -66,7 +69,9 @@ __global__ void __launch_bounds__(MAXT) stencil_kernel(const __grid_constant__ S
   volatile long long *tile_s = reinterpret_cast<volatile long long *>(smc + NST * L::BUF + 64);
   float *w = reinterpret_cast<float *>(smc + NST * L::BUF + 256);
   __shared__ unsigned s_last;
-  const int units = blockDim.x, u = threadIdx.x;
+  const int units = a.units, u = threadIdx.x;
+  const int cw = (units + 31) >> 5;            // warps holding units
+  const int ptid = PW ? cw * 32 : 0;           // the producer thread
   for (int e = threadIdx.x; e < F * F; e += blockDim.x) w[e] = a.w[e];
   __syncthreads();
   float wr[F * F];   // the taps live in registers for the whole kernel
@@ -126,14 +131,14 @@ __global__ void __launch_bounds__(MAXT) stencil_kernel(const __grid_constant__ S
                   (int)(i0 - R - a.row0), bars + buf);
     }
   };
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == ptid) {
     tma_prefetch_desc(&tmw);
     if constexpr (L::WIDE) tma_prefetch_desc(&tmw8);
     if (strip) tma_prefetch_desc(&tms);
 #pragma unroll
     for (int b = 0; b < NST; ++b) {
       tma_mbar_init(bars + b, 1);
-      tma_mbar_init(bars + NST + b, (units + 31) >> 5);
+      tma_mbar_init(bars + NST + b, cw);
     }
     tma_fence_init();
   }
@@ -152,11 +157,20 @@ __global__ void __launch_bounds__(MAXT) stencil_kernel(const __grid_constant__ S
     else tma_mbar_arrive(bars + slot);
     prod = nx;
   };
-  if (threadIdx.x == 0)
+  if (PW && threadIdx.x >= cw * 32) {
+    // dedicated producer: tile m into slot m % NST once every unit warp has
+    // released that slot's previous tile (m - NST)
+    if (threadIdx.x == ptid)
+      for (int64_t m = 0; prod >= 0; ++m) {
+        const int slot = (int)(m % NST);
+        produce(slot, m >= NST, (unsigned)(((m - NST) / NST) & 1));
+      }
+  } else {
+  if (!PW && threadIdx.x == 0)
     for (int k = 0; k < NST - 1 && prod >= 0; ++k) produce(k, false, 0);
   for (int iter = 0;; ++iter) {
     const int buf = iter % NST;
-    if (threadIdx.x == 0 && prod >= 0) {
+    if (!PW && threadIdx.x == 0 && prod >= 0) {
       // tile of iteration iter + NST - 1 into the buffer iteration iter - 1 used
       const int slot = (iter + NST - 1) % NST;
       produce(slot, iter >= 1, (unsigned)(((iter - 1) / NST) & 1));
@@ -244,7 +258,7 @@ __global__ void __launch_bounds__(MAXT) stencil_kernel(const __grid_constant__ S
         }
       }
     } else if (ic == 4) {
-      for (int k = u; k * 4 < POS; k += units) {
+      for (int k = u; u < units && k * 4 < POS; k += units) {
         const int r = (k * 4) / BN, c = (k * 4) % BN;
         const int64_t i = i0 + r, j = j0 + c;
         if (i < a.lb0 || i >= a.ub0 || j + 3 < a.lb1 || j >= a.ub1) continue;
@@ -288,7 +302,7 @@ __global__ void __launch_bounds__(MAXT) stencil_kernel(const __grid_constant__ S
         }
       }
     } else {
-      for (int64_t k = u; k * ic < POS; k += units) {
+      for (int64_t k = u; u < units && k * ic < POS; k += units) {
         for (int pos = (int)(k * ic); pos < (int)min((int64_t)POS, (k + 1) * ic); ++pos) {
           const int r = pos / BN, c = pos % BN;
           const int64_t i = i0 + r, j = j0 + c;
@@ -309,6 +323,7 @@ __global__ void __launch_bounds__(MAXT) stencil_kernel(const __grid_constant__ S
     __syncwarp();
     if ((threadIdx.x & 31) == 0) tma_mbar_arrive(bars + NST + buf);   // this warp is done with `buf`
   }
+  }   // unit warps
   if (a.sched == SK_DYNAMIC) {
     if (threadIdx.x == 0) {
       __threadfence();
@@ -338,9 +353,12 @@ cudaError_t launch_r(const StencilArgs &a, int teams, int units, cudaStream_t s)
   auto k = (BN == 512 && units == 128)   ? stencil_kernel<R, BM, BN, 128>
            : units <= 256                 ? stencil_kernel<R, BM, BN, 256>
                                           : stencil_kernel<R, BM, BN, 1024>;
+  const int threads = units <= 256 ? (units + 31) / 32 * 32 + 32 : units;   // + the producer warp
   cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
   if (e != cudaSuccess) return e;
-  k<<<teams, units, L::SMEM, s>>>(a, tm, tm8, tms);
+  StencilArgs b = a;
+  b.units = units;
+  k<<<teams, threads, L::SMEM, s>>>(b, tm, tm8, tms);
   return cudaGetLastError();
 }
 

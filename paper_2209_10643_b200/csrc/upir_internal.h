@@ -144,6 +144,7 @@ struct StencilArgs {
   unsigned long long *dyn_counter;
   unsigned int *done;
   int32_t *trace;
+  int32_t units;        // units per team (the launch may add a producer warp)
 };
 bool stencil_supported(int F, int bm, int bn);
 cudaError_t launch_stencil(const StencilArgs &a, int F, int bm, int bn, int teams, int units, cudaStream_t s);
