@@ -176,7 +176,16 @@ extern "C" upir_status upir_init(int cuda_device, const upir_world *world, upir_
     c->compute = (cudaStream_t)world->compute_stream;
     c->copy = (cudaStream_t)world->copy_stream;
   }
-  auto cleanup = [&](upir_status s) { delete c; return s; };
+  auto cleanup = [&](upir_status s) {   // release whatever was created before the failure
+    if (c->slots) cudaFree(c->slots);
+    if (c->done) cudaFree(c->done);
+    if (c->one) cudaFree(c->one);
+    if (c->win) cudaFree(c->win);
+    if (c->own_compute && c->compute) cudaStreamDestroy(c->compute);
+    if (c->own_copy && c->copy) cudaStreamDestroy(c->copy);
+    delete c;
+    return s;
+  };
   if (!c->compute) {
     if (cudaStreamCreateWithFlags(&c->compute, cudaStreamNonBlocking) != cudaSuccess)
       return cleanup(fail(UPIR_E_CUDA, "stream create failed"));
