@@ -33,6 +33,23 @@ __device__ __forceinline__ void tma_mbar_wait(uint64_t *bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
+// Wait with a short back-off between probes: for a producer thread whose
+// wait spans a whole tile of consumer work (its spinning would take issue
+// slots from the consumer warps of its SM sub-partition).
+__device__ __forceinline__ void tma_mbar_wait_backoff(uint64_t *bar, unsigned parity) {
+  for (;;) {
+    unsigned ok;
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        " selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(tma_smem(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    __nanosleep(64);
+  }
+}
 __device__ __forceinline__ void tma_fence_proxy() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
 
 // 2-D tiled TMA load of the box at (c0 = inner/column, c1 = row) into smem.

@@ -24,6 +24,8 @@
 // bumps my counter with a .sys release after the whole sweep).  Interior
 // tiles never wait: the transfer and the neighbour skew overlap the bulk of
 // the sweep.
+#include <cstdlib>
+
 #include "dev_peer.cuh"
 #include "dev_tma.cuh"
 #include "upir_internal.h"
@@ -54,17 +56,17 @@ namespace {
 
 constexpr int align128(int x) { return (x + 127) / 128 * 128; }
 
-template <int BM, int BN>
+template <int BM, int BN, int NST>
 struct JLayout {
   static constexpr int R = BM + 2;
   static constexpr int CEN = align128(R * BN * 4);
   static constexpr int HAL = align128(R * 4 * 4);
   static constexpr int BUF = CEN + 2 * HAL;
   static constexpr int TX = R * BN * 4 + 2 * R * 16;   // bytes per tile load
-  static constexpr int SMEM = 2 * BUF + 128;           // + mbarriers / tile ids
+  static constexpr int SMEM = NST * BUF + 256;         // + mbarriers / tile ids
 };
 
-// Tile iterator of the tile loop (executed by thread 0 only).
+// Tile iterator of the tile loop (executed by the producer thread only).
 struct TileIter {
   int64_t cur = 0, end = 0, k = 0;
   bool started = false;
@@ -94,22 +96,34 @@ __device__ __forceinline__ int64_t next_tile(TileIter &it, const JacobiArgs &a, 
   return it.cur++;
 }
 
-template <int BM, int BN, bool TRACE>
+// NST-deep producer / consumer ring of tile windows without CTA-wide
+// barriers: the producer claims tiles in schedule order and loads tile m into
+// slot m % NST once every unit warp has released the slot's previous tile
+// (empty barrier); the unit warps wait only for their data (full barrier).  A
+// tile id < 0 ends the loop (its full barrier completed by a plain arrive).
+// PW: teams of up to 992 units get one extra warp whose lane 0 is the
+// producer and executes no iterations (reading c34); larger teams produce
+// from thread 0 between its own tiles, NST - 1 tiles ahead.
+template <int BM, int BN, int NST, bool PW, bool TRACE>
 __global__ void __launch_bounds__(1024) jacobi5_kernel(const __grid_constant__ JacobiArgs a,
                                                        const __grid_constant__ CUtensorMap tmc,
                                                        const __grid_constant__ CUtensorMap tmh) {
-  using L = JLayout<BM, BN>;
+  using L = JLayout<BM, BN, NST>;
   extern __shared__ __align__(128) char smem[];
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + 2 * L::BUF);
-  volatile long long *tile_s = reinterpret_cast<volatile long long *>(smem + 2 * L::BUF + 16);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(smem + NST * L::BUF);   // full[NST], empty[NST]
+  // per slot: tile id, first row / column of the tile, interior flag
+  // (written by the producer before the slot's full barrier completes)
+  volatile long long *tile_s = reinterpret_cast<volatile long long *>(smem + NST * L::BUF + 128);   // [NST][4]
   __shared__ unsigned s_last;
   const int64_t nt = a.ntr * a.ntc;
+  const int units = a.units, u = threadIdx.x;
+  const int cw = (units + 31) >> 5;          // warps holding units
+  const int ptid = PW ? cw * 32 : 0;         // the producer thread
   TileIter it;
 
-  auto issue = [&](int64_t tile, int buf) {
-    const int64_t ti = a.ti0 + tile / a.ntc, tj = a.tj0 + tile % a.ntc;
-    const int r0 = (int)(ti * BM - 1 - a.row0);   // local row of the box's first row
-    const int c0 = (int)(tj * BN);
+  auto issue = [&](int64_t i0, int64_t j0, int buf) {
+    const int r0 = (int)(i0 - 1 - a.row0);   // local row of the box's first row
+    const int c0 = (int)j0;
     char *b = smem + buf * L::BUF;
     tma_fence_proxy();
     tma_mbar_expect_tx(bars + buf, L::TX);
@@ -134,120 +148,177 @@ __global__ void __launch_bounds__(1024) jacobi5_kernel(const __grid_constant__ J
     }
     if (waited) fence_proxy_async_global();
   };
-  if (threadIdx.x == 0) {
+  int64_t prod = 0;   // producer: id of the tile it produced last
+  auto produce = [&](int slot, bool wait_empty, unsigned parity) {
+    const int64_t nx = next_tile(it, a, nt);
+    if (wait_empty) {
+      if (PW) tma_mbar_wait_backoff(bars + NST + slot, parity);
+      else tma_mbar_wait(bars + NST + slot, parity);
+    }
+    tile_s[4 * slot] = nx;
+    if (nx >= 0) {
+      // interior tile: every position an iteration, no peer boundary row
+      const int64_t i0 = (a.ti0 + nx / a.ntc) * BM, j0 = (a.tj0 + nx % a.ntc) * BN;
+      const bool fast = !TRACE && a.inner_chunk == 4 && (a.units & 31) == 0 && i0 >= a.lb0 && i0 + BM <= a.ub0 &&
+                        j0 >= a.lb1 && j0 + BN <= a.ub1 && (a.ld & 3) == 0 && ((uintptr_t)a.out & 15) == 0 &&
+                        (!a.win || ((a.send_up_row < i0 || a.send_up_row >= i0 + BM) &&
+                                    (a.send_dn_row < i0 || a.send_dn_row >= i0 + BM)));
+      tile_s[4 * slot + 1] = i0;
+      tile_s[4 * slot + 2] = j0;
+      tile_s[4 * slot + 3] = fast;
+      if (a.win) peer_wait(nx);
+      issue(i0, j0, slot);
+    } else {
+      tma_mbar_arrive(bars + slot);
+    }
+    prod = nx;
+  };
+  if (threadIdx.x == ptid) {
     if (a.win) gen = *reinterpret_cast<volatile unsigned long long *>(a.win + WIN_HALO_GEN);
     tma_prefetch_desc(&tmc);
     tma_prefetch_desc(&tmh);
-    tma_mbar_init(bars + 0, 1);
-    tma_mbar_init(bars + 1, 1);
-    tma_fence_init();
-    const int64_t t0 = next_tile(it, a, nt);
-    tile_s[0] = t0;
-    if (t0 >= 0) {
-      if (a.win) peer_wait(t0);
-      issue(t0, 0);
+#pragma unroll
+    for (int b = 0; b < NST; ++b) {
+      tma_mbar_init(bars + b, 1);
+      tma_mbar_init(bars + NST + b, cw);
     }
+    tma_fence_init();
   }
   __syncthreads();
 
-  const int units = blockDim.x, u = threadIdx.x;
   const int ic = a.inner_chunk;
   constexpr int POS = BM * BN;
-  for (int iter = 0;; ++iter) {
-    const int buf = iter & 1;
-    const int64_t tile = tile_s[buf];
-    if (tile < 0) break;
-    if (threadIdx.x == 0) {
-      const int64_t nx = next_tile(it, a, nt);
-      tile_s[buf ^ 1] = nx;
-      if (nx >= 0) {
-        if (a.win) peer_wait(nx);
-        issue(nx, buf ^ 1);
+  if (PW && threadIdx.x >= cw * 32) {
+    if (threadIdx.x == ptid)
+      for (int64_t m = 0; prod >= 0; ++m) {
+        const int slot = (int)(m % NST);
+        produce(slot, m >= NST, (unsigned)(((m - NST) / NST) & 1));
       }
-    }
-    tma_mbar_wait(bars + buf, (unsigned)((iter >> 1) & 1));
-    const int64_t ti = a.ti0 + tile / a.ntc, tj = a.tj0 + tile % a.ntc;
-    const int64_t i0 = ti * BM, j0 = tj * BN;
-    const float *cen = reinterpret_cast<const float *>(smem + buf * L::BUF);
-    const float *lef = reinterpret_cast<const float *>(smem + buf * L::BUF + L::CEN);
-    const float *rig = reinterpret_cast<const float *>(smem + buf * L::BUF + L::CEN + L::HAL);
-    auto at = [&](int r, int c) -> float {   // smem row r (global row i0-1+r), tile column c in [-1, BN]
-      if (c < 0) return lef[r * 4 + 3];
-      if (c >= BN) return rig[r * 4 + (c - BN)];
-      return cen[r * BN + c];
-    };
-    if (ic == 4) {
-      // static,4 over units: chunk k = 4 consecutive columns of one row
-      for (int k = u; k * 4 < POS; k += units) {
-        const int r = (k * 4) / BN, c = (k * 4) % BN;
-        const int64_t i = i0 + r;
-        if (i < a.lb0 || i >= a.ub0) continue;
-        const int64_t j = j0 + c;
-        if (j + 3 < a.lb1 || j >= a.ub1) continue;
-        const float4 up = *reinterpret_cast<const float4 *>(cen + r * BN + c);
-        const float4 dn = *reinterpret_cast<const float4 *>(cen + (r + 2) * BN + c);
-        const float4 md = *reinterpret_cast<const float4 *>(cen + (r + 1) * BN + c);
-        const float w0 = at(r + 1, c - 1), e3 = at(r + 1, c + 4);
-        float4 o;
-        o.x = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(up.x, dn.x), __fadd_rn(w0, md.y)));
-        o.y = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(up.y, dn.y), __fadd_rn(md.x, md.z)));
-        o.z = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(up.z, dn.z), __fadd_rn(md.y, md.w)));
-        o.w = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(up.w, dn.w), __fadd_rn(md.z, e3)));
-        float *dst = a.out + (i - a.row0) * a.ld + j;
-        // peer mode: my boundary rows also land in the neighbour's halo row
-        float *pdst = (a.win && i == a.send_up_row && a.peer_up) ? a.peer_up + (i - a.peer_up_row0) * a.ld + j
-                                                                  : nullptr;
-        float *pdst2 = (a.win && i == a.send_dn_row && a.peer_dn) ? a.peer_dn + (i - a.peer_dn_row0) * a.ld + j
-                                                                   : nullptr;
-        if (j >= a.lb1 && j + 4 <= a.ub1) {
-          __stcs(reinterpret_cast<float4 *>(dst), o);
-          if (pdst) *reinterpret_cast<float4 *>(pdst) = o;
-          if (pdst2) *reinterpret_cast<float4 *>(pdst2) = o;
-        } else {
-          const float ov[4] = {o.x, o.y, o.z, o.w};
-#pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (j + q >= a.lb1 && j + q < a.ub1) {
-              dst[q] = ov[q];
-              if (pdst) pdst[q] = ov[q];
-              if (pdst2) pdst2[q] = ov[q];
-            }
+  } else {
+    if (!PW && threadIdx.x == 0)
+      for (int k = 0; k < NST - 1 && prod >= 0; ++k) produce(k, false, 0);
+    for (int iter = 0;; ++iter) {
+      const int buf = iter % NST;
+      if (!PW && threadIdx.x == 0 && prod >= 0) {
+        // tile of iteration iter + NST - 1 into the slot iteration iter - 1 used
+        const int slot = (iter + NST - 1) % NST;
+        produce(slot, iter >= 1, (unsigned)(((iter - 1) / NST) & 1));
+      }
+      tma_mbar_wait(bars + buf, (unsigned)((iter / NST) & 1));
+      const int64_t tile = tile_s[4 * buf];
+      if (tile < 0) break;
+      const int64_t i0 = tile_s[4 * buf + 1], j0 = tile_s[4 * buf + 2];
+      const bool fast = tile_s[4 * buf + 3] != 0;
+      const float *cen = reinterpret_cast<const float *>(smem + buf * L::BUF);
+      const float *lef = reinterpret_cast<const float *>(smem + buf * L::BUF + L::CEN);
+      const float *rig = reinterpret_cast<const float *>(smem + buf * L::BUF + L::CEN + L::HAL);
+      auto at = [&](int r, int c) -> float {   // smem row r (global row i0-1+r), tile column c in [-1, BN]
+        if (c < 0) return lef[r * 4 + 3];
+        if (c >= BN) return rig[r * 4 + (c - BN)];
+        return cen[r * BN + c];
+      };
+      // interior tile: static,4 chunks with tile-relative int32 indexing; the
+      // west / east neighbours come from the adjacent lanes' vectors (warp
+      // shuffles), from shared memory only at the warp's edge lanes or the
+      // halo columns
+      if (fast) {
+        float *obase = a.out + (i0 - a.row0) * a.ld + j0;
+        const int ld = (int)a.ld;
+        const int lane = threadIdx.x & 31;
+#pragma unroll 4
+        for (int k = u; k * 4 < POS; k += units) {
+          const int r = (k * 4) / BN, c = (k * 4) % BN;
+          const float *pc = cen + r * BN + c;
+          const float4 up = *reinterpret_cast<const float4 *>(pc);
+          const float4 md = *reinterpret_cast<const float4 *>(pc + BN);
+          const float4 dn = *reinterpret_cast<const float4 *>(pc + 2 * BN);
+          float w0 = __shfl_up_sync(0xffffffffu, md.w, 1);
+          float e3 = __shfl_down_sync(0xffffffffu, md.x, 1);
+          if (c == 0) w0 = lef[(r + 1) * 4 + 3];
+          else if (lane == 0) w0 = pc[BN - 1];
+          if (c + 4 == BN) e3 = rig[(r + 1) * 4];
+          else if (lane == 31) e3 = pc[BN + 4];
+          float4 o;
+          o.x = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(up.x, dn.x), __fadd_rn(w0, md.y)));
+          o.y = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(up.y, dn.y), __fadd_rn(md.x, md.z)));
+          o.z = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(up.z, dn.z), __fadd_rn(md.y, md.w)));
+          o.w = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(up.w, dn.w), __fadd_rn(md.z, e3)));
+          __stcs(reinterpret_cast<float4 *>(obase + (int64_t)r * ld + c), o);
         }
-        if constexpr (TRACE) {
+      } else if (ic == 4) {
+        // static,4 over units: chunk k = 4 consecutive columns of one row
+        for (int k = u; u < units && k * 4 < POS; k += units) {
+          const int r = (k * 4) / BN, c = (k * 4) % BN;
+          const int64_t i = i0 + r;
+          if (i < a.lb0 || i >= a.ub0) continue;
+          const int64_t j = j0 + c;
+          if (j + 3 < a.lb1 || j >= a.ub1) continue;
+          const float4 up = *reinterpret_cast<const float4 *>(cen + r * BN + c);
+          const float4 dn = *reinterpret_cast<const float4 *>(cen + (r + 2) * BN + c);
+          const float4 md = *reinterpret_cast<const float4 *>(cen + (r + 1) * BN + c);
+          const float w0 = at(r + 1, c - 1), e3 = at(r + 1, c + 4);
+          float4 o;
+          o.x = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(up.x, dn.x), __fadd_rn(w0, md.y)));
+          o.y = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(up.y, dn.y), __fadd_rn(md.x, md.z)));
+          o.z = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(up.z, dn.z), __fadd_rn(md.y, md.w)));
+          o.w = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(up.w, dn.w), __fadd_rn(md.z, e3)));
+          float *dst = a.out + (i - a.row0) * a.ld + j;
+          // peer mode: my boundary rows also land in the neighbour's halo row
+          float *pdst = (a.win && i == a.send_up_row && a.peer_up) ? a.peer_up + (i - a.peer_up_row0) * a.ld + j
+                                                                    : nullptr;
+          float *pdst2 = (a.win && i == a.send_dn_row && a.peer_dn) ? a.peer_dn + (i - a.peer_dn_row0) * a.ld + j
+                                                                     : nullptr;
+          if (j >= a.lb1 && j + 4 <= a.ub1) {
+            __stcs(reinterpret_cast<float4 *>(dst), o);
+            if (pdst) *reinterpret_cast<float4 *>(pdst) = o;
+            if (pdst2) *reinterpret_cast<float4 *>(pdst2) = o;
+          } else {
+            const float ov[4] = {o.x, o.y, o.z, o.w};
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
-            if (j + q >= a.lb1 && j + q < a.ub1) {
-              const int64_t idx = tile * POS + r * BN + c + q;
+            for (int q = 0; q < 4; ++q)
+              if (j + q >= a.lb1 && j + q < a.ub1) {
+                dst[q] = ov[q];
+                if (pdst) pdst[q] = ov[q];
+                if (pdst2) pdst2[q] = ov[q];
+              }
+          }
+          if constexpr (TRACE) {
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+              if (j + q >= a.lb1 && j + q < a.ub1) {
+                const int64_t idx = tile * POS + r * BN + c + q;
+                a.trace[idx] = blockIdx.x;
+                a.trace[nt * POS + idx] = u;
+                atomicAdd(a.trace + 2 * nt * POS + idx, 1);
+              }
+          }
+        }
+      } else {
+        // static,ic over units, element by element
+        for (int64_t k = u; u < units && k * ic < POS; k += units) {
+          for (int pos = (int)(k * ic); pos < (int)min((int64_t)POS, (k + 1) * ic); ++pos) {
+            const int r = pos / BN, c = pos % BN;
+            const int64_t i = i0 + r, j = j0 + c;
+            if (i < a.lb0 || i >= a.ub0 || j < a.lb1 || j >= a.ub1) continue;
+            const float v = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(at(r, c), at(r + 2, c)),
+                                                       __fadd_rn(at(r + 1, c - 1), at(r + 1, c + 1))));
+            a.out[(i - a.row0) * a.ld + j] = v;
+            if (a.win) {
+              if (i == a.send_up_row && a.peer_up) a.peer_up[(i - a.peer_up_row0) * a.ld + j] = v;
+              if (i == a.send_dn_row && a.peer_dn) a.peer_dn[(i - a.peer_dn_row0) * a.ld + j] = v;
+            }
+            if constexpr (TRACE) {
+              const int64_t idx = tile * POS + pos;
               a.trace[idx] = blockIdx.x;
               a.trace[nt * POS + idx] = u;
               atomicAdd(a.trace + 2 * nt * POS + idx, 1);
             }
-        }
-      }
-    } else {
-      // static,ic over units, element by element
-      for (int64_t k = u; k * ic < POS; k += units) {
-        for (int pos = (int)(k * ic); pos < (int)min((int64_t)POS, (k + 1) * ic); ++pos) {
-          const int r = pos / BN, c = pos % BN;
-          const int64_t i = i0 + r, j = j0 + c;
-          if (i < a.lb0 || i >= a.ub0 || j < a.lb1 || j >= a.ub1) continue;
-          const float v = __fmul_rn(0.25f, __fadd_rn(__fadd_rn(at(r, c), at(r + 2, c)),
-                                                     __fadd_rn(at(r + 1, c - 1), at(r + 1, c + 1))));
-          a.out[(i - a.row0) * a.ld + j] = v;
-          if (a.win) {
-            if (i == a.send_up_row && a.peer_up) a.peer_up[(i - a.peer_up_row0) * a.ld + j] = v;
-            if (i == a.send_dn_row && a.peer_dn) a.peer_dn[(i - a.peer_dn_row0) * a.ld + j] = v;
-          }
-          if constexpr (TRACE) {
-            const int64_t idx = tile * POS + pos;
-            a.trace[idx] = blockIdx.x;
-            a.trace[nt * POS + idx] = u;
-            atomicAdd(a.trace + 2 * nt * POS + idx, 1);
           }
         }
       }
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) tma_mbar_arrive(bars + NST + buf);   // this warp is done with `buf`
     }
-    __syncthreads();   // buffer `buf` free; tile_s[buf ^ 1] visible
   }
   // peer mode: after the whole sweep (every unit's peer stores fenced), the
   // last team counts the sweep and delivers it to both neighbours
@@ -280,15 +351,51 @@ __global__ void __launch_bounds__(1024) jacobi5_kernel(const __grid_constant__ J
   }
 }
 
+template <int BM, int BN, int NST>
+cudaError_t launch_nst(const JacobiArgs &a, const CUtensorMap &c, const CUtensorMap &h, int teams, int units,
+                       bool trace, cudaStream_t s) {
+  using L = JLayout<BM, BN, NST>;
+  const bool pw = units <= 992;
+  auto k = pw ? jacobi5_kernel<BM, BN, NST, true, false> : jacobi5_kernel<BM, BN, NST, false, false>;
+  if constexpr (NST == 2) {   // traced runs (tests) use the 2-deep ring
+    if (trace) k = pw ? jacobi5_kernel<BM, BN, NST, true, true> : jacobi5_kernel<BM, BN, NST, false, true>;
+  }
+  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
+  if (e != cudaSuccess) return e;
+  JacobiArgs b = a;
+  b.units = units;
+  const int threads = pw ? (units + 31) / 32 * 32 + 32 : units;   // + the producer warp
+  k<<<teams, threads, L::SMEM, s>>>(b, c, h);
+  return cudaGetLastError();
+}
+
+// Ring depth: the deepest ring that keeps at most ~112 KB of tile windows per
+// SM (teams resident per SM x NST x window bytes).  Measured on B200 (C3,
+// tools/debug/jacobi_sweep.py): 3 teams/SM x 2 slots and 2 teams/SM x 3 slots
+// of 16x256 tiles are best; deeper rings at the same residency lose 10-15 %
+// (more reads queued ahead of the write-back stream).
 template <int BM, int BN>
 cudaError_t launch_bmbn(const JacobiArgs &a, const CUtensorMap &c, const CUtensorMap &h, int teams, int units,
                         bool trace, cudaStream_t s) {
-  using L = JLayout<BM, BN>;
-  auto k = trace ? jacobi5_kernel<BM, BN, true> : jacobi5_kernel<BM, BN, false>;
-  cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, L::SMEM);
-  if (e != cudaSuccess) return e;
-  k<<<teams, units, L::SMEM, s>>>(a, c, h);
-  return cudaGetLastError();
+  int nst = 0;
+  if (const char *v = getenv("UPIR_JACOBI_NST")) nst = atoi(v);
+  if (trace) {
+    nst = 2;
+  } else if (nst < 2 || nst > 4) {
+    const int per_sm = teams >= 148 ? (teams + 147) / 148 : 1;   // teams resident per SM (148 SMs)
+    const int smem_budget = 227 * 1024 / per_sm - 1024;
+    nst = 2;
+    for (int d = 4; d > 2; --d) {
+      const int sm = d == 4 ? JLayout<BM, BN, 4>::SMEM : JLayout<BM, BN, 3>::SMEM;
+      if (sm <= smem_budget && per_sm * d * JLayout<BM, BN, 2>::TX <= 112 * 1024) {
+        nst = d;
+        break;
+      }
+    }
+  }
+  if (nst == 4) return launch_nst<BM, BN, 4>(a, c, h, teams, units, trace, s);
+  if (nst == 3) return launch_nst<BM, BN, 3>(a, c, h, teams, units, trace, s);
+  return launch_nst<BM, BN, 2>(a, c, h, teams, units, trace, s);
 }
 
 }  // namespace

@@ -151,7 +151,10 @@ __global__ void __launch_bounds__(MAXT + (PW ? 32 : 0)) stencil_kernel(const __g
   int64_t prod = 0;   // thread 0: id of the tile it produced last
   auto produce = [&](int slot, bool wait_empty, unsigned parity) {
     const int64_t nx = next_tile();
-    if (wait_empty) tma_mbar_wait(bars + NST + slot, parity);
+    if (wait_empty) {
+      if (PW) tma_mbar_wait_backoff(bars + NST + slot, parity);
+      else tma_mbar_wait(bars + NST + slot, parity);
+    }
     tile_s[slot] = nx;
     if (nx >= 0) issue(nx, slot);
     else tma_mbar_arrive(bars + slot);

@@ -118,6 +118,7 @@ struct JacobiArgs {
   unsigned long long *dyn_counter;
   unsigned int *done;
   int32_t *trace;       // [team | unit | hits] planes of ntiles*BM*BN int32, or null
+  int32_t units;        // num_units (set by the launcher; the CTA may carry a producer warp)
   // fused halo exchange with ranks r-1 / r+1 (peer mode): null win = off
   unsigned long long *win;          // local peer window
   unsigned long long *win_up, *win_dn;  // neighbours' windows (null at the ends)

@@ -31,6 +31,33 @@ __global__ void __launch_bounds__(256) k(float *out, const float *win, float wp0
   out[blockIdx.x * blockDim.x + threadIdx.x] = s;
 }
 
+// Packed FFMA2 (fma.rn.f32x2, sm_100): 16 pair accumulators = 32 FMA lanes per
+// iteration half, same dependency depth as the scalar forms.
+__global__ void __launch_bounds__(256) k2(float *out, const float *win, int iters) {
+  unsigned long long w01, w23, a[16];
+  asm("mov.b64 %0, {%1,%2};" : "=l"(w01) : "f"(win[0]), "f"(win[1]));
+  asm("mov.b64 %0, {%1,%2};" : "=l"(w23) : "f"(win[2]), "f"(win[3]));
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    const float v = threadIdx.x * 1e-3f + i;
+    asm("mov.b64 %0, {%1,%2};" : "=l"(a[i]) : "f"(v), "f"(v + 0.5f));
+  }
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(a[i]) : "l"(w01), "l"(w23));
+#pragma unroll
+    for (int i = 0; i < 16; ++i) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(a[i]) : "l"(w23), "l"(w01));
+  }
+  float s = 0;
+#pragma unroll
+  for (int i = 0; i < 16; ++i) {
+    float x, y;
+    asm("mov.b64 {%0,%1}, %2;" : "=f"(x), "=f"(y) : "l"(a[i]));
+    s += x + y;
+  }
+  out[blockIdx.x * blockDim.x + threadIdx.x] = s;
+}
+
 int main() {
   float *out, *win;
   cudaMalloc(&out, 148 * 8 * 256 * 4);
@@ -55,6 +82,20 @@ int main() {
       printf("form %d (%s) ctas/SM %d: %.2f TFLOP/s fp32\n", form, form == 0 ? "3-reg" : form == 1 ? "param" : "imm",
              bps, 2 * fma / ms / 1e9);
     }
+  }
+  for (int bps = 2; bps <= 8; bps *= 2) {
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    k2<<<148 * bps, 256>>>(out, win, 100);
+    cudaEventRecord(e0);
+    k2<<<148 * bps, 256>>>(out, win, iters);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms;
+    cudaEventElapsedTime(&ms, e0, e1);
+    double fma = 148.0 * bps * 256 * iters * 64;
+    printf("form 3 (ffma2 packed) ctas/SM %d: %.2f TFLOP/s fp32\n", bps, 2 * fma / ms / 1e9);
   }
   return 0;
 }
