@@ -890,7 +890,7 @@ def bench_jacobi32k(args, U, ctx, stream, barrier, rank, world, peaks, peak_src,
                                f"{bm}x{bn} static,1 over {teams} teams",
                    "parallelism": f"dp{world}", "l2": "2 x 4 GiB grids >> L2"},
         "roofline": {"bound": "hbm", "achieved": per_rank_gbs, "peak": peak, "unit": "GB/s",
-                     "frac": per_rank_gbs / peak, "traffic": ncu_traffic("jacobi"),
+                     "frac": per_rank_gbs / peak, "traffic": ncu_traffic("jacobi32k"),
                      "kernel": f"jacobi5_kernel<{bm},{bn}>", "peak_source": peak_src},
         "clocks": clocks, "gpu_launches": launches,
         "e2e": {"value": None, "unit": "GLUP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

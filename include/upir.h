@@ -85,8 +85,9 @@ upir_status upir_comm_unique_id(void *out128);
 /* The context's streams: which = 0 compute, 1 copy. */
 upir_status upir_ctx_stream(upir_ctx ctx, int which, uintptr_t *out);
 /* Counters since upir_init: out[0] H2D bytes enqueued by maps/updates,
- * out[1] D2H bytes, out[2] live maps, out[3] device launches (kernels and
- * graph launches) issued by this context. */
+ * out[1] D2H bytes, out[2] live maps, out[3] library kernels launched by this
+ * context (a graph launch counts the kernels captured into the graph; a
+ * capture itself launches nothing). */
 upir_status upir_ctx_stats(upir_ctx ctx, int64_t out[4]);
 
 /* ---- upir.data: mapping, movement, memory management (Figs. 5-6) -------

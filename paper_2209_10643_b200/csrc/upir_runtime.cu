@@ -88,6 +88,7 @@ struct upir_event_s {
 struct upir_graph_s {
   cudaGraph_t graph;
   cudaGraphExec_t exec;
+  int64_t kernels = 0;   // library kernels captured (counted per graph launch)
 };
 
 struct upir_spmd_s {
@@ -129,6 +130,7 @@ struct upir_ctx_s {
   void *peer_win_base[WIN_MAX_RANKS] = {};
   // statistics
   int64_t h2d_bytes = 0, d2h_bytes = 0, launches = 0;
+  int64_t launches_at_capture = 0;
 };
 
 static upir_status sticky_check(upir_ctx c) {
@@ -1771,6 +1773,7 @@ extern "C" upir_status upir_graph_begin(upir_ctx c) {
   cudaSetDevice(c->device);
   CUDA_TRY(cudaStreamBeginCapture(c->compute, cudaStreamCaptureModeRelaxed));
   c->capturing = true;
+  c->launches_at_capture = c->launches;
   return UPIR_OK;
 }
 
@@ -1779,6 +1782,9 @@ extern "C" upir_status upir_graph_end(upir_ctx c, upir_graph *out) {
   if (!c->capturing) return fail(UPIR_E_INVALID, "not capturing");
   c->capturing = false;
   upir_graph g = new upir_graph_s();
+  // captured kernels did not run: they count when the graph is launched
+  g->kernels = c->launches - c->launches_at_capture;
+  c->launches = c->launches_at_capture;
   cudaError_t e = cudaStreamEndCapture(c->compute, &g->graph);
   if (e != cudaSuccess) { delete g; return fail(UPIR_E_CUDA, "end capture: %s", cudaGetErrorString(e)); }
   e = cudaGraphInstantiate(&g->exec, g->graph, 0);
@@ -1795,7 +1801,7 @@ extern "C" upir_status upir_graph_launch(upir_ctx c, upir_graph g) {
   if (!c || !g) return fail(UPIR_E_INVALID, "bad argument");
   cudaSetDevice(c->device);
   CUDA_TRY(cudaGraphLaunch(g->exec, c->compute));
-  c->launches++;
+  c->launches += g->kernels;
   return UPIR_OK;
 }
 

@@ -89,7 +89,11 @@ def main():
             if rb is not None and wb is not None:
                 lines.append(f"dram_traffic_bytes = {rb + wb:.0f}")
                 key = None
-                if "stream_loop_kernel<0" in kname:
+                if name in ("jacobi32k", "reduce34"):
+                    key = {"jacobi32k": "jacobi32k", "reduce34": "reduce_i64_1"}[name]
+                elif "matmul_pair_f32" in kname:
+                    key = "matmul_pair_f32"
+                elif "stream_loop_kernel<0" in kname:
                     key = "reduce_i64"
                 elif "stream_loop_kernel<1" in kname:
                     key = "reduce_f32"
