@@ -578,8 +578,11 @@ def bench_stencil7(args, U, ctx, stream, peaks, peak_src):
         U.upir_synth_fill(ctx, ma, 4, 5, 0, n, n)
         U.upir_synth_fill(ctx, mb, 4, 5, 0, n, n)
         lups = (n - 6) ** 2
-        for teams, units, tile in ((444, 128, (8, 512)), (592, 256, (16, 128)), (296, 128, (16, 512)),
-                                   (888, 64, (8, 256))):
+        cfgs = ((444, 128, (8, 512)), (592, 256, (16, 128)), (296, 128, (16, 512)), (888, 64, (8, 256)))
+        if os.environ.get("UPIR_STENCIL_CFGS"):   # sweep hook: "TEAMSxUNITS:BMxBN,..."
+            cfgs = [tuple(int(x) for x in g.split(":")[0].split("x")) + (tuple(int(x) for x in g.split(":")[1].split("x")),)
+                    for g in os.environ["UPIR_STENCIL_CFGS"].split(",")]
+        for teams, units, tile in cfgs:
             s = U.upir_spmd_launch(ctx, U.spmd_desc(teams, units))
             loop = U.loop_desc([3, 3], [n - 3, n - 3], tile=list(tile), chunk=1, distribute=U.DIST_TEAMS,
                                inner_chunk=4)
