@@ -17,7 +17,8 @@ def main():
     out = os.path.join(ROOT, "build", "var")
     os.makedirs(out, exist_ok=True)
     obj = os.path.join(out, f"{os.path.basename(src)}.{name}.o")
-    subprocess.run([B.NVCC] + B._flags() + defs + ["-c", os.path.join(B.CSRC, src), "-o", obj], check=True)
+    path = os.environ.get("SRC_OVERRIDE", os.path.join(B.CSRC, src))   # e.g. an older revision of the file
+    subprocess.run([B.NVCC] + B._flags() + ["-I" + B.CSRC] + defs + ["-c", path, "-o", obj], check=True)
     objs = [os.path.join(B.BUILD, f) for f in sorted(os.listdir(B.BUILD))
             if f.endswith(".o") and f != os.path.basename(src) + ".o"] + [obj]
     nd = B.nccl_dir()
