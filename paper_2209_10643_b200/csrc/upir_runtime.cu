@@ -976,6 +976,20 @@ static upir_status elem_view(upir_map m, int64_t esz, ElemView &v) {
   return UPIR_OK;
 }
 
+// L2 promotion of the 4-column halo boxes of the Jacobi window (16 B per
+// row).  64 B measured best (ncu, C5b 32768^2 sweep: DRAM reads 4.95 GB with
+// 256 B promotion -> 4.70 GB, +2.5 % GLUP/s; each missed 16-B halo segment
+// otherwise pulls 256 B).  Experiment hook UPIR_JACOBI_HALO_PROMO = 0 none,
+// 1 64 B, 2 128 B, 3 256 B.
+static CUtensorMapL2promotion jacobi_halo_promotion() {
+  const char *v = getenv("UPIR_JACOBI_HALO_PROMO");
+  const int k = v ? atoi(v) : 1;
+  return k == 0 ? CU_TENSOR_MAP_L2_PROMOTION_NONE
+         : k == 1 ? CU_TENSOR_MAP_L2_PROMOTION_L2_64B
+         : k == 2 ? CU_TENSOR_MAP_L2_PROMOTION_L2_128B
+                  : CU_TENSOR_MAP_L2_PROMOTION_L2_256B;
+}
+
 static const char *env_path() {
   const char *p = getenv("UPIR_PATH");
   return p ? p : "";
@@ -1340,7 +1354,7 @@ static upir_status exec_jacobi(upir_spmd s, const upir_loop_desc *l, const upir_
   if (!encode_tmap_2d(&tmc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, base, (uint64_t)ld, (uint64_t)rows_local, (uint64_t)ld * 4,
                       (uint32_t)bn, (uint32_t)(bm + 2), CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B) ||
       !encode_tmap_2d(&tmh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, base, (uint64_t)ld, (uint64_t)rows_local, (uint64_t)ld * 4, 4,
-                      (uint32_t)(bm + 2), CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B))
+                      (uint32_t)(bm + 2), CU_TENSOR_MAP_SWIZZLE_NONE, jacobi_halo_promotion()))
     return fail(UPIR_E_CUDA, "cuTensorMapEncodeTiled failed for the JACOBI5 input");
   cudaError_t e = launch_jacobi_tma(a, &tmc, &tmh, sd.num_teams, sd.num_units, bm, bn, trace != nullptr, c->compute);
   if (e != cudaSuccess) return fail(UPIR_E_CUDA, "JACOBI5 launch failed: %s", cudaGetErrorString(e));
