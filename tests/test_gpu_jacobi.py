@@ -189,3 +189,41 @@ def test_jacobi_full_size_windows(ctx):
         assert np.abs(got - ref).max() <= 1e-5 * max(1.0, np.abs(ref).max()), (r0, c0)
     U.upir_data_unmap(ctx, mb)
     U.upir_data_unmap(ctx, ma)
+
+
+@pytest.mark.parametrize("teams,units,tile", [(148, 256, (16, 256)), (444, 256, (16, 256)), (9, 128, (32, 128))])
+def test_jacobi_ring_depths_identical(ctx, monkeypatch, teams, units, tile):
+    """The window ring depth (2, 3, 4 slots; launcher's choice = 0) is a
+    staging choice only: results are bit-identical and match the oracle."""
+    g = synth.jacobi_init(203, 1028)
+    outs = []
+    for nst in ("0", "2", "3", "4"):
+        monkeypatch.setenv("UPIR_JACOBI_NST", nst)
+        out, _ = jacobi_gpu(ctx, g, 4, teams=teams, units=units, tile=tile)
+        outs.append(out)
+    assert rel(outs[0], oracle.jacobi5(g, 4)) <= 1e-5
+    for o in outs[1:]:
+        assert (o == outs[0]).all()
+
+
+@pytest.mark.parametrize("teams,units", [(5, 100), (3, 33), (2, 1000)])
+def test_jacobi_ragged_team_sizes(ctx, teams, units):
+    """Team sizes that are not a multiple of the warp (the producer warp sits
+    after the last partial warp; the units' interior fast path needs whole
+    warps, so these run the checked path) -- and > 992 units (no producer
+    warp: thread 0 produces between its own tiles)."""
+    g = synth.jacobi_init(97, 516)
+    out, tr = jacobi_gpu(ctx, g, 2, teams=teams, units=units, tile=(16, 256), trace=True)
+    assert rel(out, oracle.jacobi5(g, 2)) <= 1e-5
+    team, unit, hits = tr.reshape(3, -1)
+    assert (unit[hits > 0] < units).all() and (team[hits > 0] < teams).all()
+
+
+def test_jacobi_interior_fast_path_matches_checked(ctx):
+    """Interior tiles (lean path: shuffled west / east neighbours) and the
+    checked path (forced by a trace run) give bit-identical grids."""
+    g = synth.jacobi_init(300, 1100)
+    fast, _ = jacobi_gpu(ctx, g, 1, teams=37, units=256, tile=(16, 256))
+    checked, _ = jacobi_gpu(ctx, g, 1, teams=37, units=256, tile=(16, 256), trace=True)
+    assert (fast == checked).all()
+    assert rel(fast, oracle.jacobi5(g, 1)) <= 1e-5
