@@ -297,7 +297,28 @@ __device__ void direct_run(const StreamArgs &a, const LaneWork &w, Acc<BODY, NRE
     if (lim - VEC - w.lo0 >= 0) nfull = min(w.nk, (lim - VEC - w.lo0) / w.kstride + 1);
     const int64_t e0 = a.lb + w.lo0;
     for (; j + 4 <= nfull; j += 4) {
-      if constexpr (BODY == SB_AXPY || TRACE) {
+      if constexpr (BODY == SB_AXPY && !TRACE) {
+        // the 4 chunks' x and y vectors are all loaded before any y' store
+        // (the chunks are distinct elements, so this holds even when x and y
+        // alias): 8 loads in flight per unit instead of 2
+        const float *px = reinterpret_cast<const float *>(a.in0);
+        float *py = reinterpret_cast<float *>(a.out);
+        float4 xv[4], yv[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          xv[q] = __ldcs(reinterpret_cast<const float4 *>(px + e0 + (j + q) * w.kstride));
+          yv[q] = __ldcs(reinterpret_cast<const float4 *>(py + e0 + (j + q) * w.kstride));
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          yv[q].x = __fmaf_rn(a.alpha, xv[q].x, yv[q].x);
+          yv[q].y = __fmaf_rn(a.alpha, xv[q].y, yv[q].y);
+          yv[q].z = __fmaf_rn(a.alpha, xv[q].z, yv[q].z);
+          yv[q].w = __fmaf_rn(a.alpha, xv[q].w, yv[q].w);
+          __stcs(reinterpret_cast<float4 *>(py + e0 + (j + q) * w.kstride), yv[q]);
+          acc_f4(acc, yv[q], true, true, true, true);
+        }
+      } else if constexpr (BODY == SB_AXPY || TRACE) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) direct_vec<BODY, NRED, TRACE>(a, e0 + (j + q) * w.kstride, acc, team, unit);
       } else if constexpr (BODY == SB_RED_I64) {
