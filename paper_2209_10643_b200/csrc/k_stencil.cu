@@ -66,7 +66,9 @@ __global__ void __launch_bounds__(MAXT + (PW ? 32 : 0)) stencil_kernel(const __g
   constexpr int NST = L::NST;
   uint64_t *bars = reinterpret_cast<uint64_t *>(smc + NST * L::BUF);
   // bars: full[NST] (TMA landed / end marker), empty[NST] (every warp done with the buffer)
-  volatile long long *tile_s = reinterpret_cast<volatile long long *>(smc + NST * L::BUF + 64);
+  // per slot: tile id, first row, first column (written by the producer
+  // before the slot's full barrier completes)
+  volatile long long *tile_s = reinterpret_cast<volatile long long *>(smc + NST * L::BUF + 64);   // [NST][3]
   float *w = reinterpret_cast<float *>(smc + NST * L::BUF + 256);
   __shared__ unsigned s_last;
   const int units = a.units, u = threadIdx.x;
@@ -107,8 +109,7 @@ __global__ void __launch_bounds__(MAXT + (PW ? 32 : 0)) stencil_kernel(const __g
   // strip path: static,4 with BN = 4 * units -- unit u owns columns 4u..4u+3
   // (traced runs take the generic static,4 path: same position -> unit map)
   const bool strip = a.inner_chunk == 4 && BN == 4 * units && BN % 128 == 0 && MAXT <= 256 && !a.trace;
-  auto issue = [&](int64_t tile, int buf) {
-    const int64_t i0 = (a.ti0 + tile / a.ntc) * BM, j0 = (a.tj0 + tile % a.ntc) * BN;
+  auto issue = [&](int64_t i0, int64_t j0, int buf) {
     tma_fence_proxy();
     if (strip) {
       tma_mbar_expect_tx(bars + buf, L::STX);
@@ -155,9 +156,16 @@ __global__ void __launch_bounds__(MAXT + (PW ? 32 : 0)) stencil_kernel(const __g
       if (PW) tma_mbar_wait_backoff(bars + NST + slot, parity);
       else tma_mbar_wait(bars + NST + slot, parity);
     }
-    tile_s[slot] = nx;
-    if (nx >= 0) issue(nx, slot);
-    else tma_mbar_arrive(bars + slot);
+    tile_s[3 * slot] = nx;
+    if (nx >= 0) {
+      // the tile's origin, computed once here (the unit warps read it)
+      const int64_t i0 = (a.ti0 + nx / a.ntc) * BM, j0 = (a.tj0 + nx % a.ntc) * BN;
+      tile_s[3 * slot + 1] = i0;
+      tile_s[3 * slot + 2] = j0;
+      issue(i0, j0, slot);
+    } else {
+      tma_mbar_arrive(bars + slot);
+    }
     prod = nx;
   };
   if (PW && threadIdx.x >= cw * 32) {
@@ -179,10 +187,10 @@ __global__ void __launch_bounds__(MAXT + (PW ? 32 : 0)) stencil_kernel(const __g
       produce(slot, iter >= 1, (unsigned)(((iter - 1) / NST) & 1));
     }
     tma_mbar_wait(bars + buf, (unsigned)((iter / NST) & 1));
-    const int64_t tile = tile_s[buf];
+    const int64_t tile = tile_s[3 * buf];
     if (tile < 0) break;
     const float *win = reinterpret_cast<const float *>(smc + buf * L::BUF);
-    const int64_t i0 = (a.ti0 + tile / a.ntc) * BM, j0 = (a.tj0 + tile % a.ntc) * BN;
+    const int64_t i0 = tile_s[3 * buf + 1], j0 = tile_s[3 * buf + 2];
     const int ic = a.inner_chunk;
     if (strip) {
       // static,4 with BN = 4 * units: unit u owns the 4-column strip c = 4u of
