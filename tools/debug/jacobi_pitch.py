@@ -23,7 +23,7 @@ for pad in [int(p) for p in os.environ.get("PADS", "0,32,64,128,1024").split(","
     U.upir_synth_fill(ctx, mb, 4, 5, 0, n, ld)
     loop = U.loop_desc([1, 1], [n - 1, n - 1], tile=[16, 256], policy=U.SCHED_STATIC, chunk=1,
                        distribute=U.DIST_TEAMS, inner_chunk=4)
-    s = U.upir_spmd_launch(ctx, U.spmd_desc(444, 256))
+    s = U.upir_spmd_launch(ctx, U.spmd_desc(int(os.environ.get("TEAMS", 444)), 256))
     bodies = [U.body(U.BODY_JACOBI5, U.F32, in0=ma, out=mb, ld=(ld, 0, 0), dims=(n, 0, 0)),
               U.body(U.BODY_JACOBI5, U.F32, in0=mb, out=ma, ld=(ld, 0, 0), dims=(n, 0, 0))]
     U.upir_graph_begin(ctx)
