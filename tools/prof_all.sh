@@ -13,7 +13,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:matm
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:matmul_kernel -s 6 -c 1 -o gpurun_out/prof_matmul_f32 -f $B > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:matmul_pair_f32 -s 2 -c 1 -o gpurun_out/prof_matmul_pair_f32 -f $B > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:jacobi5 -s 5 -c 1 -o gpurun_out/prof_jacobi32k -f python bench.py --workload jacobi32k --steps 1 --warmup 0 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:stream_loop -s 2 -c 1 -o gpurun_out/prof_reduce34 -f python bench.py --workload reduce34 --steps 1 --warmup 0 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:matvec -s 3 -c 1 -o gpurun_out/prof_matvec -f $B > /dev/null 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:stencil_kernel -s 55 -c 1 -o gpurun_out/prof_stencil7 -f $B > /dev/null 2>&1
 UPIR_PROFILES_OUT=gpurun_out/profiles python tools/ncu_summary.py $TAG gpurun_out/prof_*.ncu-rep

@@ -8,4 +8,9 @@ timeout 900 $CS --tool memcheck --error-exitcode 9 python -m pytest tests/test_g
 timeout 900 $CS --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_matmul.py -q -x -k "matmul_parity and 256-512 or f32_parity and 200" > gpurun_out/san_mem_mm.log 2>&1; echo memcheck matmul rc=$?
 timeout 900 $CS --tool racecheck --racecheck-report all --error-exitcode 9 python -m pytest tests/test_gpu_jacobi.py tests/test_gpu_stencil.py tests/test_gpu_matvec.py -q -x -k "parity_tiles and 70-300 and 32-256 or stencil_parity and 70-300 and 7 or matvec_parity and 148 and 257" > gpurun_out/san_race.log 2>&1; echo racecheck rc=$?
 timeout 900 $CS --tool synccheck --error-exitcode 9 python -m pytest tests/test_gpu_stream.py tests/test_gpu_matvec.py -q -x -k "test_reduce_i64_parity and 3-37 and direct or matvec_parity and 5-96" > gpurun_out/san_sync.log 2>&1; echo synccheck rc=$?
+# the Jacobi window ring (producer warp, 2-4 slots, ragged teams) and the stencil strip ring
+J="ring_depths and 9-128 or ragged_team_sizes or interior_fast_path or strip_tiles"
+timeout 900 $CS --tool racecheck --racecheck-report all --error-exitcode 9 python -m pytest tests/test_gpu_jacobi.py tests/test_gpu_stencil.py -q -x -k "$J" > gpurun_out/san_race_ring.log 2>&1; echo racecheck ring rc=$?
+timeout 900 $CS --tool synccheck --error-exitcode 9 python -m pytest tests/test_gpu_jacobi.py tests/test_gpu_stencil.py -q -x -k "$J" > gpurun_out/san_sync_ring.log 2>&1; echo synccheck ring rc=$?
+timeout 900 $CS --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_jacobi.py tests/test_gpu_stencil.py -q -x -k "$J" > gpurun_out/san_mem_ring.log 2>&1; echo memcheck ring rc=$?
 for f in gpurun_out/san_*.log; do echo "== $f"; grep -E "ERROR SUMMARY|passed|failed" $f | tail -3; done
