@@ -520,6 +520,13 @@ def bench_axpy(args, U, ctx, stream, peaks, peak_src):
             "bound": "hbm", **out}
 
 
+def jacobi_tile_sched():
+    """Tile-loop schedule of the Jacobi lines: (chunk, tile order); chunk 0 =
+    static block, 'col' = UPIR_TILE_COLMAJOR (reading c35).  Env overrides
+    UPIR_JACOBI_CHUNK / UPIR_JACOBI_ORDER are sweep hooks."""
+    return int(os.environ.get("UPIR_JACOBI_CHUNK", 1)), os.environ.get("UPIR_JACOBI_ORDER", "row")
+
+
 def bench_jacobi(args, U, ctx, stream, peaks, peak_src, ny=8192, nx=8192, S=100):
     """C3: 2-D Jacobi 5-point 8192^2 fp32, 100 sweeps as one CUDA graph, tiles
     32x256 static,1 over 296 teams, intra-tile static,4 over 256 units."""
@@ -533,8 +540,9 @@ def bench_jacobi(args, U, ctx, stream, peaks, peak_src, ny=8192, nx=8192, S=100)
     # 16x256 tiles, 3 teams per SM: measured best of the r01 sweep (tools/sweep_jacobi_axpy.sh)
     teams = int(os.environ.get("UPIR_JACOBI_TEAMS", 444))
     bm, bn = (int(v) for v in os.environ.get("UPIR_JACOBI_TILE", "16x256").split("x"))
-    loop = U.loop_desc([1, 1], [ny - 1, nx - 1], tile=[bm, bn], policy=U.SCHED_STATIC, chunk=1,
-                       distribute=U.DIST_TEAMS, inner_chunk=4)
+    chunk, order = jacobi_tile_sched()
+    loop = U.loop_desc([1, 1], [ny - 1, nx - 1], tile=[bm, bn], policy=U.SCHED_STATIC, chunk=chunk,
+                       distribute=U.DIST_TEAMS, inner_chunk=4, flags=U.TILE_COLMAJOR if order == "col" else 0)
     s = U.upir_spmd_launch(ctx, U.spmd_desc(teams, 256))
     bodies = [U.body(U.BODY_JACOBI5, U.F32, in0=ma, out=mb, ld=(nx, 0, 0), dims=(ny, 0, 0)),
               U.body(U.BODY_JACOBI5, U.F32, in0=mb, out=ma, ld=(nx, 0, 0), dims=(ny, 0, 0))]
@@ -846,8 +854,9 @@ def bench_jacobi32k(args, U, ctx, stream, barrier, rank, world, peaks, peak_src,
         U.upir_peer_share(ctx, [ma, mb])
     teams = int(os.environ.get("UPIR_JACOBI_TEAMS", 444))
     bm, bn = (int(v) for v in os.environ.get("UPIR_JACOBI_TILE", "16x256").split("x"))
-    loop = U.loop_desc([1, 1], [n - 1, n - 1], tile=[bm, bn], policy=U.SCHED_STATIC, chunk=1,
-                       distribute=U.DIST_TEAMS, inner_chunk=4)
+    chunk, order = jacobi_tile_sched()
+    loop = U.loop_desc([1, 1], [n - 1, n - 1], tile=[bm, bn], policy=U.SCHED_STATIC, chunk=chunk,
+                       distribute=U.DIST_TEAMS, inner_chunk=4, flags=U.TILE_COLMAJOR if order == "col" else 0)
     s = U.upir_spmd_launch(ctx, U.spmd_desc(teams, 256, U.TARGET_CLUSTER))
     bodies = [(ma, U.body(U.BODY_JACOBI5, U.F32, in0=ma, out=mb, ld=(n, 0, 0), dims=(n, 0, 0))),
               (mb, U.body(U.BODY_JACOBI5, U.F32, in0=mb, out=ma, ld=(n, 0, 0), dims=(n, 0, 0)))]

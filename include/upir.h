@@ -239,6 +239,14 @@ typedef enum {
 typedef enum { UPIR_DIST_TEAMS = 1, UPIR_DIST_UNITS = 2, UPIR_DIST_TEAMS_UNITS = 3 } upir_distribute;
 
 #define UPIR_NOWAIT 1u  /* no implicit end barrier: the host does not wait */
+/* UPIR_TILE_COLMAJOR (tiled JACOBI5 nests; reading c35 of DESIGN.md): the
+ * tile loop enumerates the tiles column-major -- tile id = (tj - tj0) * ntr +
+ * (ti - ti0) -- instead of row-major (reading c24).  The paper's tiling
+ * fixes no order; with schedule(static) a team then owns a
+ * vertical run of tiles and re-reads its own previous tile's boundary row
+ * from L2 instead of a row another team fetched.  Trace records index tiles
+ * by this id.  Other bodies: UPIR_E_UNSUPPORTED. */
+#define UPIR_TILE_COLMAJOR 4u
 /* UPIR_WORLD_REDUCE: the loop's reductions are combined over all ranks as part
  * of the loop (Fig. 7 'allreduce' with ranks as units fused into the loop's
  * end barrier): every rank receives

@@ -65,6 +65,7 @@ def lib():
             "orc_matmul_rows": (i32, [i64, i64, i64, vp, vp, vp, i64, vp]),
             "orc_tile_owner": (i32, [i64, i64, i64, i64, i32, i64, i64, vp]),
             "orc_tiled_owner": (i64, [i64, i64, i64, i64, i64, i64, i32, i64, i64, i64, i64, vp, vp]),
+            "orc_tiled_owner_order": (i64, [i64, i64, i64, i64, i64, i64, i32, i64, i64, i64, i64, i32, vp, vp]),
             "orc_matvec": (i32, [i64, i64, i64, i64, i64, vp, vp, vp, vp]),
             "orc_stencil2d": (i32, [i64, i64, i64, i64, vp, vp, vp]),
             "orc_reduce_stream": (i32, [i32, i32, ctypes.c_uint64, i64, i64, vp, vp]),
@@ -126,14 +127,16 @@ def tile_owner(R, C, tm, tn, policy, chunk, p):
     return owner[:nt]
 
 
-def tiled_owner(lb0, ub0, lb1, ub1, BM, BN, policy, chunk, p_teams, ic, units):
-    """(team, unit) of every box position of a tiled collapse(2) nest (c24)."""
+def tiled_owner(lb0, ub0, lb1, ub1, BM, BN, policy, chunk, p_teams, ic, units, colmajor=False):
+    """(team, unit) of every box position of a tiled collapse(2) nest (c24);
+    colmajor: tile ids enumerate the tile grid column-major (c35)."""
     if ub0 <= lb0 or ub1 <= lb1:
         return np.zeros(0, np.int64), np.zeros(0, np.int64)
     nt = (((ub0 + BM - 1) // BM) - lb0 // BM) * (((ub1 + BN - 1) // BN) - lb1 // BN)
     team = np.zeros(nt * BM * BN, dtype=np.int64)
     unit = np.zeros(nt * BM * BN, dtype=np.int64)
-    r = lib().orc_tiled_owner(lb0, ub0, lb1, ub1, BM, BN, policy, chunk, p_teams, ic, units, _p(team), _p(unit))
+    r = lib().orc_tiled_owner_order(lb0, ub0, lb1, ub1, BM, BN, policy, chunk, p_teams, ic, units,
+                                    1 if colmajor else 0, _p(team), _p(unit))
     if r != nt:
         raise ValueError("tiled_owner failed")
     return team, unit

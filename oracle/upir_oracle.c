@@ -453,9 +453,23 @@ int orc_tile_owner(int64_t R, int64_t Cn, int64_t tm, int64_t tn, int policy,
  * static chunk ic.  For box index t = tile*BM*BN + pos: team[t], unit[t] =
  * executor, or -1 where the box position is not an iteration.  Returns the
  * number of tiles, or -1. */
+int64_t orc_tiled_owner_order(int64_t lb0, int64_t ub0, int64_t lb1, int64_t ub1, int64_t BM, int64_t BN,
+                              int policy, int64_t chunk, int64_t p_teams, int64_t ic, int64_t units,
+                              int colmajor, int64_t *team, int64_t *unit);
+
 int64_t orc_tiled_owner(int64_t lb0, int64_t ub0, int64_t lb1, int64_t ub1, int64_t BM, int64_t BN,
                         int policy, int64_t chunk, int64_t p_teams, int64_t ic, int64_t units,
                         int64_t *team, int64_t *unit)
+{
+    return orc_tiled_owner_order(lb0, ub0, lb1, ub1, BM, BN, policy, chunk, p_teams, ic, units, 0, team, unit);
+}
+
+/* As orc_tiled_owner, with the tile ids enumerated column-major when colmajor
+ * != 0 (reading c35: tile id = (tj - tj0) * ntr + (ti - ti0); the paper's
+ * tiling, fixes no order).  Arrays are indexed by that id. */
+int64_t orc_tiled_owner_order(int64_t lb0, int64_t ub0, int64_t lb1, int64_t ub1, int64_t BM, int64_t BN,
+                              int policy, int64_t chunk, int64_t p_teams, int64_t ic, int64_t units,
+                              int colmajor, int64_t *team, int64_t *unit)
 {
     if (BM <= 0 || BN <= 0 || ic <= 0 || units <= 0 || p_teams <= 0) return -1;
     if (ub0 <= lb0 || ub1 <= lb1) return 0;
@@ -466,7 +480,8 @@ int64_t orc_tiled_owner(int64_t lb0, int64_t ub0, int64_t lb1, int64_t ub1, int6
     if (!towner) return -1;
     if (orc_owner_map(policy, chunk, nt, p_teams, towner) != 0) { free(towner); return -1; }
     for (int64_t tile = 0; tile < nt; ++tile) {
-        int64_t ti = ti0 + tile / ntc, tj = tj0 + tile % ntc;
+        int64_t ti = colmajor ? ti0 + tile % ntr : ti0 + tile / ntc;
+        int64_t tj = colmajor ? tj0 + tile / ntr : tj0 + tile % ntc;
         for (int64_t pos = 0; pos < P; ++pos) {
             int64_t i = ti * BM + pos / BN, j = tj * BN + pos % BN;
             int64_t t = tile * P + pos;

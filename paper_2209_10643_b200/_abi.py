@@ -21,6 +21,7 @@ SCHED_STATIC, SCHED_DYNAMIC, SCHED_GUIDED, SCHED_RUNTIME, SCHED_AUTO = 0, 1, 2, 
 DIST_TEAMS, DIST_UNITS, DIST_TEAMS_UNITS = 1, 2, 3
 NOWAIT = 1
 WORLD_REDUCE = 2
+TILE_COLMAJOR = 4
 PEER_REC_BYTES = 256
 BODY_AXPY, BODY_REDUCE, BODY_JACOBI5, BODY_MATMUL, BODY_MATVEC, BODY_STENCIL2D = 0, 1, 2, 3, 4, 5
 OP_SUM, OP_MAX, OP_MIN = 0, 1, 2

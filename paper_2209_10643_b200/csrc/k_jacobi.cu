@@ -135,8 +135,7 @@ __global__ void __launch_bounds__(1024) jacobi5_kernel(const __grid_constant__ J
   // peer mode: sweeps this rank completed = sweeps each neighbour must have
   // delivered before a boundary tile may read / write halo rows
   unsigned long long gen = 0;
-  auto peer_wait = [&](int64_t tile) {
-    const int64_t i0 = (a.ti0 + tile / a.ntc) * BM;
+  auto peer_wait = [&](int64_t i0) {
     bool waited = false;
     if (a.win_up && a.halo_up_row >= i0 - 1 && a.halo_up_row <= i0 + BM) {
       wait_geq_sys(a.win + WIN_HALO_FROM_UP, gen);
@@ -158,7 +157,10 @@ __global__ void __launch_bounds__(1024) jacobi5_kernel(const __grid_constant__ J
     tile_s[4 * slot] = nx;
     if (nx >= 0) {
       // interior tile: every position an iteration, no peer boundary row
-      const int64_t i0 = (a.ti0 + nx / a.ntc) * BM, j0 = (a.tj0 + nx % a.ntc) * BN;
+      // tile id -> (row, column) of the tile grid: row-major (c24) or
+      // column-major (UPIR_TILE_COLMAJOR, c35)
+      const int64_t i0 = (a.ti0 + (a.colmajor ? nx % a.ntr : nx / a.ntc)) * BM;
+      const int64_t j0 = (a.tj0 + (a.colmajor ? nx / a.ntr : nx % a.ntc)) * BN;
       const bool fast = !TRACE && a.inner_chunk == 4 && (a.units & 31) == 0 && i0 >= a.lb0 && i0 + BM <= a.ub0 &&
                         j0 >= a.lb1 && j0 + BN <= a.ub1 && (a.ld & 3) == 0 && ((uintptr_t)a.out & 15) == 0 &&
                         (!a.win || ((a.send_up_row < i0 || a.send_up_row >= i0 + BM) &&
@@ -166,7 +168,7 @@ __global__ void __launch_bounds__(1024) jacobi5_kernel(const __grid_constant__ J
       tile_s[4 * slot + 1] = i0;
       tile_s[4 * slot + 2] = j0;
       tile_s[4 * slot + 3] = fast;
-      if (a.win) peer_wait(nx);
+      if (a.win) peer_wait(i0);
       issue(i0, j0, slot);
     } else {
       tma_mbar_arrive(bars + slot);

@@ -883,6 +883,8 @@ static upir_status validate_loop(const upir_spmd_desc *sd, const upir_loop_desc 
   if (st != UPIR_OK) return st;
   if (!l) return fail(UPIR_E_INVALID, "loop descriptor is NULL");
   if (l->simdlen > 4096) return fail(UPIR_E_INVALID, "simdlen %u outside [0, 4096]", l->simdlen);
+  if ((l->flags & UPIR_TILE_COLMAJOR) && kind != UPIR_BODY_JACOBI5)
+    return fail(UPIR_E_UNSUPPORTED, "UPIR_TILE_COLMAJOR is implemented for JACOBI5 tiled nests only");
   int64_t T;
   st = upir_loop_normalize(l, &T, nullptr);
   if (st != UPIR_OK) return st;
@@ -1294,6 +1296,7 @@ static upir_status exec_jacobi(upir_spmd s, const upir_loop_desc *l, const upir_
                 (long long)ub0, (long long)row0, (long long)(row0 + rows_local));
   JacobiArgs a;
   memset(&a, 0, sizeof a);
+  a.colmajor = (l->flags & UPIR_TILE_COLMAJOR) ? 1 : 0;
   if (peer) {
     int64_t plan[8];
     if ((st = upir_halo_plan(mo->dist.n_rows, mo->dist.halo_rows, c->rank, c->nranks, plan)) != UPIR_OK) return st;

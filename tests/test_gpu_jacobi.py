@@ -9,6 +9,7 @@ light-cone windows (reading c16, c25).
 """
 import numpy as np
 import pytest
+import torch
 
 import oracle
 import paper_2209_10643_b200 as U
@@ -27,7 +28,7 @@ def ctx(upir):
 
 
 def jacobi_gpu(ctx, g, S, teams=8, units=256, tile=(32, 256), policy=U.SCHED_STATIC, chunk=1, ic=4,
-               space=None, graph=False, trace=False, simdlen=0):
+               space=None, graph=False, trace=False, simdlen=0, flags=0):
     """Run S ping-pong sweeps; returns (grid after S sweeps, trace or None)."""
     ny, nx = g.shape
     a, b = g.copy(), g.copy()
@@ -35,7 +36,7 @@ def jacobi_gpu(ctx, g, S, teams=8, units=256, tile=(32, 256), policy=U.SCHED_STA
     mb = U.upir_data_map(ctx, b, U.MAP_TOFROM)
     (lb0, ub0, lb1, ub1) = space or (1, ny - 1, 1, nx - 1)
     loop = U.loop_desc([lb0, lb1], [ub0, ub1], tile=list(tile), policy=policy, chunk=chunk,
-                       distribute=U.DIST_TEAMS, inner_chunk=ic, simdlen=simdlen)
+                       distribute=U.DIST_TEAMS, inner_chunk=ic, simdlen=simdlen, flags=flags)
     s = U.upir_spmd_launch(ctx, U.spmd_desc(teams, units))
     tr = tm = None
     if trace:
@@ -227,3 +228,44 @@ def test_jacobi_interior_fast_path_matches_checked(ctx):
     checked, _ = jacobi_gpu(ctx, g, 1, teams=37, units=256, tile=(16, 256), trace=True)
     assert (fast == checked).all()
     assert rel(fast, oracle.jacobi5(g, 1)) <= 1e-5
+
+
+# ---- reading c35: column-major tile ids (UPIR_TILE_COLMAJOR) --------------------
+@pytest.mark.parametrize("policy,chunk", [(U.SCHED_STATIC, 0), (U.SCHED_STATIC, 1), (U.SCHED_STATIC, 3),
+                                          (U.SCHED_DYNAMIC, 2)])
+def test_jacobi_colmajor_parity_and_trace(ctx, policy, chunk):
+    """Column-major tile ids: same grid as the row-major order (bit-exact: the
+    order only moves work between teams), tile -> team / position -> unit
+    map bit-exact against the oracle's column-major enumeration (dynamic:
+    the position -> unit map and coverage)."""
+    g = synth.jacobi_init(150, 520)
+    teams, units, tile = 7, 128, (16, 256)
+    rowm, _ = jacobi_gpu(ctx, g, 3, teams=teams, units=units, tile=tile, policy=policy, chunk=chunk)
+    colm, _ = jacobi_gpu(ctx, g, 3, teams=teams, units=units, tile=tile, policy=policy, chunk=chunk,
+                         flags=U.TILE_COLMAJOR)
+    assert (colm == rowm).all()
+    assert rel(colm, oracle.jacobi5(g, 3)) <= 1e-5
+    _, tr = jacobi_gpu(ctx, g, 1, teams=teams, units=units, tile=tile, policy=policy, chunk=chunk,
+                       trace=True, flags=U.TILE_COLMAJOR)
+    n = len(tr) // 3
+    team, unit, hits = tr[:n], tr[n:2 * n], tr[2 * n:]
+    ot, ou = oracle.tiled_owner(1, 149, 1, 519, tile[0], tile[1], OPOL[policy], chunk, teams, 4, units,
+                                colmajor=True)
+    it = ot >= 0
+    assert (hits[it] == 1).all() and (hits[~it] == 0).all()
+    assert (unit[it] == ou[it]).all()
+    if policy == U.SCHED_STATIC:
+        assert (team[it] == ot[it]).all()
+
+
+def test_colmajor_rejected_for_other_bodies(ctx):
+    x = np.zeros(1024, np.float32)
+    m = U.upir_data_map(ctx, x, U.MAP_TO)
+    s = U.upir_spmd_launch(ctx, U.spmd_desc(4, 128))
+    r = torch.zeros(1, dtype=torch.float32, device="cuda")
+    with pytest.raises(U.UpirError):
+        U.upir_loop_exec(s, U.loop_desc(0, 1024, flags=U.TILE_COLMAJOR), U.body(U.BODY_REDUCE, U.F32, in0=m),
+                         [U.reduction(U.OP_SUM, U.F32, r)])
+    U.upir_spmd_end(s)
+    U.upir_data_unmap(ctx, m)
+    U.upir_sync(ctx)

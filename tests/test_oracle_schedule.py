@@ -205,6 +205,48 @@ def test_tiled_owner_bruteforce():
     assert (team >= 0).sum() == (ub0 - lb0) * (ub1 - lb1)
 
 
+@pytest.mark.parametrize("policy,chunk,p", [(0, 1, 3), (0, 0, 4), (0, 2, 5)])
+def test_tiled_owner_colmajor_bruteforce(policy, chunk, p):
+    """Reading c35: tile ids enumerate the tile grid column-major; the tile
+    loop schedule and the intra-tile rule are unchanged.  Brute force of the
+    reading (static block / static,c written out), and the set of executed
+    (i, j) equals the row-major enumeration's."""
+    lb0, ub0, lb1, ub1, BM, BN, ic, units = 1, 10, 1, 13, 4, 8, 4, 5
+    team, unit = oracle.tiled_owner(lb0, ub0, lb1, ub1, BM, BN, oracle.STATIC, chunk, p, ic, units, colmajor=True)
+    ntr, ntc = 3, 2
+    nt = ntr * ntc
+    tiles = [(ti, tj) for tj in range(ntc) for ti in range(ntr)]     # column-major ids
+
+    def tile_team(tid):
+        if chunk == 0:       # static block: first nt % p teams get one more
+            q, r = divmod(nt, p)
+            lo = 0
+            for u in range(p):
+                n = q + (u < r)
+                if lo <= tid < lo + n:
+                    return u
+                lo += n
+        return (tid // chunk) % p
+    t = 0
+    seen = set()
+    for tid, (ti, tj) in enumerate(tiles):
+        for pos in range(BM * BN):
+            i, j = ti * BM + pos // BN, tj * BN + pos % BN
+            if lb0 <= i < ub0 and lb1 <= j < ub1:
+                assert team[t] == tile_team(tid) and unit[t] == (pos // ic) % units
+                seen.add((i, j))
+            else:
+                assert team[t] == -1 and unit[t] == -1
+            t += 1
+    assert seen == {(i, j) for i in range(lb0, ub0) for j in range(lb1, ub1)}
+    # a row-major run gives the same per-position unit map within each tile
+    team_r, unit_r = oracle.tiled_owner(lb0, ub0, lb1, ub1, BM, BN, oracle.STATIC, chunk, p, ic, units)
+    P = BM * BN
+    for tid, (ti, tj) in enumerate(tiles):
+        rid = ti * ntc + tj
+        assert (unit[tid * P:(tid + 1) * P] == unit_r[rid * P:(rid + 1) * P]).all()
+
+
 # ---- simd(simdlen) combined with worksharing (reading c33) -------------------------
 SIMD_CASES = [(T, p, s) for T in (0, 1, 7, 64, 100, 1001) for p in (1, 3, 8) for s in (2, 4, 8)]
 
