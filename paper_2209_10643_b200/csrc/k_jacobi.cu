@@ -182,11 +182,7 @@ __global__ void __launch_bounds__(1024) jacobi5_kernel(const __grid_constant__ J
 #pragma unroll
     for (int b = 0; b < NST; ++b) {
       tma_mbar_init(bars + b, 1);
-#ifdef UPIR_RING_THREAD_ARRIVE
-      tma_mbar_init(bars + NST + b, cw * 32);
-#else
-      tma_mbar_init(bars + NST + b, cw);
-#endif
+      tma_mbar_init(bars + NST + b, cw * 32);   // every thread of the unit warps releases the slot
     }
     tma_fence_init();
   }
@@ -322,12 +318,10 @@ __global__ void __launch_bounds__(1024) jacobi5_kernel(const __grid_constant__ J
           }
         }
       }
-#ifdef UPIR_RING_THREAD_ARRIVE
-      tma_mbar_arrive(bars + NST + buf);   // this thread is done with `buf`
-#else
-      __syncwarp();
-      if ((threadIdx.x & 31) == 0) tma_mbar_arrive(bars + NST + buf);   // this warp is done with `buf`
-#endif
+      // this thread is done with `buf` (its window reads and its read of the
+      // slot record): a per-thread release, so the producer's refill is
+      // ordered after every read without relying on a warp barrier
+      tma_mbar_arrive(bars + NST + buf);
     }
   }
   // peer mode: after the whole sweep (every unit's peer stores fenced), the

@@ -65,7 +65,7 @@ __global__ void __launch_bounds__(MAXT + (PW ? 32 : 0)) stencil_kernel(const __g
   extern __shared__ __align__(128) char smc[];
   constexpr int NST = L::NST;
   uint64_t *bars = reinterpret_cast<uint64_t *>(smc + NST * L::BUF);
-  // bars: full[NST] (TMA landed / end marker), empty[NST] (every warp done with the buffer)
+  // bars: full[NST] (TMA landed / end marker), empty[NST] (every unit-warp thread done with the buffer)
   // per slot: tile id, first row, first column (written by the producer
   // before the slot's full barrier completes)
   volatile long long *tile_s = reinterpret_cast<volatile long long *>(smc + NST * L::BUF + 64);   // [NST][3]
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(MAXT + (PW ? 32 : 0)) stencil_kernel(const __g
 #pragma unroll
     for (int b = 0; b < NST; ++b) {
       tma_mbar_init(bars + b, 1);
-      tma_mbar_init(bars + NST + b, cw);
+      tma_mbar_init(bars + NST + b, cw * 32);   // every thread of the unit warps releases the slot
     }
     tma_fence_init();
   }
@@ -331,8 +331,7 @@ __global__ void __launch_bounds__(MAXT + (PW ? 32 : 0)) stencil_kernel(const __g
         }
       }
     }
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) tma_mbar_arrive(bars + NST + buf);   // this warp is done with `buf`
+    tma_mbar_arrive(bars + NST + buf);   // this thread is done with `buf` (per-thread release)
   }
   }   // unit warps
   if (a.sched == SK_DYNAMIC) {
