@@ -11,7 +11,9 @@ Sequential, fp64 / exact int64.  Every function cites the passage it follows
 Parity status per function:
   trip_count, delinearize, schedule_chunks(static, static+chunk), owner_map,
   axpy, reduce_i64, reduce_f32, jacobi5, jacobi5_window, matmul_rows,
-  tile_owner, MapSpace: pinned.
+  tile_owner, tiled_owner (row-major c24 and column-major c35 tile ids),
+  schedule_chunks(guided), matvec, stencil2d, simdlen groups (c33),
+  MapSpace: pinned.
   schedule_chunks(dynamic): chunk partition pinned; the unit assignment is
   "parity unpinned (several results correct)" -- the GPU's assignment is
   checked for validity, not equality (reading c8).
