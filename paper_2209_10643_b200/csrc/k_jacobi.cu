@@ -182,7 +182,9 @@ __global__ void __launch_bounds__(1024) jacobi5_kernel(const __grid_constant__ J
 #pragma unroll
     for (int b = 0; b < NST; ++b) {
       tma_mbar_init(bars + b, 1);
-      tma_mbar_init(bars + NST + b, cw * 32);   // every thread of the unit warps releases the slot
+      // every thread of the unit warps releases the slot: the whole (rounded-up)
+      // unit warps with a producer warp, all blockDim.x threads without one
+      tma_mbar_init(bars + NST + b, PW ? cw * 32 : blockDim.x);
     }
     tma_fence_init();
   }
