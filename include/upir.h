@@ -140,6 +140,13 @@ upir_status upir_data_update(upir_ctx ctx, upir_map map, int direction);
  * computation). */
 upir_status upir_data_update_section(upir_ctx ctx, upir_map map, int64_t byte_offset, int64_t bytes,
                                      int direction);
+/* direction UPIR_UPDATE_FORWARD_ASYNC (2): a forward section update that is
+ * NOT ordered after earlier compute work (OpenMP 'target update to(...)
+ * nowait'; the async attribute of a data movement): the
+ * caller asserts that no compute work enqueued earlier touches the section.
+ * Section copies then run back to back on the copy stream while the loop over
+ * section k executes behind copy k only (chunk-pipelined map(to)). */
+#define UPIR_UPDATE_FORWARD_ASYNC 2
 /* Device pointer of the local buffer, the number of local elements (rows *
  * row_elems, halo included) and the global element index of its first
  * element. */
@@ -251,13 +258,20 @@ typedef enum { UPIR_DIST_TEAMS = 1, UPIR_DIST_UNITS = 2, UPIR_DIST_TEAMS_UNITS =
  * of the loop (Fig. 7 'allreduce' with ranks as units fused into the loop's
  * end barrier): every rank receives
  *   init (+) P_0 (+) P_1 (+) ... (+) P_{N-1}   (ascending rank order)
- * where P_r is rank r's combination of its units' partials (fp64 for F32,
- * rounded once; the original value counted once).  With every rank's peer
- * window imported the last team of each rank exchanges the partials through
- * NVLink peer memory inside the loop kernel; otherwise (communicator only)
- * the loop is followed by upir_reduce(WORLD).  Collective: every rank must
- * execute the loop.  nranks == 1: no effect. */
+ * where P_r is rank r's combination of its units' partials (int64, or fp64
+ * for F32 rounded once; the original value counted once).  With every rank's
+ * peer window imported the last team of each rank exchanges the partials
+ * through NVLink peer memory inside the loop kernel; otherwise (communicator
+ * only, or UPIR_WORLD_VIA_COMM) the loop's last team writes P_r to a context
+ * scratch word pair, an ncclAllGather collects them and one combine kernel
+ * applies init in ascending rank order -- the same arithmetic, so both paths
+ * give identical bits.  Collective: every rank must execute the loop.
+ * nranks == 1: no effect. */
 #define UPIR_WORLD_REDUCE 2u
+/* UPIR_WORLD_VIA_COMM: with UPIR_WORLD_REDUCE, combine over ranks through the
+ * communicator (NCCL all-gather) even when the peer windows are imported
+ * (measurement of the NCCL path next to the fused one). */
+#define UPIR_WORLD_VIA_COMM 8u
 
 typedef struct {
     int32_t collapse;        /* 1..2 */

@@ -61,7 +61,6 @@ def lib():
             "orc_axpy": (i32, [i64, i64, i64, i64, dbl, vp, vp, vp]),
             "orc_reduce_i64": (i32, [i32, i64, i64, i64, i64, i32, i64, i64, vp, i64, vp, vp]),
             "orc_reduce_f32": (i32, [i32, i64, i64, i64, i64, i32, i64, i64, vp, dbl, vp, vp]),
-            "orc_sum_i64_plain": (i64, [i64, vp]),
             "orc_jacobi5": (i32, [i64, i64, i64, vp, vp]),
             "orc_jacobi5_window": (i32, [i64, i64, i64, i64, i64, i64, i64, vp, vp]),
             "orc_matmul_rows": (i32, [i64, i64, i64, vp, vp, vp, i64, vp]),

@@ -338,15 +338,6 @@ int orc_reduce_f32(int op, int64_t n, int64_t lb, int64_t ub, int64_t step,
     return 0;
 }
 
-/* Plain sequential reduction without a schedule (p = 1, static): used to time
- * the oracle on bounded samples; identical to orc_reduce_* with p = 1. */
-int64_t orc_sum_i64_plain(int64_t n, const int64_t *x)
-{
-    uint64_t s = 0;
-    for (int64_t i = 0; i < n; ++i) s += (uint64_t)x[i];
-    return (int64_t)s;
-}
-
 /* ---- o6: Jacobi 5-point (north_star; reading c16, c25) ----------------
  * One sweep: out[i][j] = 0.25*((in[i-1][j] + in[i+1][j]) + (in[i][j-1] +
  * in[i][j+1])) for 1 <= i < ny-1, 1 <= j < nx-1; boundary copied unchanged.

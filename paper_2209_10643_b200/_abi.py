@@ -22,11 +22,13 @@ DIST_TEAMS, DIST_UNITS, DIST_TEAMS_UNITS = 1, 2, 3
 NOWAIT = 1
 WORLD_REDUCE = 2
 TILE_COLMAJOR = 4
+WORLD_VIA_COMM = 8
 PEER_REC_BYTES = 256
 BODY_AXPY, BODY_REDUCE, BODY_JACOBI5, BODY_MATMUL, BODY_MATVEC, BODY_STENCIL2D = 0, 1, 2, 3, 4, 5
 OP_SUM, OP_MAX, OP_MIN = 0, 1, 2
 SCOPE_DEVICE, SCOPE_WORLD = 0, 1
 SYNC_BARRIER, SYNC_WORLD_BARRIER, SYNC_ARRIVE, SYNC_WAIT, SYNC_HALO, SYNC_JOIN = 0, 1, 2, 3, 4, 5
+UPDATE_FORWARD, UPDATE_BACKWARD, UPDATE_FORWARD_ASYNC = 0, 1, 2
 
 i32, i64, u32, u64 = ctypes.c_int32, ctypes.c_int64, ctypes.c_uint32, ctypes.c_uint64
 vp = ctypes.c_void_p

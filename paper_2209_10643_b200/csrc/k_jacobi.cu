@@ -377,7 +377,7 @@ cudaError_t launch_nst(const JacobiArgs &a, const CUtensorMap &c, const CUtensor
 
 // Ring depth: the deepest ring that keeps at most ~112 KB of tile windows per
 // SM (teams resident per SM x NST x window bytes).  Measured on B200 (C3,
-// tools/debug/jacobi_sweep.py): 3 teams/SM x 2 slots and 2 teams/SM x 3 slots
+// tools/experiments/jacobi_sweep.py): 3 teams/SM x 2 slots and 2 teams/SM x 3 slots
 // of 16x256 tiles are best; deeper rings at the same residency lose 10-15 %
 // (more reads queued ahead of the write-back stream).
 template <int BM, int BN>

@@ -65,6 +65,40 @@ __global__ void rank_combine_kernel(int op, int dtype, const void *gathered, int
   }
 }
 
+struct WorldCombineArgs { RedSpec red[2]; };
+__global__ void world_combine_kernel(const unsigned long long *g, int nranks, int nred, WorldCombineArgs w) {
+  for (int r = 0; r < nred; ++r) {
+    const RedSpec &rs = w.red[r];
+    if (rs.dtype == UPIR_I64) {
+      unsigned long long acc = rs.init_bits;
+      for (int q = 0; q < nranks; ++q) {
+        const long long v = (long long)g[q * 2 + r];
+        if (rs.op == UPIR_OP_SUM) acc += (unsigned long long)v;
+        else if (rs.op == UPIR_OP_MAX) acc = ((long long)acc > v) ? acc : (unsigned long long)v;
+        else acc = ((long long)acc < v) ? acc : (unsigned long long)v;
+      }
+      *reinterpret_cast<long long *>(rs.result) = (long long)acc;
+    } else {
+      double acc = __longlong_as_double((long long)rs.init_bits);
+      for (int q = 0; q < nranks; ++q) {
+        const double v = __longlong_as_double((long long)g[q * 2 + r]);
+        if (rs.op == UPIR_OP_SUM) acc += v;
+        else if (rs.op == UPIR_OP_MAX) acc = fmax(acc, v);
+        else acc = fmin(acc, v);
+      }
+      *reinterpret_cast<float *>(rs.result) = (float)acc;   // the one rounding
+    }
+  }
+}
+
+cudaError_t launch_world_combine(const unsigned long long *gathered, int nranks, int nred, const RedSpec *reds,
+                                 cudaStream_t s) {
+  WorldCombineArgs w;
+  for (int r = 0; r < 2; ++r) w.red[r] = r < nred ? reds[r] : RedSpec{};
+  world_combine_kernel<<<1, 1, 0, s>>>(gathered, nranks, nred, w);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_rank_combine(int op, int dtype, const void *gathered, int64_t count, int nranks,
                                 void *out, cudaStream_t s) {
   const int threads = 256;

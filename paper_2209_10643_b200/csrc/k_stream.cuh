@@ -190,9 +190,10 @@ __device__ __forceinline__ void direct_long(const StreamArgs &a, int64_t elo, in
   constexpr int STEP = VEC * NV;   // elements per load
   constexpr int AL = LINE ? STEP * U : STEP;
   int64_t e = elo;
-  const int64_t ea = min(ehi, ((elo + AL - 1) / AL) * AL);
+  const int64_t sh = a.esh;   // vectors are aligned by address, not by index
+  const int64_t ea = min(ehi, ((elo + sh + AL - 1) / AL) * AL - sh);
   for (; e < ea; ++e) body_scalar<BODY, NRED, false>(a, e, acc, 0, 0);
-  const int64_t eb = max(e, min(ehi, vec_hi) / STEP * STEP);
+  const int64_t eb = max(e, (min(ehi, vec_hi) + sh) / STEP * STEP - sh);
   for (; e + U * STEP <= eb; e += U * STEP) {
     if constexpr (BODY == SB_RED_I64) {
       const long long *p = reinterpret_cast<const long long *>(a.in0) + e;
@@ -289,7 +290,7 @@ __device__ void direct_run(const StreamArgs &a, const LaneWork &w, Acc<BODY, NRE
   if (w.nk == 0) return;
   constexpr int VEC = BODY == SB_RED_I64 ? 2 : 4;
   int64_t j = 0;
-  if (a.step == 1 && w.c == VEC && w.nk > 1 && ((a.lb + w.lo0) % VEC) == 0 &&
+  if (a.vecok && a.step == 1 && w.c == VEC && w.nk > 1 && ((a.lb + w.lo0 + a.esh) % VEC) == 0 &&
       (w.kstride % VEC) == 0) {
     // chunks that are one full, aligned vector inside the safe range
     const int64_t lim = min(a.T, a.safe_hi - a.lb);   // need klo + VEC <= lim
@@ -343,8 +344,8 @@ __device__ void direct_run(const StreamArgs &a, const LaneWork &w, Acc<BODY, NRE
   // streams its own range with wide vector loads, several in flight
   // (adjacent units are far apart, so a warp instruction touches 32 lines;
   // each line is then consumed from L1 by the following loads of the lane).
-  if (a.step == 1 && w.c > VEC) {
-    const int64_t vec_hi = (a.safe_hi / VEC) * VEC;
+  if (a.vecok && a.step == 1 && w.c > VEC) {
+    const int64_t vec_hi = a.safe_hi;
     for (; j < w.nk; ++j) {
       int64_t klo, khi;
       chunk_bounds(w, j, a.T, klo, khi);
@@ -365,9 +366,10 @@ __device__ void direct_run(const StreamArgs &a, const LaneWork &w, Acc<BODY, NRE
         continue;
       }
       int64_t e = elo;
-      const int64_t ea = min(ehi, ((elo + VEC - 1) / VEC) * VEC);
+      const int64_t sh = a.esh;
+      const int64_t ea = min(ehi, ((elo + sh + VEC - 1) / VEC) * VEC - sh);
       for (; e < ea; ++e) body_scalar<BODY, NRED, TRACE>(a, e, acc, team, unit);
-      const int64_t eb = max(e, min(ehi, vec_hi) / VEC * VEC);
+      const int64_t eb = max(e, (min(ehi, vec_hi) + sh) / VEC * VEC - sh);
       for (; e + 4 * VEC <= eb; e += 4 * VEC) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) direct_vec<BODY, NRED, TRACE>(a, e + q * VEC, acc, team, unit);
@@ -702,6 +704,9 @@ __device__ void reduce_epilogue(const StreamArgs &a, Acc<BODY, NRED> &acc, bool 
         else *reinterpret_cast<float *>(rs.result) = (float)x;
       }
       *reinterpret_cast<volatile unsigned long long *>(win + WIN_WR_GEN) = e + 1ull;
+    } else if (threadIdx.x == 0 && a.wpart) {
+#pragma unroll
+      for (int r = 0; r < NRED; ++r) a.wpart[r] = to_bits(v[r]);   // combined over ranks by the host path
     } else if (threadIdx.x == 0) {
 #pragma unroll
       for (int r = 0; r < NRED; ++r) {

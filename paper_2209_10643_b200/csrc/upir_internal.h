@@ -65,6 +65,10 @@ struct StreamArgs {
   float alpha;
   int64_t safe_lo, safe_hi;  // elements [safe_lo, safe_hi) may be read as 16-B vectors
   int32_t dvar;              // DIRECT long-chunk load variant (0: 4x16 B, 1: 4x32 B, 2: 2x32 B, 3: 8x16 B)
+  // address alignment of the element views: element e lives at a 128-B
+  // aligned base + (e + esh) * esz (esh < 128 / esz, identical for x and y);
+  // vecok = 0 when x and y disagree (only scalar accesses are then legal)
+  int32_t esh, vecok;
   int64_t simd;              // static block: SIMD group size (simdlen, reading c33), 1 = none
   // reductions
   int32_t nred;
@@ -75,6 +79,10 @@ struct StreamArgs {
   // window or null; the last team combines init (+) P_0 (+) ... (+) P_{N-1}
   unsigned long long *wwin;
   int32_t wrank, wranks;
+  // world reduction by a communicator instead: the last team writes the
+  // rank's partials (int64 / fp64 bits, init NOT applied) here, for the
+  // all-gather and the ordered fp64 combine (launch_world_combine)
+  unsigned long long *wpart;
   // trace: [team[T], unit[T], hits[T]] int32, or null
   int32_t *trace;
 };
@@ -95,6 +103,10 @@ cudaError_t launch_reduce_array(int op, int dtype, const void *in, int64_t count
 cudaError_t launch_peer_drain(unsigned long long *win, int has_up, int has_dn, cudaStream_t s);
 // Barrier over all ranks through the peer windows (communicator-less worlds).
 cudaError_t launch_peer_barrier(unsigned long long *win, int nranks, cudaStream_t s);
+// result_r = init_r (+) g[0][r] (+) ... (+) g[nranks-1][r] over gathered
+// [nranks][2] partial words of a loop's reductions (int64, or fp64 rounded once).
+cudaError_t launch_world_combine(const unsigned long long *gathered, int nranks, int nred, const RedSpec *reds,
+                                 cudaStream_t s);
 cudaError_t launch_rank_combine(int op, int dtype, const void *gathered, int64_t count,
                                 int nranks, void *out, cudaStream_t s);
 

@@ -71,7 +71,7 @@ struct upir_map_s {
   int64_t elems_local;           // local elements (rows*row_elems)
   int64_t elem_offset;           // global element index of local element 0
   int64_t elem_bytes;
-  bool pinned = false;     // took a user count on a registration
+  void *pin_reg = nullptr; // registration this map took a user count on (or null)
   // peer mode (fused halo): exported from a cudaMalloc block; neighbours'
   // buffers mapped by CUDA IPC ([0] = rank - 1, [1] = rank + 1)
   bool ipc_alloc = false;
@@ -111,10 +111,13 @@ struct upir_ctx_s {
   void *scratch = nullptr;      // world-reduce gather buffer
   size_t scratch_bytes = 0;
   void *one = nullptr;          // 1-element buffer for the world barrier
-  // guided-schedule boundary table cache (T, p, c) -> device table
-  int64_t *gtab = nullptr;
-  size_t gtab_cap = 0;
-  int64_t g_T = -1, g_p = -1, g_c = -1, g_s = -1, g_n = 0;
+  // guided-schedule boundary tables, one device table per (T, p, c, simd),
+  // never overwritten: a captured graph keeps the pointer it was built with
+  struct GTab { int64_t T, p, c, s, n; int64_t *dev; };
+  std::vector<GTab> gtabs;
+  // workspace a captured graph may still reference after it was outgrown:
+  // released at upir_finalize, never while the context lives
+  std::vector<void *> retired;
   // present table: host pointer -> map
   std::map<void *, upir_map> present;
   std::vector<upir_map> adopted;
@@ -144,8 +147,7 @@ static upir_status sticky_check(upir_ctx c) {
 static upir_status ensure_slots(upir_ctx c, size_t teams) {
   if (teams <= c->slots_teams) return UPIR_OK;
   if (c->capturing) return fail(UPIR_E_INVALID, "workspace must grow (teams=%zu) but a graph is being captured", teams);
-  CUDA_TRY(cudaStreamSynchronize(c->compute));
-  if (c->slots) CUDA_TRY(cudaFree(c->slots));
+  if (c->slots) c->retired.push_back(c->slots);   // graphs may hold it
   size_t n = std::max(teams, (size_t)1 << 16);
   CUDA_TRY(cudaMalloc(&c->slots, n * 2 * sizeof(unsigned long long)));
   c->slots_teams = n;
@@ -277,7 +279,8 @@ extern "C" upir_status upir_finalize(upir_ctx c) {
   cudaFree(c->done);
   cudaFree(c->one);
   if (c->scratch) cudaFree(c->scratch);
-  if (c->gtab) cudaFree(c->gtab);
+  for (auto &g : c->gtabs) cudaFree(g.dev);
+  for (void *p : c->retired) cudaFree(p);
   if (c->own_compute) cudaStreamDestroy(c->compute);
   if (c->own_copy) cudaStreamDestroy(c->copy);
   delete c;
@@ -371,31 +374,35 @@ static void map_range(upir_map m, bool owned_only, size_t &host_off, size_t &dev
 // (cudaHostAlloc / torch pin_memory) is used as is.  Ranges we register are
 // released at the first upir_sync (or finalize) after their last map is gone
 // -- the contract keeps host buffers valid until that sync.
-static void pin_host(upir_ctx c, void *host, size_t bytes) {
+// Returns the registration it took a user count on, or null when it took none
+// (small buffer, memory pinned by someone else, failed registration).
+static void *pin_host(upir_ctx c, void *host, size_t bytes) {
   // small buffers are copied from pageable memory (the driver stages them);
   // registering / unregistering a page per map costs more than the copy
-  if (bytes < ((size_t)1 << 20)) return;
+  if (bytes < ((size_t)1 << 20)) return nullptr;
   for (auto &r : c->registered)
     if ((char *)host >= (char *)r.ptr && (char *)host + bytes <= (char *)r.ptr + r.bytes) {
       r.users++;
-      return;
+      return r.ptr;
     }
   cudaPointerAttributes at;
   if (cudaPointerGetAttributes(&at, host) == cudaSuccess &&
       (at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeManaged))
-    return;
+    return nullptr;
   cudaGetLastError();
   cudaError_t e = cudaHostRegister(host, bytes, cudaHostRegisterDefault);
   if (e != cudaSuccess) {
     cudaGetLastError();
-    return;   // pageable copies still work (staged by the driver)
+    return nullptr;   // pageable copies still work (staged by the driver)
   }
   c->registered.push_back({host, bytes, 1});
+  return host;
 }
 
-static void unpin_host(upir_ctx c, void *host) {
+// drop the user count a map took on registration `reg`
+static void unpin_host(upir_ctx c, void *reg) {
   for (auto &r : c->registered)
-    if ((char *)host >= (char *)r.ptr && (char *)host < (char *)r.ptr + r.bytes) {
+    if (r.ptr == reg) {
       r.users--;
       return;
     }
@@ -465,15 +472,13 @@ extern "C" upir_status upir_data_map(upir_ctx c, void *host, size_t bytes, upir_
     delete m;
     return fail(UPIR_E_OOM, "device allocation of %zu bytes failed: %s", alloc, cudaGetErrorString(e));
   }
-  if (kind != UPIR_MAP_ALLOC) {
-    pin_host(c, host, bytes);
-    m->pinned = true;
-  }
+  if (kind != UPIR_MAP_ALLOC) m->pin_reg = pin_host(c, host, bytes);
   if (kind == UPIR_MAP_TO || kind == UPIR_MAP_TOFROM) {   // data_movement forward
     size_t ho, dof, len;
     map_range(m, false, ho, dof, len);
     e = cudaMemcpyAsync((char *)m->dev + dof, (char *)host + ho, len, cudaMemcpyHostToDevice, c->copy);
     if (e != cudaSuccess) {
+      if (m->pin_reg) unpin_host(c, m->pin_reg);
       cudaFreeAsync(m->dev, c->copy);
       delete m;
       return fail(UPIR_E_CUDA, "H2D copy failed: %s", cudaGetErrorString(e));
@@ -481,7 +486,12 @@ extern "C" upir_status upir_data_map(upir_ctx c, void *host, size_t bytes, upir_
     c->h2d_bytes += (int64_t)len;
   }
   st = copy_to_compute(c);
-  if (st != UPIR_OK) return st;
+  if (st != UPIR_OK) {
+    if (m->pin_reg) unpin_host(c, m->pin_reg);
+    cudaFreeAsync(m->dev, c->copy);
+    delete m;
+    return st;
+  }
   c->present[host] = m;
   *out = m;
   return UPIR_OK;
@@ -541,7 +551,7 @@ extern "C" upir_status upir_data_unmap(upir_ctx c, upir_map m) {
   } else {
     CUDA_TRY(cudaFreeAsync(m->dev, c->copy));   // mm_deallocator
   }
-  if (m->pinned) unpin_host(c, m->host);
+  if (m->pin_reg) unpin_host(c, m->pin_reg);
   c->present.erase(it);
   delete m;
   return sticky_check(c);
@@ -549,7 +559,8 @@ extern "C" upir_status upir_data_unmap(upir_ctx c, upir_map m) {
 
 extern "C" upir_status upir_data_update(upir_ctx c, upir_map m, int direction) {
   if (!c || !m || m->ctx != c || !m->owned || !m->host) return fail(UPIR_E_INVALID, "bad map");
-  if (direction != 0 && direction != 1) return fail(UPIR_E_INVALID, "direction must be 0 or 1");
+  if (direction < 0 || direction > UPIR_UPDATE_FORWARD_ASYNC)
+    return fail(UPIR_E_INVALID, "direction must be 0 (forward), 1 (backward) or 2 (forward async)");
   upir_status st = compute_to_copy(c);
   if (st != UPIR_OK) return st;
   size_t ho, dof, len;
@@ -567,7 +578,8 @@ extern "C" upir_status upir_data_update(upir_ctx c, upir_map m, int direction) {
 
 extern "C" upir_status upir_data_update_section(upir_ctx c, upir_map m, int64_t off, int64_t bytes, int direction) {
   if (!c || !m || m->ctx != c || !m->owned || !m->host) return fail(UPIR_E_INVALID, "bad map");
-  if (direction != 0 && direction != 1) return fail(UPIR_E_INVALID, "direction must be 0 or 1");
+  if (direction < 0 || direction > UPIR_UPDATE_FORWARD_ASYNC)
+    return fail(UPIR_E_INVALID, "direction must be 0 (forward), 1 (backward) or 2 (forward async)");
   if (off < 0 || bytes < 0 || off + bytes > (int64_t)m->dev_bytes)
     return fail(UPIR_E_INVALID, "section [%lld, +%lld) outside the local buffer (%zu B)", (long long)off,
                 (long long)bytes, m->dev_bytes);
@@ -576,9 +588,11 @@ extern "C" upir_status upir_data_update_section(upir_ctx c, upir_map m, int64_t 
   size_t ho, dof, len;
   map_range(m, false, ho, dof, len);
   char *h = (char *)m->host + ho - dof + off;
-  upir_status st = compute_to_copy(c);
-  if (st != UPIR_OK) return st;
-  if (direction == 0) {
+  if (direction != UPIR_UPDATE_FORWARD_ASYNC) {   // ordered after the compute work so far
+    upir_status st = compute_to_copy(c);
+    if (st != UPIR_OK) return st;
+  }
+  if (direction != 1) {
     CUDA_TRY(cudaMemcpyAsync((char *)m->dev + off, h, (size_t)bytes, cudaMemcpyHostToDevice, c->copy));
     c->h2d_bytes += bytes;
   } else {
@@ -958,6 +972,7 @@ struct ElemView {
   char *base_shifted;   // element i at base_shifted + i*esz
   int64_t lo, hi;       // valid global element indices
   bool aligned16;
+  int32_t esh;          // base_shifted = 128-B aligned address + esh * esz
 };
 
 static upir_status elem_view(upir_map m, int64_t esz, ElemView &v) {
@@ -975,6 +990,9 @@ static upir_status elem_view(upir_map m, int64_t esz, ElemView &v) {
   v.lo = off;
   v.hi = off + n;
   v.aligned16 = ((uintptr_t)v.base_shifted % 16) == 0;
+  if ((uintptr_t)v.base_shifted % esz != 0)
+    return fail(UPIR_E_INVALID, "buffer is not aligned to its %lld-byte elements", (long long)esz);
+  v.esh = (int32_t)(((uintptr_t)v.base_shifted % 128) / esz);
   return UPIR_OK;
 }
 
@@ -1001,11 +1019,12 @@ static const char *env_path() {
 // (PAPER.md:644 'guided'), cached on the device per (T, p, c).
 static upir_status guided_table(upir_ctx c, int64_t T, int64_t p, int64_t ch, int64_t simd, const int64_t **tab,
                                 int64_t *nc) {
-  if (c->g_T == T && c->g_p == p && c->g_c == ch && c->g_s == simd) {
-    *tab = c->gtab;
-    *nc = c->g_n;
-    return UPIR_OK;
-  }
+  for (auto &g : c->gtabs)
+    if (g.T == T && g.p == p && g.c == ch && g.s == simd) {
+      *tab = g.dev;
+      *nc = g.n;
+      return UPIR_OK;
+    }
   if (c->capturing) return fail(UPIR_E_INVALID, "guided table must be built before graph capture");
   // chunk sequence over the G = ceil(T/s) SIMD groups (s = 1: iterations),
   // boundaries scaled back to iterations (reading c33)
@@ -1022,20 +1041,12 @@ static upir_status guided_table(upir_ctx c, int64_t T, int64_t p, int64_t ch, in
     b.push_back(std::min(start * simd, T));
   }
   const size_t bytes = b.size() * sizeof(int64_t);
-  CUDA_TRY(cudaStreamSynchronize(c->compute));
-  if (bytes > c->gtab_cap) {
-    if (c->gtab) CUDA_TRY(cudaFree(c->gtab));
-    CUDA_TRY(cudaMalloc(&c->gtab, bytes));
-    c->gtab_cap = bytes;
-  }
-  CUDA_TRY(cudaMemcpy(c->gtab, b.data(), bytes, cudaMemcpyHostToDevice));
-  c->g_T = T;
-  c->g_p = p;
-  c->g_c = ch;
-  c->g_s = simd;
-  c->g_n = (int64_t)b.size() - 1;
-  *tab = c->gtab;
-  *nc = c->g_n;
+  int64_t *dev = nullptr;
+  CUDA_TRY(cudaMalloc(&dev, bytes));
+  CUDA_TRY(cudaMemcpy(dev, b.data(), bytes, cudaMemcpyHostToDevice));
+  c->gtabs.push_back({T, p, ch, simd, (int64_t)b.size() - 1, dev});
+  *tab = dev;
+  *nc = (int64_t)b.size() - 1;
   return UPIR_OK;
 }
 
@@ -1096,6 +1107,11 @@ static upir_status exec_stream(upir_spmd s, const upir_loop_desc *l, const upir_
   a.simd = simd;
   a.in0 = vx.base_shifted;
   a.out = body == SB_AXPY ? vy.base_shifted : nullptr;
+  // vector accesses are aligned by address (an adopted view with a storage
+  // offset, or a BLOCK slice starting mid-line, is not 32-B aligned by index);
+  // x and y at different offsets within a line: scalar accesses only
+  a.esh = vx.esh;
+  a.vecok = body != SB_AXPY || vy.esh == vx.esh;
   a.alpha = (float)b->alpha;
   a.safe_hi = body == SB_AXPY ? std::min(vx.hi, vy.hi) : vx.hi;
   a.safe_lo = body == SB_AXPY ? std::max(vx.lo, vy.lo) : vx.lo;
@@ -1120,22 +1136,23 @@ static upir_status exec_stream(upir_spmd s, const upir_loop_desc *l, const upir_
   // by upir_reduce(WORLD) (NCCL) on each result -- the same combination
   bool world_after = false;
   if ((l->flags & UPIR_WORLD_REDUCE) && c->nranks > 1 && n_reds > 0) {
-    if (world_ready(c)) {
+    if (world_ready(c) && !((l->flags & UPIR_WORLD_VIA_COMM) && c->comm)) {
       a.wwin = c->win;
       a.wrank = c->rank;
       a.wranks = c->nranks;
     } else if (c->comm) {
+      // each rank's int64 / fp64 partials are all-gathered and combined with
+      // init in ascending rank order, rounded once -- the same arithmetic as
+      // the fused peer path
       world_after = true;
-      if (c->rank != 0)
-        for (int r = 0; r < n_reds; ++r) {
-          if (reds[r].dtype == UPIR_I64) {
-            int64_t v = reds[r].op == UPIR_OP_SUM ? 0 : (reds[r].op == UPIR_OP_MAX ? INT64_MIN : INT64_MAX);
-            a.red[r].init_bits = (uint64_t)v;
-          } else {
-            double v = reds[r].op == UPIR_OP_SUM ? 0.0 : (reds[r].op == UPIR_OP_MAX ? -HUGE_VAL : HUGE_VAL);
-            memcpy(&a.red[r].init_bits, &v, 8);
-          }
-        }
+      a.wpart = reinterpret_cast<unsigned long long *>(reinterpret_cast<char *>(c->done) + 128);
+      const size_t need = (size_t)c->nranks * 16;
+      if (need > c->scratch_bytes) {
+        if (c->capturing) return fail(UPIR_E_INVALID, "scratch must grow during capture");
+        if (c->scratch) c->retired.push_back(c->scratch);   // graphs may hold it
+        CUDA_TRY(cudaMalloc(&c->scratch, need));
+        c->scratch_bytes = need;
+      }
     } else {
       return fail(UPIR_E_INVALID, "UPIR_WORLD_REDUCE needs every rank's peer window (upir_peer_import) or a communicator");
     }
@@ -1208,15 +1225,25 @@ static upir_status exec_stream(upir_spmd s, const upir_loop_desc *l, const upir_
     }
   }
   if (!staged) { segv = 0; nst = 0; smem = 0; }
+  // experiment hook UPIR_DIRECT_OCC = k: reserve dynamic shared memory so
+  // that at most k teams are resident per SM (fewer concurrent per-unit
+  // streams; the direct path itself uses no dynamic shared memory)
+  if (!staged)
+    if (const char *v = getenv("UPIR_DIRECT_OCC")) {
+      const int k = atoi(v);
+      if (k > 0) smem = (size_t)(228 * 1024) / (size_t)(k + 1) + 1024;
+    }
   cudaError_t e = launch_stream_loop(body, staged ? PATH_STAGED : PATH_DIRECT, segv, nst, trace != nullptr,
                                      sd.num_teams, sd.num_units, smem, a, c->compute);
   if (e != cudaSuccess) return fail(UPIR_E_CUDA, "loop kernel launch failed: %s", cudaGetErrorString(e));
   c->launches++;
-  if (world_after)
-    for (int r = 0; r < n_reds; ++r) {
-      st = upir_reduce(c, reds[r].op, reds[r].dtype, reds[r].dev_result, 1, reds[r].dev_result, UPIR_SCOPE_WORLD);
-      if (st != UPIR_OK) return st;
-    }
+  if (world_after) {
+    NCCL_TRY(ncclAllGather(a.wpart, c->scratch, 2, ncclUint64, c->comm, c->compute));
+    e = launch_world_combine(reinterpret_cast<const unsigned long long *>(c->scratch), c->nranks, n_reds, a.red,
+                             c->compute);
+    if (e != cudaSuccess) return fail(UPIR_E_CUDA, "world combine launch failed: %s", cudaGetErrorString(e));
+    c->launches++;
+  }
   return UPIR_OK;
 }
 
@@ -1235,7 +1262,6 @@ extern "C" upir_status upir_loop_exec(upir_spmd s, const upir_loop_desc *l, cons
   if (st != UPIR_OK) return st;
   if (c->sticky != cudaSuccess) return sticky_check(c);
   cudaSetDevice(c->device);
-  if (b->out) b->out->halo_fused = false;   // set again by a peer-mode sweep
   switch (b->kind) {
     case UPIR_BODY_AXPY:
     case UPIR_BODY_REDUCE: st = exec_stream(s, l, b, reds, n_reds, trace); break;
@@ -1245,6 +1271,9 @@ extern "C" upir_status upir_loop_exec(upir_spmd s, const upir_loop_desc *l, cons
     case UPIR_BODY_STENCIL2D: st = exec_stencil(s, l, b, trace); break;
   }
   if (st != UPIR_OK) return st;
+  // out was validated by the body (REDUCE ignores it): a write by anything but
+  // a peer-mode sweep leaves the halos un-exchanged
+  if (b->kind != UPIR_BODY_REDUCE && b->kind != UPIR_BODY_JACOBI5) b->out->halo_fused = false;
   // implicit barrier at the end of a worksharing loop: stream
   // order makes every later operation wait; the host waits only at upir_sync.
   return UPIR_OK;
@@ -1329,7 +1358,10 @@ static upir_status exec_jacobi(upir_spmd s, const upir_loop_desc *l, const upir_
   a.lb1 = lb1;
   a.ub1 = ub1;
   const bool empty = ub0 <= lb0 || ub1 <= lb1;
-  if (empty && !peer) return UPIR_OK;   // empty iteration space
+  if (empty && !peer) {   // empty iteration space
+    mo->halo_fused = false;
+    return UPIR_OK;
+  }
   if (!empty) {
     a.ti0 = lb0 / bm;
     a.tj0 = lb1 / bn;
@@ -1362,7 +1394,7 @@ static upir_status exec_jacobi(upir_spmd s, const upir_loop_desc *l, const upir_
   cudaError_t e = launch_jacobi_tma(a, &tmc, &tmh, sd.num_teams, sd.num_units, bm, bn, trace != nullptr, c->compute);
   if (e != cudaSuccess) return fail(UPIR_E_CUDA, "JACOBI5 launch failed: %s", cudaGetErrorString(e));
   c->launches++;
-  if (peer) mo->halo_fused = true;
+  mo->halo_fused = peer;
   return UPIR_OK;
 }
 static upir_status exec_stencil(upir_spmd s, const upir_loop_desc *l, const upir_body *b, upir_map trace) {
@@ -1646,8 +1678,7 @@ extern "C" upir_status upir_reduce(upir_ctx c, int32_t op, int32_t dtype, const 
   const size_t need = esz * (size_t)count * (size_t)c->nranks;
   if (need > c->scratch_bytes) {
     if (c->capturing) return fail(UPIR_E_INVALID, "scratch must grow during capture");
-    CUDA_TRY(cudaStreamSynchronize(c->compute));
-    if (c->scratch) CUDA_TRY(cudaFree(c->scratch));
+    if (c->scratch) c->retired.push_back(c->scratch);   // graphs may hold it
     CUDA_TRY(cudaMalloc(&c->scratch, need));
     c->scratch_bytes = need;
   }

@@ -139,3 +139,82 @@ def jacobi_worker(rank, world, port, out_dir, ny, nx, S, tile, use_graph, adopt)
     U.upir_sync(ctx, U.SYNC_WORLD_BARRIER)
     U.upir_finalize(ctx)
     dist.destroy_process_group()
+
+
+def block_reduce_worker(rank, world, port, out_dir, n, sched, chunk):
+    """C5a pattern: each rank adopts ONLY its BLOCK slice (rank r's first
+    element is global index lo_r, generally not a multiple of the 32-B vector:
+    the vector paths must align by address), fills it on the device from the
+    global stream, and runs a CLUSTER-target loop with the world reduction
+    fused over the peer windows."""
+    dist, U, ctx = _setup(rank, world, port)
+    import torch
+    lo, hi = U.upir_dist_owned_rows(n, rank, world)
+    xi = torch.empty(hi - lo, dtype=torch.int64, device="cuda")
+    xf = torch.empty(hi - lo, dtype=torch.float32, device="cuda")
+    res = torch.zeros(4, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    mi = U.upir_data_adopt(ctx, xi, U.dist(n, 1, 8))
+    mf = U.upir_data_adopt(ctx, xf, U.dist(n, 1, 4))
+    U.upir_synth_fill(ctx, mi, 2, 6)
+    U.upir_synth_fill(ctx, mf, 0, 7)
+    U.upir_peer_share(ctx)
+    b = res.data_ptr()
+    s = U.upir_spmd_launch(ctx, U.spmd_desc(37, 128, U.TARGET_CLUSTER))
+    U.upir_loop_exec(s, U.loop_desc(0, n, policy=sched, chunk=chunk, flags=U.WORLD_REDUCE),
+                     U.body(U.BODY_REDUCE, U.I64, in0=mi),
+                     [U.reduction(U.OP_SUM, U.I64, b), U.reduction(U.OP_MAX, U.I64, b + 8)])
+    U.upir_loop_exec(s, U.loop_desc(0, n, policy=sched, chunk=chunk, flags=U.WORLD_REDUCE),
+                     U.body(U.BODY_REDUCE, U.F32, in0=mf),
+                     [U.reduction(U.OP_SUM, U.F32, b + 16), U.reduction(U.OP_MAX, U.F32, b + 24)])
+    U.upir_spmd_end(s)
+    U.upir_sync(ctx)
+    np.save(os.path.join(out_dir, f"blk_{rank}.npy"), res.cpu().numpy())
+    np.save(os.path.join(out_dir, f"blkoff_{rank}.npy"), np.array([lo, hi], np.int64))
+    U.upir_sync(ctx, U.SYNC_WORLD_BARRIER)
+    U.upir_data_unmap(ctx, mf)
+    U.upir_data_unmap(ctx, mi)
+    U.upir_sync(ctx)
+    U.upir_finalize(ctx)
+    dist.destroy_process_group()
+
+
+def matmul_rows_worker(rank, world, port, out_dir, M, N, K, dtype_name):
+    """NEXT #4 multi-GPU matmul: A and C BLOCK-distributed by rows, B
+    replicated, CLUSTER-target collapse(2) loop; every rank computes its own
+    rows (no collective)."""
+    dist, U, ctx = _setup(rank, world, port)
+    import synth
+    if dtype_name == "bf16":
+        A = synth.bf16_sym_as_f32(3, 0, M * K).reshape(M, K)
+        B = synth.bf16_sym_as_f32(4, 0, K * N).reshape(K, N)
+        a = (A.view(np.uint32) >> 16).astype(np.uint16)
+        b = (B.view(np.uint32) >> 16).astype(np.uint16)
+        dt, esz, units = U.BF16, 2, 256
+    elif dtype_name == "int":
+        rng = np.random.default_rng(5)
+        A = rng.integers(-2, 3, (M, K)).astype(np.float32)
+        B = rng.integers(-2, 3, (K, N)).astype(np.float32)
+        a = (A.view(np.uint32) >> 16).astype(np.uint16)
+        b = (B.view(np.uint32) >> 16).astype(np.uint16)
+        dt, esz, units = U.BF16, 2, 512
+    else:
+        a = synth.f32_sym(3, 0, M * K).reshape(M, K)
+        b = synth.f32_sym(4, 0, K * N).reshape(K, N)
+        dt, esz, units = U.F32, 4, 384
+    C = np.zeros((M, N), np.float32)
+    ma = U.upir_data_map(ctx, a, U.MAP_TO, U.dist(M, K, esz))
+    mb = U.upir_data_map(ctx, b, U.MAP_TO)
+    mc = U.upir_data_map(ctx, C, U.MAP_FROM, U.dist(M, N, 4))
+    s = U.upir_spmd_launch(ctx, U.spmd_desc(7, units, U.TARGET_CLUSTER))
+    U.upir_loop_exec(s, U.loop_desc([0, 0], [M, N], chunk=1, distribute=U.DIST_TEAMS),
+                     U.body(U.BODY_MATMUL, dt, in0=ma, in1=mb, out=mc, ld=(K, N, N), dims=(K, M, N)))
+    U.upir_spmd_end(s)
+    for m in (mc, mb, ma):
+        U.upir_data_unmap(ctx, m)
+    U.upir_sync(ctx)
+    lo, hi = U.upir_dist_owned_rows(M, rank, world)
+    np.save(os.path.join(out_dir, f"mm_{rank}.npy"), C[lo:hi].copy())
+    U.upir_sync(ctx, U.SYNC_WORLD_BARRIER)
+    U.upir_finalize(ctx)
+    dist.destroy_process_group()

@@ -194,10 +194,13 @@ def test_c1_axpy_sum_1e6(ctx, teams, units):
 
 
 # ---- NEXT #1: async two-step sync and chunk-pipelined map -----------------------
-def test_pipelined_map_sections_reduce(ctx):
+@pytest.mark.parametrize("direction", [U.UPDATE_FORWARD, U.UPDATE_FORWARD_ASYNC])
+def test_pipelined_map_sections_reduce(ctx, direction):
     """map(alloc) + per-section forward update + a loop over that section:
     the loop of section k waits only for copy k (overlap), results combine
-    with a device-scope upir_reduce."""
+    with a device-scope upir_reduce.  FORWARD_ASYNC copies are not ordered
+    after the earlier section loops (they run back to back on the copy
+    stream); the result is the same."""
     n, K = 1_000_000, 8
     x = synth.i64_sym(6, 0, n)
     m = U.upir_data_map(ctx, x, U.MAP_ALLOC)
@@ -208,7 +211,7 @@ def test_pipelined_map_sections_reduce(ctx):
     bounds = np.linspace(0, n, K + 1).astype(np.int64)
     for k in range(K):
         lo, hi = int(bounds[k]), int(bounds[k + 1])
-        U.upir_data_update_section(ctx, m, lo * 8, (hi - lo) * 8, 0)
+        U.upir_data_update_section(ctx, m, lo * 8, (hi - lo) * 8, direction)
         U.upir_loop_exec(s, U.loop_desc(lo, hi), U.body(U.BODY_REDUCE, U.I64, in0=m),
                          [U.reduction(U.OP_SUM, U.I64, parts.data_ptr() + 8 * k)])
     U.upir_spmd_end(s)

@@ -96,3 +96,52 @@ def test_fused_halo_jacobi(upir, tmp_path, world, ny, nx, S, tile, use_graph, ad
     assert np.abs(got - ref).max() <= 1e-5 * np.abs(ref).max()
     one = _jacobi_one_rank(g, S, tile)
     assert (got == one).all()
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("world,n,sched,chunk", [(3, 1_000_003, U.SCHED_STATIC, 0), (3, 1_000_003, U.SCHED_STATIC, 2),
+                                                 (2, 777_777, U.SCHED_STATIC, 4), (3, 1_000_003, U.SCHED_DYNAMIC, 4)])
+def test_block_slices_odd_offsets_world_reduce(upir, tmp_path, world, n, sched, chunk):
+    """C5a pattern with rank offsets that are not multiples of the vector
+    width: the global result on every rank equals the oracle
+    on the whole stream; int64 bit-exact, fp32 within 1e-5 (sum) / exact (max)."""
+    _spawn(peer_worker.block_reduce_worker, world, str(tmp_path), n, sched, chunk)
+    offs = [int(np.load(tmp_path / f"blkoff_{r}.npy")[0]) for r in range(world)]
+    assert any(o % 4 for o in offs)   # at least one rank starts mid-vector
+    xi = synth.i64_sym(6, 0, n)
+    xf = synth.f32_unit(7, 0, n)
+    for r in range(world):
+        got = np.load(tmp_path / f"blk_{r}.npy")
+        assert int(got[0]) == oracle.reduce_i64(oracle.SUM, xi)
+        assert int(got[1]) == oracle.reduce_i64(oracle.MAX, xi)
+        fs, fm = np.frombuffer(got[2:].tobytes(), np.float32)[[0, 2]]
+        rs = oracle.reduce_f32(oracle.SUM, xf)
+        assert abs(float(fs) - rs) <= 1e-5 * rs
+        assert float(fm) == oracle.reduce_f32(oracle.MAX, xf)
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("world,M,N,K,dt", [(2, 600, 512, 256, "bf16"), (3, 1000, 768, 128, "bf16"),
+                                            (2, 768, 512, 320, "int"), (2, 500, 512, 96, "f32")])
+def test_multirank_matmul_block_rows(upir, tmp_path, world, M, N, K, dt):
+    """NEXT #4: rows of A / C BLOCK-sharded, B replicated; the
+    assembled C matches the oracle (small integers: bit-exact, else
+    componentwise-scaled 1e-5) and, for bf16, is bit-identical to one rank."""
+    _spawn(peer_worker.matmul_rows_worker, world, str(tmp_path), M, N, K, dt)
+    got = np.concatenate([np.load(tmp_path / f"mm_{r}.npy") for r in range(world)])
+    assert got.shape == (M, N)
+    if dt == "int":
+        rng = np.random.default_rng(5)
+        A = rng.integers(-2, 3, (M, K)).astype(np.float32)
+        B = rng.integers(-2, 3, (K, N)).astype(np.float32)
+        assert (got == oracle.matmul(A, B)).all()
+        return
+    gen = synth.bf16_sym_as_f32 if dt == "bf16" else synth.f32_sym
+    A = gen(3, 0, M * K).reshape(M, K)
+    B = gen(4, 0, K * N).reshape(K, N)
+    scale = np.abs(A.astype(np.float64)) @ np.abs(B.astype(np.float64))
+    assert (np.abs(got - oracle.matmul(A, B)) / scale).max() <= 1e-5
+    _spawn(peer_worker.matmul_rows_worker, 1, str(tmp_path), M, N, K, dt)
+    one = np.load(tmp_path / "mm_0.npy")
+    if dt == "bf16":
+        assert (got == one).all()

@@ -248,3 +248,70 @@ def test_guided_axpy_f32(ctx, path):
     ref = oracle.axpy(0.5, x, y)
     assert np.abs(yy - ref).max() <= 1e-5 * np.abs(ref).max()
     assert abs(s - oracle.reduce_f32(oracle.SUM, yy)) <= 1e-5 * np.abs(yy).sum()
+
+
+# ---- address alignment: an adopted view with a storage
+# offset is not 16/32-B aligned by element index; the vector paths must align
+# by address (or fall back to scalar accesses when x and y disagree)
+@pytest.mark.parametrize("path", PATHS)
+@pytest.mark.parametrize("off", [1, 2, 3, 5])
+@pytest.mark.parametrize("policy,chunk", [(U.SCHED_STATIC, 0), (U.SCHED_STATIC, 2), (U.SCHED_STATIC, 4),
+                                          (U.SCHED_DYNAMIC, 4)])
+def test_reduce_misaligned_adopted_view(ctx, path, off, policy, chunk):
+    import torch
+    n = 200_003
+    xi = synth.i64_sym(6, 0, n + off)
+    xf = synth.f32_unit(7, 0, n + off)
+    ti = torch.from_numpy(xi).cuda()[off:]
+    tf = torch.from_numpy(xf).cuda()[off:]
+    r = torch.zeros(4, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    mi, mf = U.upir_data_adopt(ctx, ti), U.upir_data_adopt(ctx, tf)
+    b = r.data_ptr()
+    with upir_path(path):
+        s = U.upir_spmd_launch(ctx, U.spmd_desc(37, 128))
+        U.upir_loop_exec(s, U.loop_desc(0, n, policy=policy, chunk=chunk), U.body(U.BODY_REDUCE, U.I64, in0=mi),
+                         [U.reduction(U.OP_SUM, U.I64, b), U.reduction(U.OP_MAX, U.I64, b + 8)])
+        U.upir_loop_exec(s, U.loop_desc(0, n, policy=policy, chunk=chunk), U.body(U.BODY_REDUCE, U.F32, in0=mf),
+                         [U.reduction(U.OP_SUM, U.F32, b + 16), U.reduction(U.OP_MAX, U.F32, b + 24)])
+        U.upir_spmd_end(s)
+    U.upir_sync(ctx)
+    got = r.cpu().numpy()
+    assert int(got[0]) == oracle.reduce_i64(oracle.SUM, xi[off:])
+    assert int(got[1]) == oracle.reduce_i64(oracle.MAX, xi[off:])
+    fs, fm = np.frombuffer(got[2:].tobytes(), np.float32)[[0, 2]]
+    rs = oracle.reduce_f32(oracle.SUM, xf[off:])
+    assert abs(float(fs) - rs) <= 1e-5 * rs
+    assert float(fm) == oracle.reduce_f32(oracle.MAX, xf[off:])
+    U.upir_data_unmap(ctx, mf)
+    U.upir_data_unmap(ctx, mi)
+    U.upir_sync(ctx)
+
+
+@pytest.mark.parametrize("xoff,yoff", [(1, 1), (1, 2), (0, 3), (5, 5)])
+@pytest.mark.parametrize("policy,chunk", [(U.SCHED_STATIC, 0), (U.SCHED_STATIC, 4), (U.SCHED_DYNAMIC, 4)])
+def test_axpy_misaligned_adopted_views(ctx, xoff, yoff, policy, chunk):
+    import torch
+    n = 100_001
+    x = synth.f32_unit(1, 0, n + 8)
+    y = synth.f32_unit(2, 0, n + 8)
+    tx = torch.from_numpy(x).cuda()[xoff:xoff + n]
+    ty_base = torch.from_numpy(y).cuda()
+    ty = ty_base[yoff:yoff + n]
+    r = torch.zeros(1, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+    mx, my = U.upir_data_adopt(ctx, tx), U.upir_data_adopt(ctx, ty)
+    s = U.upir_spmd_launch(ctx, U.spmd_desc(148, 256))
+    U.upir_loop_exec(s, U.loop_desc(0, n, policy=policy, chunk=chunk),
+                     U.body(U.BODY_AXPY, U.F32, in0=mx, out=my, alpha=2.0), [U.reduction(U.OP_SUM, U.F32, r)])
+    U.upir_spmd_end(s)
+    U.upir_sync(ctx)
+    full = ty_base.cpu().numpy()
+    ref = oracle.axpy(2.0, x[xoff:xoff + n], y[yoff:yoff + n])
+    assert (full[yoff:yoff + n] == ref.astype(np.float32)).all()      # 2^-24 grid: exact
+    assert (full[:yoff] == y[:yoff]).all() and (full[yoff + n:] == y[yoff + n:]).all()   # nothing else written
+    rs = oracle.reduce_f32(oracle.SUM, full[yoff:yoff + n])
+    assert abs(r.item() - rs) <= 1e-5 * rs
+    U.upir_data_unmap(ctx, my)
+    U.upir_data_unmap(ctx, mx)
+    U.upir_sync(ctx)

@@ -1,6 +1,6 @@
 """Sweep: AXPY (fused fp32 sum) under schedule(static) block vs. SPMD geometry
 and long-chunk variant (UPIR_DVAR).  Prints GB/s per (teams, units, dvar).
-Run on the GPU box: python tools/debug/axpy_geom.py"""
+Run on the GPU box: python tools/experiments/axpy_geom.py"""
 import os
 import sys
 

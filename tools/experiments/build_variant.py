@@ -1,6 +1,6 @@
 """Experiment builds: libupir.so with one source compiled under extra -D flags.
 
-    python tools/debug/build_variant.py <name> <source.cu> -DFOO=1 ...
+    python tools/experiments/build_variant.py <name> <source.cu> -DFOO=1 ...
 writes build/var/libupir_<name>.so (swap it in on the GPU box to compare)."""
 import os
 import subprocess

@@ -1,6 +1,6 @@
 """Sweep: C3 Jacobi (8192^2, 100 sweeps, one graph) over teams x tile x ring
 depth (UPIR_JACOBI_NST; 0 = the launcher's choice).  Run on the GPU box:
-python tools/debug/jacobi_sweep.py"""
+python tools/experiments/jacobi_sweep.py"""
 import os
 import sys
 import types
