@@ -735,13 +735,14 @@ def line_c5b(E, S=100):
     bm, bn = (int(v) for v in os.environ.get("UPIR_JACOBI_TILE", "16x256").split("x"))
     s = U.upir_spmd_launch(E.ctx, U.spmd_desc(teams, 256, U.TARGET_CLUSTER))
     tch, tfl = jacobi_tile_sched(U)
-    full = U.loop_desc([1, 1], [n - 1, n - 1], tile=[bm, bn], policy=U.SCHED_STATIC, chunk=tch,
+    tpol, tpol_name = jacobi_policy(U)
+    full = U.loop_desc([1, 1], [n - 1, n - 1], tile=[bm, bn], policy=tpol, chunk=tch,
                        distribute=U.DIST_TEAMS, inner_chunk=4, flags=tfl)
     bodies = [(ma, U.body(U.BODY_JACOBI5, U.F32, in0=ma, out=mb, ld=(n, 0, 0), dims=(n, 0, 0))),
               (mb, U.body(U.BODY_JACOBI5, U.F32, in0=mb, out=ma, ld=(n, 0, 0), dims=(n, 0, 0)))]
     # rank-local row ranges of the split sweep (global rows, interior [1, n-1))
     r_lo, r_hi = max(lo, 1), min(hi, n - 1)
-    inner = U.loop_desc([r_lo + 1, 1], [r_hi - 1, n - 1], tile=[bm, bn], policy=U.SCHED_STATIC, chunk=tch,
+    inner = U.loop_desc([r_lo + 1, 1], [r_hi - 1, n - 1], tile=[bm, bn], policy=tpol, chunk=tch,
                         distribute=U.DIST_TEAMS, inner_chunk=4, flags=tfl)
     edges = [U.loop_desc([r, 1], [r + 1, n - 1], tile=[bm, bn], policy=U.SCHED_STATIC, chunk=1,
                          distribute=U.DIST_TEAMS, inner_chunk=4) for r in sorted({r_lo, r_hi - 1})]
@@ -808,7 +809,7 @@ def line_c5b(E, S=100):
     del a_t, b_t
     vals = list(checks.values())
     return {"workload": f"C5b: Jacobi 5-point {n}x{n} fp32, {S} sweeps as one CUDA graph, BLOCK row slabs over "
-                        f"{E.world} GPU(s) with 1-row halos, tiles {bm}x{bn} static,{tch}{' column-major' if tfl else ''} "
+                        f"{E.world} GPU(s) with 1-row halos, tiles {bm}x{bn} {tpol_name},{tch}{' column-major' if tfl else ''} "
                         f"over {teams} teams",
             "grid_bytes": 4 * n * n,
             "metric": "GLUP/s of the whole job ((n-2)^2 x 100 lattice updates)", "scaling": "strong",
@@ -865,6 +866,12 @@ def jacobi_tile_sched(U):
     return chunk, flags
 
 
+def jacobi_policy(U, default="static"):
+    """Tile-loop schedule kind of a Jacobi line (sweep hook UPIR_JACOBI_POLICY)."""
+    p = os.environ.get("UPIR_JACOBI_POLICY", default)
+    return {"static": U.SCHED_STATIC, "dynamic": U.SCHED_DYNAMIC}[p], p
+
+
 # --------------------------------------------------------------------------- kernel lines (N = 1)
 def bench_axpy(E):
     """a6 axpy y = y + a*x with a fused fp32 sum (C1 body) at n = 2^28."""
@@ -912,7 +919,8 @@ def bench_jacobi(E, ny=8192, nx=8192, S=100):
     teams = int(os.environ.get("UPIR_JACOBI_TEAMS", 444))
     bm, bn = (int(v) for v in os.environ.get("UPIR_JACOBI_TILE", "16x256").split("x"))
     tch, tfl = jacobi_tile_sched(U)
-    loop = U.loop_desc([1, 1], [ny - 1, nx - 1], tile=[bm, bn], policy=U.SCHED_STATIC, chunk=tch,
+    tpol, tpol_name = jacobi_policy(U)
+    loop = U.loop_desc([1, 1], [ny - 1, nx - 1], tile=[bm, bn], policy=tpol, chunk=tch,
                        distribute=U.DIST_TEAMS, inner_chunk=4, flags=tfl)
     s = U.upir_spmd_launch(E.ctx, U.spmd_desc(teams, 256))
     bodies = [U.body(U.BODY_JACOBI5, U.F32, in0=ma, out=mb, ld=(nx, 0, 0), dims=(ny, 0, 0)),
@@ -934,7 +942,7 @@ def bench_jacobi(E, ny=8192, nx=8192, S=100):
     U.upir_data_unmap(E.ctx, mb)
     U.upir_sync(E.ctx)
     return {"workload": f"C3: Jacobi 5-point {ny}x{nx} fp32, {S} sweeps (one CUDA graph), tiles {bm}x{bn} "
-                        f"static,{tch}{' column-major' if tfl else ''} over {teams} teams, static,4 over 256 units",
+                        f"{tpol_name},{tch}{' column-major' if tfl else ''} over {teams} teams, static,4 over 256 units",
             "ms_per_100_sweeps": ms, "GLUP/s": glups, "bound": "hbm",
             "summary": {"C3": dict(value=glups, unit="GLUP/s", **fracs(gbs, E.peak))},
             "roofline": {"achieved": gbs, "peak": E.peak, "unit": "GB/s", "frac": gbs / E.peak,

@@ -308,11 +308,17 @@ typedef struct {
  *            (collapse 2, k sequential inside the iteration); in0 = A (M x K),
  *            in1 = B (K x N), out = C (M x N fp32), row-major; dims = (K, M,
  *            N), ld = (lda, ldb, ldc) in elements (multiples of 8).  dtype
- *            BF16: bf16 inputs, fp32 accumulation on tcgen05 tensor cores,
- *            teams of exactly 256 units; F32: fp32 inputs via 3xTF32
- *            (kind::tf32, hi/lo split in shared memory), teams of exactly 384
- *            units.  The tile loop (128 x 256 tiles) runs over the teams;
- *            other unit counts are rejected, never clamped.
+ *            BF16: bf16 inputs, fp32 accumulation on tcgen05 tensor cores;
+ *            F32: fp32 inputs via 3xTF32 (kind::tf32, D += lo_a*hi_b +
+ *            hi_a*lo_b + hi_a*hi_b; A and B are split into tf32 hi / lo
+ *            copies in HBM by one elementwise pass before the loop kernel).
+ *            Team geometry (the tile loop runs over the teams, reading c24):
+ *              BF16, 256 units: one CTA per team, 128 x 256 tiles;
+ *              BF16, 512 units: a team is a 2-CTA cluster (CTA pair,
+ *                tcgen05.mma.cta_group::2), 256 x 256 tiles;
+ *              F32, 384 units: one CTA per team, 128 x 256 tiles;
+ *              F32, 768 units: CTA pair, 256 x 256 tiles.
+ *            Other unit counts are rejected (UPIR_E_INVALID), never clamped.
  *  MATVEC  : y[i] = sum_k A[i][k] * x[k] over the loop's rows i (collapse 1,
  *            step 1, the paper's fourth kernel); in0 = A (M x K
  *            fp32, row pitch ld[0]), in1 = x (K), out = y (M); dims = (K, M).
@@ -324,7 +330,8 @@ typedef struct {
  *            (the paper's "2D stencil, filter size = 7"; the
  *            weights are an input, reading c28); in0 = in, in1 = w (F x F
  *            fp32, F = 2R+1 in {3,5,7}), out = out; ld[0] = row pitch,
- *            dims = (ny, F).  Tiled like JACOBI5 (tiles 16x128 or 8x64).
+ *            dims = (ny, F).  Tiled like JACOBI5 (tiles BM x BN in {16x128,
+ *            8x64, 16x512, 16x1024, 8x512, 8x1024, 8x256, 4x512, 4x256}).
  * The element index used by a body is the induction value itself (global
  * index; for distributed maps the runtime subtracts the local offset). */
 typedef enum { UPIR_BODY_AXPY = 0, UPIR_BODY_REDUCE = 1, UPIR_BODY_JACOBI5 = 2,

@@ -5,13 +5,18 @@
 // schedule (static block / static,c / dynamic); inside a tile the BM x BN box
 // positions are scheduled static,ic over UNITS.
 //
-// B200 design: each team (CTA) walks its tiles with a 2-deep TMA pipeline:
-// while it computes tile t from shared memory, one elected thread has the
-// next tile's (BM+2) x BN centre box and two (BM+2) x 4 halo-column boxes in
-// flight (cp.async.bulk.tensor.2d, mbarrier complete_tx; out-of-range rows /
-// columns are zero-filled by the TMA unit and never written).  Results are
-// stored as coalesced 16-B vectors.  Every input element is read from HBM
-// once per sweep (neighbour tiles' halos hit L2): 8 B per lattice update.
+// B200 design: each team (CTA) walks its tiles through an NST-slot ring of
+// windows -- the tile's (BM+2) x BN centre box and two (BM+2) x 4 halo-column
+// boxes (cp.async.bulk.tensor.2d, mbarrier complete_tx; out-of-range rows /
+// columns are zero-filled by the TMA unit and never written).  A dedicated
+// producer warp (it executes no iterations, reading c34) claims the tiles in
+// schedule order, computes each origin once and refills a slot as soon as
+// every unit thread has released it (per-thread arrivals on the slot's empty
+// mbarrier); unit warps wait only on their slot's full barrier, never on a
+// CTA-wide barrier.  Interior tiles take a lean path (int32 tile-relative
+// indexing, west / east neighbours by warp shuffle).  Results are stored as
+// coalesced 16-B vectors.  Every input element is read from HBM about once
+// per sweep (neighbour tiles' halos hit L2): 8 B per lattice update.
 // fp32 arithmetic with explicit __fadd_rn/__fmul_rn: no FMA contraction, so
 // the result is independent of decomposition (1 vs N GPUs bit-identical).
 //

@@ -24,6 +24,7 @@
 #include <math_constants.h>
 #include <stdint.h>
 
+#include <cstdlib>
 #include <type_traits>
 
 #include "dev_peer.cuh"
@@ -284,7 +285,7 @@ __device__ __forceinline__ void direct_long(const StreamArgs &a, int64_t elo, in
   for (; e < ehi; ++e) body_scalar<BODY, NRED, false>(a, e, acc, 0, 0);
 }
 
-template <int BODY, int NRED, bool TRACE>
+template <int BODY, int NRED, bool TRACE, int LB = 1024>
 __device__ void direct_run(const StreamArgs &a, const LaneWork &w, Acc<BODY, NRED> &acc, int team,
                            int unit) {
   if (w.nk == 0) return;
@@ -728,8 +729,8 @@ __device__ void reduce_epilogue(const StreamArgs &a, Acc<BODY, NRED> &acc, bool 
 }
 
 // ================================================================ kernel
-template <int BODY, int NRED, bool TRACE, int PATH, int SEGV, int NST>
-__global__ void __launch_bounds__(1024) stream_loop_kernel(const __grid_constant__ StreamArgs a) {
+template <int BODY, int NRED, bool TRACE, int PATH, int SEGV, int NST, int LB = 1024>
+__global__ void __launch_bounds__(LB, LB <= 256 ? 2 : 1) stream_loop_kernel(const __grid_constant__ StreamArgs a) {
   extern __shared__ __align__(128) char dyn_smem[];
   const UnitIds u = unit_ids(a.distribute);
   const int team = blockIdx.x, unit = threadIdx.x;
@@ -744,7 +745,7 @@ __global__ void __launch_bounds__(1024) stream_loop_kernel(const __grid_constant
 
   auto run = [&](const LaneWork &w) {
     if constexpr (PATH == PATH_STAGED) staged_run<BODY, NRED, TRACE, SEGV, NST>(a, w, acc, team, unit, wsm, sglob);
-    else direct_run<BODY, NRED, TRACE>(a, w, acc, team, unit);
+    else direct_run<BODY, NRED, TRACE, LB>(a, w, acc, team, unit);
   };
 
   if (a.sched == SK_DYNAMIC || a.sched == SK_GUIDED) {
@@ -786,6 +787,16 @@ cudaError_t launch_stream_body(int nred, int path, int segv, int nst, bool trace
     if (trace) { UPIR_PICK(2, true) } else { UPIR_PICK(2, false) }
   }
 #undef UPIR_PICK
+  // teams of <= 256 units: the direct kernel compiled for 256 threads (up to
+  // 255 registers: the AXPY long-chunk loop keeps 4 x 2 x 32 B of x / y in
+  // flight per unit without spilling, which the 64-register bound of a
+  // 1024-thread compile cannot)
+  // (AXPY by default; experiment hook UPIR_LB256 = 0 never / 1 every body)
+  const int lb256 = getenv("UPIR_LB256") ? atoi(getenv("UPIR_LB256")) : -1;
+  if (path == PATH_DIRECT && !trace && units <= 256 && (lb256 == 1 || (lb256 < 0 && BODY == SB_AXPY)))
+    k = nred == 0 ? stream_loop_kernel<BODY, 0, false, PATH_DIRECT, 0, 0, 256>
+        : nred == 1 ? stream_loop_kernel<BODY, 1, false, PATH_DIRECT, 0, 0, 256>
+                    : stream_loop_kernel<BODY, 2, false, PATH_DIRECT, 0, 0, 256>;
   if (!k) return cudaErrorInvalidValue;
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

@@ -1194,7 +1194,6 @@ static upir_status exec_stream(upir_spmd s, const upir_loop_desc *l, const upir_
   // Default: DIRECT (long per-unit chunks use 256-bit loads with a 256-B L2
   // prefetch, measured at ~1.0x the copy bandwidth on B200, above the staged
   // variant); UPIR_PATH=staged selects the TMA-bulk staged path.
-  (void)unit_chunk;
   bool staged = false;
   const char *ep = env_path();
   if (!strcmp(ep, "direct")) staged = false;
@@ -1225,6 +1224,16 @@ static upir_status exec_stream(upir_spmd s, const upir_loop_desc *l, const upir_
     }
   }
   if (!staged) { segv = 0; nst = 0; smem = 0; }
+  // AXPY with long per-unit chunks (static block): every unit streams its own
+  // x, y and y' ranges -- 3 DRAM streams per unit.  Measured best with 2 x
+  // 32-B loads per array in flight per unit (dvar 1, no line alignment) and
+  // ONE resident team per SM (fewer concurrent streams, better DRAM row
+  // locality): 0.69 -> 0.82 of the copy bandwidth at 592 x 256 over 2^28
+  // (tools/sweep_r2.py); reserved dynamic shared memory enforces the
+  // residency (the direct path uses none).
+  const bool axpy_long = body == SB_AXPY && !staged && unit_chunk >= 256 && sd.num_units <= 256;
+  if (axpy_long && !getenv("UPIR_DVAR")) a.dvar = 1;
+  if (axpy_long && !getenv("UPIR_DIRECT_OCC")) smem = (size_t)(228 * 1024) / 2 + 1024;
   // experiment hook UPIR_DIRECT_OCC = k: reserve dynamic shared memory so
   // that at most k teams are resident per SM (fewer concurrent per-unit
   // streams; the direct path itself uses no dynamic shared memory)

@@ -215,6 +215,6 @@ def matmul_rows_worker(rank, world, port, out_dir, M, N, K, dtype_name):
     U.upir_sync(ctx)
     lo, hi = U.upir_dist_owned_rows(M, rank, world)
     np.save(os.path.join(out_dir, f"mm_{rank}.npy"), C[lo:hi].copy())
-    U.upir_sync(ctx, U.SYNC_WORLD_BARRIER)
+    dist.barrier()   # no collective on the data path: host barrier only
     U.upir_finalize(ctx)
     dist.destroy_process_group()

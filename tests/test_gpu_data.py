@@ -275,3 +275,49 @@ def test_async_halo_join_overlapped_sweeps(ctx):
     with pytest.raises(U.UpirError) as ei:
         U.upir_sync(ctx, U.SYNC_JOIN)
     assert ei.value.status == U.E_SYNC
+
+
+def test_async_halo_join_graph_capture(ctx):
+    """The split sweep (async HALO on the copy stream, interior rows, JOIN,
+    boundary rows) captured as one CUDA graph -- the form bench.py times for
+    C5b -- replays to the same bits as eager synchronous sweeps."""
+    ny, nx, S = 66, 520, 8
+    g = synth.jacobi_init(ny, nx)
+    d = U.dist(ny, nx, 4, halo_rows=1)
+    res = []
+    for graph in (False, True):
+        a, b = g.copy(), g.copy()
+        ma = U.upir_data_map(ctx, a, U.MAP_TOFROM, d)
+        mb = U.upir_data_map(ctx, b, U.MAP_TOFROM, d)
+        s = U.upir_spmd_launch(ctx, U.spmd_desc(7, 256, U.TARGET_CLUSTER))
+        bodies = [(ma, U.body(U.BODY_JACOBI5, U.F32, in0=ma, out=mb, ld=(nx, 0, 0), dims=(ny, 0, 0))),
+                  (mb, U.body(U.BODY_JACOBI5, U.F32, in0=mb, out=ma, ld=(nx, 0, 0), dims=(ny, 0, 0)))]
+        full = U.loop_desc([1, 1], [ny - 1, nx - 1], tile=[16, 256], distribute=U.DIST_TEAMS, inner_chunk=4)
+        inner = U.loop_desc([2, 1], [ny - 2, nx - 1], tile=[16, 256], distribute=U.DIST_TEAMS, inner_chunk=4)
+        edges = [U.loop_desc([r, 1], [r + 1, nx - 1], tile=[16, 256], distribute=U.DIST_TEAMS, inner_chunk=4)
+                 for r in (1, ny - 2)]
+        if graph:
+            U.upir_graph_begin(ctx)
+            for k in range(S):
+                src, body = bodies[k % 2]
+                tok = U.upir_sync(ctx, U.SYNC_HALO, halo_map=src, async_=True)
+                U.upir_loop_exec(s, inner, body)
+                U.upir_sync(ctx, U.SYNC_JOIN, token=tok)
+                for e in edges:
+                    U.upir_loop_exec(s, e, body)
+            gr = U.upir_graph_end(ctx)
+            U.upir_graph_launch(ctx, gr)
+            U.upir_sync(ctx)
+            U.upir_graph_destroy(gr)
+        else:
+            for k in range(S):
+                src, body = bodies[k % 2]
+                U.upir_sync(ctx, U.SYNC_HALO, halo_map=src)
+                U.upir_loop_exec(s, full, body)
+        U.upir_spmd_end(s)
+        U.upir_data_unmap(ctx, mb)
+        U.upir_data_unmap(ctx, ma)
+        U.upir_sync(ctx)
+        res.append(a if S % 2 == 0 else b)
+    assert (res[0] == res[1]).all()
+    assert np.abs(res[0] - oracle.jacobi5(g, S)).max() <= 1e-5

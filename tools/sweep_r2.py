@@ -33,28 +33,39 @@ def main():
     E = bench.Env(args_ns())
     out = []
     if "axpy" in what:
-        for occ in (None, 1, 2, 3):
-            for dvar in (None, 1, 4, 7, 9):
-                setenv(UPIR_DIRECT_OCC=occ, UPIR_DVAR=dvar)
-                r = bench.bench_axpy(E)
-                out.append({"axpy": {"occ": occ, "dvar": dvar, **r["summary"]}})
-                print(json.dumps(out[-1]), flush=True)
-        setenv(UPIR_DIRECT_OCC=None, UPIR_DVAR=None)
+        for lb in (None, 0):
+            for occ in (None, 1):
+                for dvar in (None, 1, 4, 7, 9):
+                    setenv(UPIR_DIRECT_OCC=occ, UPIR_DVAR=dvar, UPIR_LB256=lb)
+                    r = bench.bench_axpy(E)
+                    out.append({"axpy": {"lb256": lb, "occ": occ, "dvar": dvar, **r["summary"]}})
+                    print(json.dumps(out[-1]), flush=True)
+        setenv(UPIR_DIRECT_OCC=None, UPIR_DVAR=None, UPIR_LB256=None)
+    if "reduce" in what:
+        for lb in (None, 1):
+            setenv(UPIR_LB256=lb)
+            r = bench.bench_c2(E)
+            out.append({"reduce": {"lb256": lb, **r["summary"]}})
+            print(json.dumps(out[-1]), flush=True)
+            E.free()
+        setenv(UPIR_LB256=None)
     for key, fn in (("jacobi", bench.bench_jacobi), ("c5b", bench.line_c5b)):
         if key not in what:
             continue
-        for order, chunk in (("row", 1), ("row", 2), ("col", 1), ("col", 4), ("col", 8), ("col", 16), ("col", 32)):
+        cfgs = [(pol, "row", c) for pol in ("static", "dynamic") for c in (1, 2, 4)]
+        for pol, order, chunk in cfgs:
             for teams in (444, 296):
-                setenv(UPIR_JACOBI_ORDER=order, UPIR_JACOBI_CHUNK=chunk, UPIR_JACOBI_TEAMS=teams)
+                setenv(UPIR_JACOBI_ORDER=order, UPIR_JACOBI_CHUNK=chunk, UPIR_JACOBI_TEAMS=teams,
+                       UPIR_JACOBI_POLICY=pol)
                 try:
                     r = fn(E)
                     summ = r.get("summary") or {k: v for k, v in r["paths"].items()}
                 except Exception as e:
                     summ = {"error": str(e)[:200]}
-                out.append({key: {"order": order, "chunk": chunk, "teams": teams, **summ}})
+                out.append({key: {"policy": pol, "order": order, "chunk": chunk, "teams": teams, **summ}})
                 print(json.dumps(out[-1]), flush=True)
                 E.free()
-        setenv(UPIR_JACOBI_ORDER=None, UPIR_JACOBI_CHUNK=None, UPIR_JACOBI_TEAMS=None)
+        setenv(UPIR_JACOBI_ORDER=None, UPIR_JACOBI_CHUNK=None, UPIR_JACOBI_TEAMS=None, UPIR_JACOBI_POLICY=None)
     E.U.upir_finalize(E.ctx)
 
 
