@@ -734,8 +734,12 @@ def line_c5b(E, S=100):
     teams = int(os.environ.get("UPIR_JACOBI_TEAMS", 444))
     bm, bn = (int(v) for v in os.environ.get("UPIR_JACOBI_TILE", "16x256").split("x"))
     s = U.upir_spmd_launch(E.ctx, U.spmd_desc(teams, 256, U.TARGET_CLUSTER))
+    # C5b fixes no schedule (BASELINE configs[4]): dynamic,1 keeps the teams'
+    # tile front tight, so a tile's halo rows are still in L2 when the tile
+    # below loads them (ncu: 4.30 GB read per sweep vs 4.61 GB under static,1,
+    # whose persistent teams drift apart)
     tch, tfl = jacobi_tile_sched(U)
-    tpol, tpol_name = jacobi_policy(U)
+    tpol, tpol_name = jacobi_policy(U, default="dynamic")
     full = U.loop_desc([1, 1], [n - 1, n - 1], tile=[bm, bn], policy=tpol, chunk=tch,
                        distribute=U.DIST_TEAMS, inner_chunk=4, flags=tfl)
     bodies = [(ma, U.body(U.BODY_JACOBI5, U.F32, in0=ma, out=mb, ld=(n, 0, 0), dims=(n, 0, 0))),
@@ -814,7 +818,9 @@ def line_c5b(E, S=100):
             "grid_bytes": 4 * n * n,
             "metric": "GLUP/s of the whole job ((n-2)^2 x 100 lattice updates)", "scaling": "strong",
             "n_gpus": E.world, "rows_identical_across_paths": all(v == vals[0] for v in vals),
-            "kernel": f"jacobi5_kernel<{bm},{bn}>", "paths": paths}
+            "kernel": f"jacobi5_kernel<{bm},{bn}>", "paths": paths,
+            "traffic_per_sweep_1gpu": {"dynamic,2": ncu_traffic("jacobi32k"), "static,1": ncu_traffic("jacobi32k_static"),
+                                       "algorithmic": 8 * (n - 2) * (n - 2), "unit": "DRAM bytes (ncu)"}}
 
 
 def line_matmul_rows(E, n=8192):
@@ -902,7 +908,9 @@ def bench_axpy(E):
     U.upir_data_unmap(E.ctx, my)
     U.upir_sync(E.ctx)
     return {"workload": "axpy y=y+2x + fused fp32 sum, n=2^28, 592x256, 12 B/iter", "bound": "hbm",
-            "peak_source": E.peak_src, "summary": summ, **out}
+            "peak_source": E.peak_src, "summary": summ,
+            "traffic": {"static": ncu_traffic("axpy"), "static4": ncu_traffic("axpy4"),
+                        "algorithmic": 12 * n, "unit": "DRAM bytes per launch (ncu)"}, **out}
 
 
 def bench_jacobi(E, ny=8192, nx=8192, S=100):
@@ -1080,7 +1088,7 @@ def bench_matmul(E, n=8192):
             "roofline": {"bound": "tensor", "achieved": res[bf]["TFLOP/s"], "peak": peak, "unit": "TFLOP/s",
                          "frac": res[bf]["frac"], "peak_source": E.peak_src + " bf16 burst",
                          "fp32_peak": "tf32 = bf16 x 1/2 (nominal ratio); 3xTF32 bar = tf32 / 3",
-                         "traffic": ncu_traffic("matmul")},
+                         "traffic": ncu_traffic("matmul_pair")},
             **res}
 
 

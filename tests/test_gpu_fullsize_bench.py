@@ -86,7 +86,7 @@ def test_c4_f32_3xtf32_8192_sampled_rows(ctx, teams, units, rows):
     _check_rows(C, rows, synth.f32_sym)
 
 
-def _jacobi_run(ctx, n, S, teams, bm, bn, cluster):
+def _jacobi_run(ctx, n, S, teams, bm, bn, cluster, policy=U.SCHED_STATIC):
     """The bench's Jacobi geometry: S sweeps captured as one CUDA graph."""
     import torch
     if cluster:
@@ -98,7 +98,7 @@ def _jacobi_run(ctx, n, S, teams, bm, bn, cluster):
     mb = U.upir_data_adopt(ctx, b_t, d) if cluster else U.upir_data_adopt(ctx, b_t)
     U.upir_synth_fill(ctx, ma, 4, 5, 0, n, n)
     U.upir_synth_fill(ctx, mb, 4, 5, 0, n, n)
-    loop = U.loop_desc([1, 1], [n - 1, n - 1], tile=[bm, bn], policy=U.SCHED_STATIC, chunk=1,
+    loop = U.loop_desc([1, 1], [n - 1, n - 1], tile=[bm, bn], policy=policy, chunk=1,
                        distribute=U.DIST_TEAMS, inner_chunk=4)
     s = U.upir_spmd_launch(ctx, U.spmd_desc(teams, 256, U.TARGET_CLUSTER if cluster else U.TARGET_GPU))
     bodies = [U.body(U.BODY_JACOBI5, U.F32, in0=ma, out=mb, ld=(n, 0, 0), dims=(n, 0, 0)),
@@ -145,11 +145,13 @@ def test_c3_bench_geometry_windows(ctx):
     _check_windows(res, n, S, corners)
 
 
-def test_c5b_32768_one_gpu_windows(ctx):
+@pytest.mark.parametrize("policy", [U.SCHED_DYNAMIC, U.SCHED_STATIC])
+def test_c5b_32768_one_gpu_windows(ctx, policy):
     """C5b on one GPU: 32768^2 (4 GiB per grid), 100 sweeps, CLUSTER target
-    with BLOCK maps as bench.py runs it at N = 1."""
+    with BLOCK maps as bench.py runs it at N = 1 (dynamic,1 tile loop; and
+    static,1)."""
     n, S = 32768, 100
-    res = _jacobi_run(ctx, n, S, 444, 16, 256, cluster=True)
+    res = _jacobi_run(ctx, n, S, 444, 16, 256, cluster=True, policy=policy)
     corners = [(0, 0), (0, n - 16), (n - 16, 0), (n - 16, n - 16)]
     cols = [0, 16384 - 8, n - 16]
     for k in range(1, 8):   # the would-be slab boundaries of an 8-GPU split

@@ -1,12 +1,12 @@
 #!/bin/bash
 # Exercise bench.py's N > 1 code on a one-GPU box: every rank on cuda:0,
-# gloo host plumbing, communicator-less upir world (peer windows only).
-# Numbers printed here are NOT bench values (ranks time-slice one GPU).
-set -x
-R=torch.distributed.run
-for wl in reduce reduce34 jacobi32k; do
-  UPIR_BENCH_SHARED_GPU=1 UPIR_C5A_LOG2=24 UPIR_C5B_N=2048 timeout 300 python -m $R --nnodes=1 --nproc-per-node 2 \
-    --master-addr 127.0.0.1 --master-port $((29500 + RANDOM % 1000)) bench.py --gpus 2 --steps 3 --warmup 3 \
-    --n-log2 24 --e2e-steps 1 --workload $wl
-  echo "rc[$wl]=$?"
+# gloo host plumbing, communicator-less upir world (peer windows only; the
+# NCCL lines report "unavailable").  Numbers printed here are NOT bench
+# values (the ranks time-slice one GPU).
+cd "${GRAFT_REPO_ROOT:-$(dirname "$0")/..}"
+mkdir -p gpurun_out
+for n in 2 3; do
+  UPIR_BENCH_SHARED_GPU=1 UPIR_C5A_LOG2=26 UPIR_C5B_N=4096 timeout 600 python bench.py --gpus $n --steps 3 \
+    --warmup 3 --n-log2 26 --e2e-steps 1 --no-kernels > gpurun_out/shared_$n.json 2> gpurun_out/shared_$n.err
+  echo "rc[N=$n]=$?"
 done

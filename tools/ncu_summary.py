@@ -33,6 +33,9 @@ KEYS = [
     "sm__pipe_tensor_op_hmma_cycles_active.avg.pct_of_peak_sustained_elapsed",
     "sm__cycles_elapsed.avg.per_second",
     "l1tex__t_bytes.sum",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "lts__t_sector_hit_rate.pct",
+    "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active",
 ]
 
 
@@ -88,29 +91,7 @@ def main():
             wb = to_bytes(*d["dram__bytes_write.sum"]) if "dram__bytes_write.sum" in d else None
             if rb is not None and wb is not None:
                 lines.append(f"dram_traffic_bytes = {rb + wb:.0f}")
-                key = None
-                if name in ("jacobi32k", "reduce34"):
-                    key = {"jacobi32k": "jacobi32k", "reduce34": "reduce_i64_1"}[name]
-                elif "matmul_pair_f32" in kname:
-                    key = "matmul_pair_f32"
-                elif "stream_loop_kernel<0" in kname:
-                    key = "reduce_i64"
-                elif "stream_loop_kernel<1" in kname:
-                    key = "reduce_f32"
-                elif "stream_loop_kernel<2" in kname:
-                    key = "axpy"
-                elif "jacobi5" in kname:
-                    key = "jacobi"
-                elif "matmul_pair_kernel" in kname:
-                    key = "matmul_pair"
-                elif "matmul_kernel<2>" in kname or "matmul_kernel<(int)2>" in kname:
-                    key = "matmul_f32"
-                elif "matmul" in kname:
-                    key = "matmul"
-                elif "matvec" in kname:
-                    key = "matvec"
-                elif "stencil" in kname:
-                    key = "stencil7"
+                key = name   # the profile name of tools/prof_all.sh (= the bench's traffic key)
                 if key and key not in traffic.get("_seen_" + tag, []):
                     traffic[key] = rb + wb
                     traffic.setdefault("_seen_" + tag, []).append(key)

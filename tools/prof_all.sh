@@ -1,21 +1,29 @@
 #!/bin/bash
 # bench + launch list + ncu --set full of every loop-body kernel (1 B200).
+#   TAG=r02 bash tools/prof_all.sh        (under gpurun)
+# Each capture runs tools/one_kernel.py: the kernel's bench configuration,
+# launched twice; ncu records the second launch (-s 1 -c 1).
 cd "$GRAFT_REPO_ROOT"
-TAG=${TAG:-r01}
-timeout 900 python bench.py > gpurun_out/bench.log 2>&1; tail -1 gpurun_out/bench.log | cut -c1-300
-timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
-B="python bench.py --steps 1 --warmup 0 --e2e-steps 0 --no-cpu-baseline"
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:stream_loop -c 2 -o gpurun_out/prof_reduce -f $B --no-kernels > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:stream_loop -s 2 -c 1 -o gpurun_out/prof_axpy -f $B > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:jacobi5 -s 10 -c 1 -o gpurun_out/prof_jacobi -f $B > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:matmul_kernel -s 3 -c 1 -o gpurun_out/prof_matmul -f $B > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:matmul_pair_kernel -s 3 -c 1 -o gpurun_out/prof_matmul_pair -f $B > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:matmul_kernel -s 6 -c 1 -o gpurun_out/prof_matmul_f32 -f $B > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:matmul_pair_f32 -s 2 -c 1 -o gpurun_out/prof_matmul_pair_f32 -f $B > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:jacobi5 -s 5 -c 1 -o gpurun_out/prof_jacobi32k -f python bench.py --workload jacobi32k --steps 1 --warmup 0 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:matvec -s 3 -c 1 -o gpurun_out/prof_matvec -f $B > /dev/null 2>&1
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:stencil_kernel -s 55 -c 1 -o gpurun_out/prof_stencil7 -f $B > /dev/null 2>&1
+TAG=${TAG:-r02}
+mkdir -p gpurun_out
+timeout 900 python bench.py --steps 20 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/bench.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv \
+  python bench.py --steps 3 --warmup 3 --e2e-steps 0 --no-cpu-baseline > /dev/null 2>&1
+prof() {   # name kernel-regex one_kernel-mode [env...]
+  local name=$1 re=$2 mode=$3; shift 3
+  env "$@" timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$re" -s 1 -c 1 \
+    -o gpurun_out/prof_$name -f python tools/one_kernel.py $mode > gpurun_out/prof_$name.log 2>&1
+}
+prof reduce_i64 stream_loop reduce_i64
+prof reduce_f32 stream_loop reduce_f32
+prof axpy stream_loop axpy_static
+prof axpy4 stream_loop axpy_static4
+prof jacobi jacobi5 jacobi_c3
+prof jacobi32k jacobi5 jacobi_c5b UPIR_JACOBI_POLICY=dynamic UPIR_JACOBI_CHUNK=2
+prof jacobi32k_static jacobi5 jacobi_c5b
+prof matmul_pair matmul_pair_kernel matmul_pair
+prof matmul_pair_f32 matmul_pair_f32 matmul_f32_pair
+prof matvec matvec matvec
+prof stencil7 stencil_kernel stencil7
 UPIR_PROFILES_OUT=gpurun_out/profiles python tools/ncu_summary.py $TAG gpurun_out/prof_*.ncu-rep
-mkdir -p /tmp/ncu_keep && mv gpurun_out/prof_*.ncu-rep /tmp/ncu_keep/
-cp /tmp/ncu_keep/prof_jacobi.ncu-rep /tmp/ncu_keep/prof_stencil7.ncu-rep gpurun_out/ 2>/dev/null
 ls -la gpurun_out gpurun_out/profiles

@@ -52,20 +52,23 @@ def main():
     for key, fn in (("jacobi", bench.bench_jacobi), ("c5b", bench.line_c5b)):
         if key not in what:
             continue
-        cfgs = [(pol, "row", c) for pol in ("static", "dynamic") for c in (1, 2, 4)]
-        for pol, order, chunk in cfgs:
-            for teams in (444, 296):
+        cfgs = [("static", sk, c) for sk in ("0", "3", "4", "5", "8", "12") for c in (1, 2)] + \
+               [("dynamic", None, c) for c in (1, 2)]
+        for pol, skew, chunk in cfgs:
+            order = "row"
+            for teams in (444,):
                 setenv(UPIR_JACOBI_ORDER=order, UPIR_JACOBI_CHUNK=chunk, UPIR_JACOBI_TEAMS=teams,
-                       UPIR_JACOBI_POLICY=pol)
+                       UPIR_JACOBI_POLICY=pol, UPIR_JACOBI_SKEW=skew)
                 try:
                     r = fn(E)
                     summ = r.get("summary") or {k: v for k, v in r["paths"].items()}
                 except Exception as e:
                     summ = {"error": str(e)[:200]}
-                out.append({key: {"policy": pol, "order": order, "chunk": chunk, "teams": teams, **summ}})
+                out.append({key: {"policy": pol, "skew": skew, "chunk": chunk, "teams": teams, **summ}})
                 print(json.dumps(out[-1]), flush=True)
                 E.free()
-        setenv(UPIR_JACOBI_ORDER=None, UPIR_JACOBI_CHUNK=None, UPIR_JACOBI_TEAMS=None, UPIR_JACOBI_POLICY=None)
+        setenv(UPIR_JACOBI_ORDER=None, UPIR_JACOBI_CHUNK=None, UPIR_JACOBI_TEAMS=None, UPIR_JACOBI_POLICY=None,
+               UPIR_JACOBI_SKEW=None)
     E.U.upir_finalize(E.ctx)
 
 
