@@ -64,11 +64,16 @@ __global__ void __launch_bounds__(MAXT + (PW ? 32 : 0)) stencil_kernel(const __g
   constexpr int F = L::F, WR = L::WR, WCP = L::WC;
   extern __shared__ __align__(128) char smc[];
   constexpr int NST = L::NST;
-  uint64_t *bars = reinterpret_cast<uint64_t *>(smc + NST * L::BUF);
-  // bars: full[NST] (TMA landed / end marker), empty[NST] (every unit-warp thread done with the buffer)
+  // full[NST][NWB] (TMA landed / end marker; strip path: one barrier per warp
+  // strip, so a warp waits only for its own box), empty[NST] (every unit-warp
+  // thread done with the buffer)
+  constexpr int NWB = L::NS > 0 ? L::NS : 1;
+  uint64_t *full = reinterpret_cast<uint64_t *>(smc + NST * L::BUF);
+  uint64_t *empty = full + NST * NWB;
+  static_assert((NST * NWB + NST) * 8 <= 192, "barrier block");
   // per slot: tile id, first row, first column (written by the producer
-  // before the slot's full barrier completes)
-  volatile long long *tile_s = reinterpret_cast<volatile long long *>(smc + NST * L::BUF + 64);   // [NST][3]
+  // before the slot's full barriers complete)
+  volatile long long *tile_s = reinterpret_cast<volatile long long *>(smc + NST * L::BUF + 192);   // [NST][3]
   float *w = reinterpret_cast<float *>(smc + NST * L::BUF + 256);
   __shared__ unsigned s_last;
   const int units = a.units, u = threadIdx.x;
@@ -112,24 +117,26 @@ __global__ void __launch_bounds__(MAXT + (PW ? 32 : 0)) stencil_kernel(const __g
   auto issue = [&](int64_t i0, int64_t j0, int buf) {
     tma_fence_proxy();
     if (strip) {
-      tma_mbar_expect_tx(bars + buf, L::STX);
 #pragma unroll 1
-      for (int w = 0; w < L::NS; ++w)
+      for (int w = 0; w < L::NS; ++w) {
+        tma_mbar_expect_tx(full + buf * NWB + w, L::STX / L::NS);
         tma_load_2d(smc + buf * L::BUF + w * L::SBLK, &tms, (int)(j0 - 4 + 128 * w), (int)(i0 - R - a.row0),
-                    bars + buf);
+                    full + buf * NWB + w);
+      }
       return;
     }
-    tma_mbar_expect_tx(bars + buf, WR * WCP * 4);
+    uint64_t *bar0 = full + buf * NWB;
+    tma_mbar_expect_tx(bar0, WR * WCP * 4);
     // window rows [i0-R, i0+BM+R) x cols [j0-4, j0+BN+4) of the local buffer
     if constexpr (!L::WIDE) {
-      tma_load_2d(smc + buf * L::BUF, &tmw, (int)(j0 - 4), (int)(i0 - R - a.row0), bars + buf);
+      tma_load_2d(smc + buf * L::BUF, &tmw, (int)(j0 - 4), (int)(i0 - R - a.row0), bar0);
     } else {
 #pragma unroll
       for (int q = 0; q < L::NB; ++q)
         tma_load_2d(smc + buf * L::BUF + q * (WR * 256 * 4), &tmw, (int)(j0 - 4 + 256 * q), (int)(i0 - R - a.row0),
-                    bars + buf);
+                    bar0);
       tma_load_2d(smc + buf * L::BUF + L::NB * (WR * 256 * 4), &tmw8, (int)(j0 - 4 + 256 * L::NB),
-                  (int)(i0 - R - a.row0), bars + buf);
+                  (int)(i0 - R - a.row0), bar0);
     }
   };
   if (threadIdx.x == ptid) {
@@ -138,10 +145,11 @@ __global__ void __launch_bounds__(MAXT + (PW ? 32 : 0)) stencil_kernel(const __g
     if (strip) tma_prefetch_desc(&tms);
 #pragma unroll
     for (int b = 0; b < NST; ++b) {
-      tma_mbar_init(bars + b, 1);
+#pragma unroll
+      for (int w = 0; w < NWB; ++w) tma_mbar_init(full + b * NWB + w, 1);
       // every thread of the unit warps releases the slot: the whole (rounded-up)
       // unit warps with a producer warp, all blockDim.x threads without one
-      tma_mbar_init(bars + NST + b, PW ? cw * 32 : blockDim.x);
+      tma_mbar_init(empty + b, PW ? cw * 32 : blockDim.x);
     }
     tma_fence_init();
   }
@@ -155,8 +163,8 @@ __global__ void __launch_bounds__(MAXT + (PW ? 32 : 0)) stencil_kernel(const __g
   auto produce = [&](int slot, bool wait_empty, unsigned parity) {
     const int64_t nx = next_tile();
     if (wait_empty) {
-      if (PW) tma_mbar_wait_backoff(bars + NST + slot, parity);
-      else tma_mbar_wait(bars + NST + slot, parity);
+      if (PW) tma_mbar_wait_backoff(empty + slot, parity);
+      else tma_mbar_wait(empty + slot, parity);
     }
     tile_s[3 * slot] = nx;
     if (nx >= 0) {
@@ -166,7 +174,8 @@ __global__ void __launch_bounds__(MAXT + (PW ? 32 : 0)) stencil_kernel(const __g
       tile_s[3 * slot + 2] = j0;
       issue(i0, j0, slot);
     } else {
-      tma_mbar_arrive(bars + slot);
+#pragma unroll
+      for (int w = 0; w < NWB; ++w) tma_mbar_arrive(full + slot * NWB + w);
     }
     prod = nx;
   };
@@ -188,7 +197,7 @@ __global__ void __launch_bounds__(MAXT + (PW ? 32 : 0)) stencil_kernel(const __g
       const int slot = (iter + NST - 1) % NST;
       produce(slot, iter >= 1, (unsigned)(((iter - 1) / NST) & 1));
     }
-    tma_mbar_wait(bars + buf, (unsigned)((iter / NST) & 1));
+    tma_mbar_wait(full + buf * NWB + (strip ? (u >> 5) % NWB : 0), (unsigned)((iter / NST) & 1));
     const int64_t tile = tile_s[3 * buf];
     if (tile < 0) break;
     const float *win = reinterpret_cast<const float *>(smc + buf * L::BUF);
@@ -333,7 +342,7 @@ __global__ void __launch_bounds__(MAXT + (PW ? 32 : 0)) stencil_kernel(const __g
         }
       }
     }
-    tma_mbar_arrive(bars + NST + buf);   // this thread is done with `buf` (per-thread release)
+    tma_mbar_arrive(empty + buf);   // this thread is done with `buf` (per-thread release)
   }
   }   // unit warps
   if (a.sched == SK_DYNAMIC) {

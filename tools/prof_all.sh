@@ -12,8 +12,9 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 prof() {   # name kernel-regex one_kernel-mode [env...]
   local name=$1 re=$2 mode=$3; shift 3
   env "$@" timeout 900 ncu --set full --clock-control none --import-source on -k regex:"$re" -s 1 -c 1 \
-    -o gpurun_out/prof_$name -f python tools/one_kernel.py $mode > gpurun_out/prof_$name.log 2>&1
+    -o /tmp/ncu/prof_$name -f python tools/one_kernel.py $mode > gpurun_out/prof_$name.log 2>&1
 }
+mkdir -p /tmp/ncu
 prof reduce_i64 stream_loop reduce_i64
 prof reduce_f32 stream_loop reduce_f32
 prof axpy stream_loop axpy_static
@@ -25,5 +26,10 @@ prof matmul_pair matmul_pair_kernel matmul_pair
 prof matmul_pair_f32 matmul_pair_f32 matmul_f32_pair
 prof matvec matvec matvec
 prof stencil7 stencil_kernel stencil7
-UPIR_PROFILES_OUT=gpurun_out/profiles python tools/ncu_summary.py $TAG gpurun_out/prof_*.ncu-rep
+# reports stay on the box (gpurun copies back <= 64 MiB): summaries only
+UPIR_PROFILES_OUT=gpurun_out/profiles python tools/ncu_summary.py $TAG /tmp/ncu/prof_*.ncu-rep
+for r in /tmp/ncu/prof_*.ncu-rep; do
+  n=$(basename $r .ncu-rep)
+  ncu -i $r --page details --csv > gpurun_out/profiles/${TAG}_${n#prof_}_details.csv 2>/dev/null
+done
 ls -la gpurun_out gpurun_out/profiles
