@@ -13,4 +13,9 @@ J="ring_depths and 9-128 or ragged_team_sizes or interior_fast_path or strip_til
 timeout 900 $CS --tool racecheck --racecheck-report all --error-exitcode 9 python -m pytest tests/test_gpu_jacobi.py tests/test_gpu_stencil.py -q -x -k "$J" > gpurun_out/san_race_ring.log 2>&1; echo racecheck ring rc=$?
 timeout 900 $CS --tool synccheck --error-exitcode 9 python -m pytest tests/test_gpu_jacobi.py tests/test_gpu_stencil.py -q -x -k "$J" > gpurun_out/san_sync_ring.log 2>&1; echo synccheck ring rc=$?
 timeout 900 $CS --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_jacobi.py tests/test_gpu_stencil.py -q -x -k "$J" > gpurun_out/san_mem_ring.log 2>&1; echo memcheck ring rc=$?
+# round 2: address-aligned vector paths (misaligned adopted views), the 256-thread AXPY kernel with
+# one team per SM, the chunk-pipelined map and the graph-captured async halo
+timeout 1500 $CS --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_stream.py -q -x -k "misaligned and direct or axpy_misaligned or axpy_parity and 148-256 and direct" > gpurun_out/san_mem_align.log 2>&1; echo memcheck align rc=$?
+timeout 900 $CS --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_data.py -q -x -k "pipelined or graph_capture or async_halo" > gpurun_out/san_mem_data.log 2>&1; echo memcheck data rc=$?
+timeout 900 $CS --tool racecheck --racecheck-report all --error-exitcode 9 python -m pytest tests/test_gpu_stencil.py -q -x -k "strip_tiles" > gpurun_out/san_race_stencil.log 2>&1; echo racecheck stencil rc=$?
 for f in gpurun_out/san_*.log; do echo "== $f"; grep -E "ERROR SUMMARY|passed|failed" $f | tail -3; done

@@ -52,13 +52,12 @@ def main():
     for key, fn in (("jacobi", bench.bench_jacobi), ("c5b", bench.line_c5b)):
         if key not in what:
             continue
-        cfgs = [("static", sk, c) for sk in ("0", "3", "4", "5", "8", "12") for c in (1, 2)] + \
-               [("dynamic", None, c) for c in (1, 2)]
+        cfgs = [("static", None, c) for c in (1, 8, 16, 32, 37, 64)] + [("dynamic", None, c) for c in (1,)]
         for pol, skew, chunk in cfgs:
             order = "row"
             for teams in (444,):
                 setenv(UPIR_JACOBI_ORDER=order, UPIR_JACOBI_CHUNK=chunk, UPIR_JACOBI_TEAMS=teams,
-                       UPIR_JACOBI_POLICY=pol, UPIR_JACOBI_SKEW=skew)
+                       UPIR_JACOBI_POLICY=pol)
                 try:
                     r = fn(E)
                     summ = r.get("summary") or {k: v for k, v in r["paths"].items()}
@@ -67,8 +66,7 @@ def main():
                 out.append({key: {"policy": pol, "skew": skew, "chunk": chunk, "teams": teams, **summ}})
                 print(json.dumps(out[-1]), flush=True)
                 E.free()
-        setenv(UPIR_JACOBI_ORDER=None, UPIR_JACOBI_CHUNK=None, UPIR_JACOBI_TEAMS=None, UPIR_JACOBI_POLICY=None,
-               UPIR_JACOBI_SKEW=None)
+        setenv(UPIR_JACOBI_ORDER=None, UPIR_JACOBI_CHUNK=None, UPIR_JACOBI_TEAMS=None, UPIR_JACOBI_POLICY=None)
     E.U.upir_finalize(E.ctx)
 
 
