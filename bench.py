@@ -199,6 +199,7 @@ def run_reference(args):
     rank, world, _ = dist_env()
     if rank != 0:
         return
+    world = max(world, args.gpus)
     import oracle
     import synth
     lg = int(os.environ.get("UPIR_REF_LOG2", 28))
@@ -1094,14 +1095,16 @@ def bench_matmul(E, n=8192):
 
 def main():
     args = parse()
+    if args.impl == "reference":
+        # the oracle runs on rank 0's host cores only: no GPU and no extra
+        # ranks needed (under torchrun the other ranks exit without work)
+        run_reference(args)
+        return
     maybe_self_launch(args)
     rank, world, _ = dist_env()
     if world != args.gpus:
         sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
         sys.exit(2)
-    if args.impl == "reference":
-        run_reference(args)
-        return
     run_upir(args)
 
 
