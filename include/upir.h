@@ -270,7 +270,9 @@ typedef enum { UPIR_DIST_TEAMS = 1, UPIR_DIST_UNITS = 2, UPIR_DIST_TEAMS_UNITS =
 #define UPIR_WORLD_REDUCE 2u
 /* UPIR_WORLD_VIA_COMM: with UPIR_WORLD_REDUCE, combine over ranks through the
  * communicator (NCCL all-gather) even when the peer windows are imported
- * (measurement of the NCCL path next to the fused one). */
+ * (measurement of the NCCL path next to the fused one).  At nranks == 1 the
+ * same partial / gather / combine sequence runs with a device copy as the
+ * gather (the result equals the plain loop's). */
 #define UPIR_WORLD_VIA_COMM 8u
 
 typedef struct {

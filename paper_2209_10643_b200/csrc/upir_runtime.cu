@@ -1135,12 +1135,15 @@ static upir_status exec_stream(upir_spmd s, const upir_loop_desc *l, const upir_
   // else the loop with the original value applied on rank 0 only, followed
   // by upir_reduce(WORLD) (NCCL) on each result -- the same combination
   bool world_after = false;
-  if ((l->flags & UPIR_WORLD_REDUCE) && c->nranks > 1 && n_reds > 0) {
-    if (world_ready(c) && !((l->flags & UPIR_WORLD_VIA_COMM) && c->comm)) {
+  // (nranks == 1 with UPIR_WORLD_VIA_COMM: the same partial / combine path
+  // with a device copy for the gather -- its arithmetic is testable on one GPU)
+  const bool via_comm = (l->flags & UPIR_WORLD_VIA_COMM) != 0;
+  if ((l->flags & UPIR_WORLD_REDUCE) && n_reds > 0 && (c->nranks > 1 || via_comm)) {
+    if (c->nranks > 1 && world_ready(c) && !(via_comm && c->comm)) {
       a.wwin = c->win;
       a.wrank = c->rank;
       a.wranks = c->nranks;
-    } else if (c->comm) {
+    } else if (c->comm || c->nranks == 1) {
       // each rank's int64 / fp64 partials are all-gathered and combined with
       // init in ascending rank order, rounded once -- the same arithmetic as
       // the fused peer path
@@ -1247,7 +1250,8 @@ static upir_status exec_stream(upir_spmd s, const upir_loop_desc *l, const upir_
   if (e != cudaSuccess) return fail(UPIR_E_CUDA, "loop kernel launch failed: %s", cudaGetErrorString(e));
   c->launches++;
   if (world_after) {
-    NCCL_TRY(ncclAllGather(a.wpart, c->scratch, 2, ncclUint64, c->comm, c->compute));
+    if (c->nranks > 1) NCCL_TRY(ncclAllGather(a.wpart, c->scratch, 2, ncclUint64, c->comm, c->compute));
+    else CUDA_TRY(cudaMemcpyAsync(c->scratch, a.wpart, 16, cudaMemcpyDeviceToDevice, c->compute));
     e = launch_world_combine(reinterpret_cast<const unsigned long long *>(c->scratch), c->nranks, n_reds, a.red,
                              c->compute);
     if (e != cudaSuccess) return fail(UPIR_E_CUDA, "world combine launch failed: %s", cudaGetErrorString(e));

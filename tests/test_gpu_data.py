@@ -321,3 +321,33 @@ def test_async_halo_join_graph_capture(ctx):
         res.append(a if S % 2 == 0 else b)
     assert (res[0] == res[1]).all()
     assert np.abs(res[0] - oracle.jacobi5(g, S)).max() <= 1e-5
+
+
+@pytest.mark.parametrize("dt", ["i64", "f32"])
+def test_world_combine_path_world1_matches_plain(ctx, dt):
+    """The communicator world-reduction path (last team writes the int64 /
+    fp64 partial, gather, one combine kernel applies init and rounds once) run
+    at world size 1 via UPIR_WORLD_VIA_COMM: bit-identical to the plain loop
+    for sum / max / min with an original value (reading c9, c10)."""
+    n = 300_007
+    if dt == "i64":
+        x, dtype, tdt, inits = synth.i64_sym(6, 0, n), U.I64, torch.int64, [np.array([7], np.int64)] * 2
+    else:
+        x, dtype, tdt, inits = synth.f32_unit(7, 0, n), U.F32, torch.float32, [np.array([0.5], np.float32)] * 2
+    m = U.upir_data_map(ctx, x, U.MAP_TO)
+    outs = {}
+    for flags in (0, U.WORLD_REDUCE | U.WORLD_VIA_COMM):
+        for ops in ((U.OP_SUM, U.OP_MAX), (U.OP_MIN, U.OP_SUM)):
+            r = torch.zeros(2, dtype=tdt, device="cuda")
+            torch.cuda.synchronize()
+            s = U.upir_spmd_launch(ctx, U.spmd_desc(37, 128))
+            U.upir_loop_exec(s, U.loop_desc(0, n, chunk=4, flags=flags), U.body(U.BODY_REDUCE, dtype, in0=m),
+                             [U.reduction(ops[0], dtype, r.data_ptr(), init=inits[0]),
+                              U.reduction(ops[1], dtype, r.data_ptr() + r.element_size(), init=inits[1])])
+            U.upir_spmd_end(s)
+            U.upir_sync(ctx)
+            outs[(flags, ops)] = r.cpu().numpy().tobytes()
+    for ops in ((U.OP_SUM, U.OP_MAX), (U.OP_MIN, U.OP_SUM)):
+        assert outs[(0, ops)] == outs[(U.WORLD_REDUCE | U.WORLD_VIA_COMM, ops)]
+    U.upir_data_unmap(ctx, m)
+    U.upir_sync(ctx)
