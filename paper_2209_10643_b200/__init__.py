@@ -71,6 +71,8 @@ def reduction(op, dtype, dev_result, init=None):
     r.op, r.dtype = op, dtype
     r.dev_result = dev_ptr(dev_result).value
     if init is not None:
+        if hasattr(init, "item"):   # numpy scalar / one-element array
+            init = init.item() if getattr(init, "size", 1) == 1 else init
         buf = (ctypes.c_int64(int(init)) if dtype == _abi.I64 else ctypes.c_float(float(init)))
         r._init_buf = buf
         r.init = ctypes.cast(ctypes.pointer(buf), ctypes.c_void_p)

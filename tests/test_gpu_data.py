@@ -331,9 +331,9 @@ def test_world_combine_path_world1_matches_plain(ctx, dt):
     for sum / max / min with an original value (reading c9, c10)."""
     n = 300_007
     if dt == "i64":
-        x, dtype, tdt, inits = synth.i64_sym(6, 0, n), U.I64, torch.int64, [np.array([7], np.int64)] * 2
+        x, dtype, tdt, inits = synth.i64_sym(6, 0, n), U.I64, torch.int64, [7, -3]
     else:
-        x, dtype, tdt, inits = synth.f32_unit(7, 0, n), U.F32, torch.float32, [np.array([0.5], np.float32)] * 2
+        x, dtype, tdt, inits = synth.f32_unit(7, 0, n), U.F32, torch.float32, [0.5, 0.25]
     m = U.upir_data_map(ctx, x, U.MAP_TO)
     outs = {}
     for flags in (0, U.WORLD_REDUCE | U.WORLD_VIA_COMM):
