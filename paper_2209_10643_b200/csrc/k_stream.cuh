@@ -9,16 +9,22 @@
 // combines the slots in a fixed order and applies init (readings c9, c10).
 //
 // Two memory paths:
-//  DIRECT : every unit loads its own elements.  Used when a unit's chunk is
-//           at most one 16-B vector: adjacent units own adjacent chunks, so a
-//           warp's loads are coalesced (chunked static / dynamic, small c).
-//  STAGED : chunks longer than a vector (static block, large c): adjacent
-//           units are far apart, so per-unit vector loads would touch 32
-//           lines per warp instruction.  Instead every unit moves its own
-//           next 64-256 B segment into a private shared-memory row with one
-//           TMA bulk copy (NST stages deep, mbarrier-tracked) and executes
-//           the body on ITS OWN iterations from that row.  AXPY results go
-//           back by bulk store, element-exact at unit boundaries.
+//  DIRECT (default): every unit loads its own elements.  One-vector chunks
+//           (chunked static / dynamic with c = one 16-B vector): adjacent
+//           units own adjacent vectors, so a warp's loads are coalesced (the
+//           x / y of 4 chunks in flight).  Long chunks (static block, large
+//           c): each unit streams its own range with 256-bit loads
+//           (ld.global.cs.L2::256B), several in flight; vectors are aligned by
+//           ADDRESS (esh), so adopted views with a storage offset and BLOCK
+//           slices that start mid-line stay legal.  AXPY teams of <= 256
+//           units run the 256-thread compile (no register spills), long
+//           chunks with one resident team per SM.
+//  STAGED (UPIR_PATH=staged): every unit moves its own next 64-256 B segment
+//           into a private shared-memory row with one TMA bulk copy (NST
+//           stages deep, mbarrier-tracked) and executes the body on ITS OWN
+//           iterations from that row.  AXPY results go back by bulk store,
+//           element-exact at unit boundaries.  Kept as the coalesced
+//           alternative; measured slower than DIRECT on B200.
 #pragma once
 #include <cuda_runtime.h>
 #include <math_constants.h>

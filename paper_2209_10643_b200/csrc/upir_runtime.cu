@@ -1132,8 +1132,9 @@ static upir_status exec_stream(upir_spmd s, const upir_loop_desc *l, const upir_
     }
   }
   // UPIR_WORLD_REDUCE: upir.sync allreduce fused into the loop (peer windows),
-  // else the loop with the original value applied on rank 0 only, followed
-  // by upir_reduce(WORLD) (NCCL) on each result -- the same combination
+  // or through the communicator: the last team writes the rank's partials,
+  // NCCL all-gathers them and one kernel combines init (+) P_0 (+) ... -- the
+  // same arithmetic as the fused path
   bool world_after = false;
   // (nranks == 1 with UPIR_WORLD_VIA_COMM: the same partial / combine path
   // with a device copy for the gather -- its arithmetic is testable on one GPU)
@@ -1161,9 +1162,10 @@ static upir_status exec_stream(upir_spmd s, const upir_loop_desc *l, const upir_
     }
   }
   a.trace = trace ? (int32_t *)trace->dev : nullptr;
-  // long per-unit chunks: 256-bit loads, 4 in flight; AXPY aligns each unit's
-  // main loop to whole 128-B lines so its stores complete lines (measured best
-  // in tools/sweep_axpy.sh: partial-line write-backs cost DRAM re-reads)
+  // long per-unit chunks: 256-bit loads, 4 in flight (dvar 1); for AXPY teams
+  // of > 256 units the main loop is aligned to whole 128-B lines (dvar 8) --
+  // teams of <= 256 units take the axpy_long setting below (round-1 / round-2
+  // sweeps, tools/sweep_r2.py)
   a.dvar = body == SB_AXPY ? 8 : 1;
   if (const char *dv = getenv("UPIR_DVAR")) a.dvar = atoi(dv);
   // dynamic tickets: m chunks per unit so a ticket covers >= ~256 KiB
