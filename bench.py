@@ -584,7 +584,7 @@ def bench_c2(E):
         U.upir_data_unmap(ctx, m1)
         U.upir_sync(ctx)
 
-    e2e_ms = pipe_ms = float("nan")
+    e2e_ms = pipe_ms = h2d_gbs = float("nan")
     e2e_res = pipe_res = None
     if args.e2e_steps > 0:
         e2e_step()   # warm-up (pins nothing: the host buffers are pinned by torch)
@@ -604,6 +604,17 @@ def bench_c2(E):
             E.barrier()
             pipe_ms = (time.perf_counter() - te0) * 1e3 / args.e2e_steps
             pipe_res = hres[:4].copy()
+        # the link's own rate: torch's pinned H2D copy of the same 12 GiB
+        dx_i = torch.empty_like(hx_i, device="cuda")
+        dx_f = torch.empty_like(hx_f, device="cuda")
+        torch.cuda.synchronize()
+        tl0 = time.perf_counter()
+        dx_i.copy_(hx_i, non_blocking=True)
+        dx_f.copy_(hx_f, non_blocking=True)
+        torch.cuda.synchronize()
+        h2d_gbs = (hx_i.numel() * 8 + hx_f.numel() * 4) / (time.perf_counter() - tl0) / 1e9
+        del dx_i, dx_f
+        E.free()
     # the e2e paths are timed by the host clock around synchronous steps (each
     # step ends in upir_sync), max over ranks
     ms, e2e_ms, pipe_ms = E.ranks_max([ms_local, e2e_ms, pipe_ms])
@@ -645,7 +656,8 @@ def bench_c2(E):
         "clocks": clocks,
         "e2e": {"value": bytes_rank * world / (e2e_ms / 1e3) / 1e9, "unit": "GB/s",
                 "h2d_bytes_per_step": bytes_rank, "d2h_bytes_per_step": 32, "ms": e2e_ms,
-                "host_affinity_cpus": E.numa_cpus},
+                "host_affinity_cpus": E.numa_cpus,
+                "h2d_link_GBps_torch_copy": h2d_gbs},
         "e2e_pipelined": pipe,
     }
 
