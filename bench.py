@@ -58,8 +58,9 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="upir", choices=["upir", "reference"])
-    ap.add_argument("--sched", default="static", choices=["static", "static1", "dynamic"],
-                    help="schedule of the C2 headline loops")
+    ap.add_argument("--sched", default="static1", choices=["static", "static1", "dynamic"],
+                    help="schedule of the C2 headline loops: static1 = chunked static with one 16-B vector per "
+                         "chunk (SURVEY 8(d) C2's throughput schedule); static = block; dynamic = one vector")
     ap.add_argument("--n-log2", type=int, default=30)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -182,47 +183,67 @@ def fracs(gbs, peak):
 
 def c2_config(sched, world):
     return {"workload": "C2: int64 and fp32 sum/max reduction, n=2^30 per GPU, teams x units 592x256, "
-                        f"schedule {sched}, map to/from",
+                        f"schedule {c2_sched_label(sched)}, map to/from",
             "teams": 592, "units": 256, "schedule": sched,
             "l2": "inputs 12 GiB per GPU >> 126 MB L2 (no flush needed)", "parallelism": f"dp{world}"}
 
 
 # --------------------------------------------------------------------------- reference arm
+SCHED_CHUNKS = {"static": (0, 0), "static1": (2, 4), "dynamic": (2, 4)}
+
+
+def c2_sched_label(sched):
+    return {"static": "static (block)", "static1": "static,2 int64 / static,4 fp32 (one 16-B vector per chunk)",
+            "dynamic": "dynamic,2 int64 / dynamic,4 fp32"}[sched]
+
+
 def run_reference(args):
     """The oracle (plain sequential CPU interpreter, as it stands) as the
     reference arm: each step interprets the C2 loops -- int64 sum and max,
-    fp32 sum and max under schedule(static) over p = 592 x 256 units -- on a
-    bounded sample of the C2 input stream (2^28 elements per array by
-    default, sized so that the driver's 20 + 5 steps end within ~2 minutes),
-    timed with the host clock on this host's cores.  ms_per_step is the
-    measured time of one such step (no extrapolation)."""
+    fp32 sum and max under the GPU arm's schedule over p = 592 x 256 units --
+    on a bounded sample of the C2 input stream, timed with the host clock on
+    this host's cores.  The sample is the largest power of two (<= 2^28
+    elements per array) whose warm-up + timed steps fit ~2 minutes, from a
+    calibration step at 2^20; ms_per_step is the measured time of one such
+    step (no extrapolation)."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
     world = max(world, args.gpus)
     import oracle
     import synth
-    lg = int(os.environ.get("UPIR_REF_LOG2", 28))
+    p = 148 * 4 * 256
+    ci, cf = SCHED_CHUNKS[args.sched]
+    pol = oracle.DYNAMIC if args.sched == "dynamic" else oracle.STATIC
+
+    def step(xi, xf):
+        oracle.reduce_i64(oracle.SUM, xi, p=p, policy=pol, chunk=ci)
+        oracle.reduce_i64(oracle.MAX, xi, p=p, policy=pol, chunk=ci)
+        oracle.reduce_f32(oracle.SUM, xf, p=p, policy=pol, chunk=cf)
+        oracle.reduce_f32(oracle.MAX, xf, p=p, policy=pol, chunk=cf)
+
+    lg = os.environ.get("UPIR_REF_LOG2")
+    if lg is None:
+        c = 1 << 20
+        t0 = time.perf_counter()
+        step(synth.c_i64_sym(6, 0, c), synth.c_f32_unit(7, 0, c))
+        per_elem = (time.perf_counter() - t0) / c
+        budget = 120.0 / max(1, args.steps + args.warmup)
+        lg = max(20, min(28, int(math.floor(math.log2(max(budget / per_elem, 1.0))))))
+    lg = int(lg)
     n = 1 << lg
     xi = synth.c_i64_sym(6, 0, n)
     xf = synth.c_f32_unit(7, 0, n)
-    p = 148 * 4 * 256
-
-    def step():
-        oracle.reduce_i64(oracle.SUM, xi, p=p)
-        oracle.reduce_i64(oracle.MAX, xi, p=p)
-        oracle.reduce_f32(oracle.SUM, xf, p=p)
-        oracle.reduce_f32(oracle.MAX, xf, p=p)
-
     for _ in range(args.warmup):
-        step()
+        step(xi, xf)
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        step()
+        step(xi, xf)
     dt = (time.perf_counter() - t0) / args.steps
     gbs = n * 12 / dt / 1e9
     sample = (f"n=2^{lg} int64 + 2^{lg} fp32 elements of the C2 streams per step (sum and max of each, "
-              f"schedule(static) over 592x256 units), of the 2^30 the GPU arm reduces; GB/s = 12 B x n / t")
+              f"{c2_sched_label(args.sched)} over 592x256 units), of the 2^30 the GPU arm reduces; "
+              f"GB/s = 12 B x n / t")
     print(json.dumps({
         "impl": "reference", "metric": C2_METRIC,
         "value": gbs, "unit": "GB/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
@@ -234,21 +255,23 @@ def run_reference(args):
     }), flush=True)
 
 
-def cpu_baseline_reduce():
+def cpu_baseline_reduce(sched):
     import oracle
     import synth
-    n = 1 << 26
+    n = 1 << 25
     xi = synth.c_i64_sym(6, 0, n)
     xf = synth.c_f32_unit(7, 0, n)
     p = 148 * 4 * 256
+    ci, cf = SCHED_CHUNKS[sched]
+    pol = oracle.DYNAMIC if sched == "dynamic" else oracle.STATIC
     t0 = time.perf_counter()
-    oracle.reduce_i64(oracle.SUM, xi, p=p)
-    oracle.reduce_i64(oracle.MAX, xi, p=p)
-    oracle.reduce_f32(oracle.SUM, xf, p=p)
-    oracle.reduce_f32(oracle.MAX, xf, p=p)
+    oracle.reduce_i64(oracle.SUM, xi, p=p, policy=pol, chunk=ci)
+    oracle.reduce_i64(oracle.MAX, xi, p=p, policy=pol, chunk=ci)
+    oracle.reduce_f32(oracle.SUM, xf, p=p, policy=pol, chunk=cf)
+    oracle.reduce_f32(oracle.MAX, xf, p=p, policy=pol, chunk=cf)
     dt = time.perf_counter() - t0
     return {"value": n * 12 / dt / 1e9, "unit": "GB/s", "cores": 1, "kind": "oracle",
-            "sample": "2^26 int64 + 2^26 fp32 elements, sum and max each (one pass per op), "
+            "sample": f"2^25 int64 + 2^25 fp32 elements, sum and max each (one pass per op), {c2_sched_label(sched)}, "
                       "GB/s counted as 12 B per element pair like the GPU metric"}
 
 
@@ -395,7 +418,7 @@ def run_upir(args):
     if E.rank == 0:
         out["summary"].update(summarize(lines, kernels))
         if E.world == 1 and not args.no_cpu_baseline:
-            out["cpu_baseline"] = cpu_baseline_reduce()
+            out["cpu_baseline"] = cpu_baseline_reduce(args.sched)
         out["scaling_lines"] = lines
         out["kernels"] = kernels
         print(json.dumps(clean(out)), flush=True)
@@ -450,7 +473,7 @@ def bench_c2(E):
     teams, units = 148 * 4, 256
     # static1 / dynamic: chunk = one 16-B vector per unit (2 int64 / 4 fp32)
     pol = {"static": U.SCHED_STATIC, "static1": U.SCHED_STATIC, "dynamic": U.SCHED_DYNAMIC}[args.sched]
-    ci, cf = (0, 0) if args.sched == "static" else (2, 4)
+    ci, cf = SCHED_CHUNKS[args.sched]
     # device-resident inputs: adopted buffers + on-device synthetic fill (rank
     # r holds global elements [r*n, (r+1)*n) of each stream)
     xi_t = torch.empty(n, dtype=torch.int64, device="cuda")
@@ -506,6 +529,23 @@ def bench_c2(E):
     # correctness guard on the last step (cheap properties)
     r = res_t.cpu()
     assert -(1 << 28) <= r[1:2].view(torch.int64).item() < (1 << 28)
+    # the other two C2 schedules of SURVEY 8(d), kernel time only (same arrays)
+    other = {}
+    for name, (opol, oci, ocf) in (("static", (U.SCHED_STATIC, 0, 0)), ("static1", (U.SCHED_STATIC, 2, 4)),
+                                   ("dynamic", (U.SCHED_DYNAMIC, 2, 4))):
+        if name == args.sched:
+            continue
+        li = U.loop_desc(0, n, policy=opol, chunk=oci, flags=wflag)
+        lf = U.loop_desc(0, n, policy=opol, chunk=ocf, flags=wflag)
+
+        def ostep():
+            U.upir_loop_exec(spmd, li, U.body(U.BODY_REDUCE, U.I64, in0=mi), reds_i)
+            U.upir_loop_exec(spmd, lf, U.body(U.BODY_REDUCE, U.F32, in0=mf), reds_f)
+
+        ostep()
+        E.barrier()
+        (oms,) = E.ranks_max([E.time_stream(ostep, max(3, args.steps // 2))])
+        other[name] = {"value": n * 12 * world / (oms / 1e3) / 1e9, "unit": "GB/s", "ms_per_step": oms}
     U.upir_spmd_end(spmd)
 
     # ---- e2e: host buffers through the C-ABI ------------------------------------
@@ -644,7 +684,8 @@ def bench_c2(E):
                        world_reduce=("none" if world == 1 else
                                      "fused in-kernel (NVLink peer windows)" if peer else "NCCL all-gather")),
         "gpu_launches": launches,
-        "summary": {"C2:reduce_i64": fracs(ach_i, E.peak), "C2:reduce_f32": fracs(ach_f, E.peak)},
+        "summary": dict({"C2:reduce_i64": fracs(ach_i, E.peak), "C2:reduce_f32": fracs(ach_f, E.peak)},
+                        **{f"C2:{k}": {"GB/s": round(v["value"], 1)} for k, v in other.items()}),
         "roofline": {"bound": "hbm", "achieved": ach_i, "peak": E.peak, "unit": "GB/s",
                      "frac": ach_i / E.peak, "frac_8TB": ach_i / NOMINAL_HBM_GBS,
                      "traffic": ncu_traffic("reduce_i64"),
@@ -653,6 +694,7 @@ def bench_c2(E):
                      "other_kernels": {"reduce_f32": {"achieved": ach_f, "frac": ach_f / E.peak,
                                                       "traffic": ncu_traffic("reduce_f32")}}},
         "kernel_ms": {"reduce_i64": ki, "reduce_f32": kf},
+        "other_schedules": other,
         "clocks": clocks,
         "e2e": {"value": bytes_rank * world / (e2e_ms / 1e3) / 1e9, "unit": "GB/s",
                 "h2d_bytes_per_step": bytes_rank, "d2h_bytes_per_step": 32, "ms": e2e_ms,
