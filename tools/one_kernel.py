@@ -42,7 +42,8 @@ def main():
         dt, code, st = (U.I64, 2, 6) if what == "reduce_i64" else (U.F32, 0, 7)
         m = adopt(n, torch.int64 if dt == U.I64 else torch.float32, code, st)
         s = U.upir_spmd_launch(ctx, U.spmd_desc(592, 256))
-        run = lambda: U.upir_loop_exec(s, U.loop_desc(0, n), U.body(U.BODY_REDUCE, dt, in0=m),  # noqa: E731
+        ch = int(os.environ.get("UPIR_C2_CHUNK", 2 if dt == U.I64 else 4))   # bench's C2 schedule: one 16-B vector
+        run = lambda: U.upir_loop_exec(s, U.loop_desc(0, n, chunk=ch), U.body(U.BODY_REDUCE, dt, in0=m),  # noqa: E731
                                        [U.reduction(U.OP_SUM, dt, b), U.reduction(U.OP_MAX, dt, b + 8)])
     elif what.startswith("jacobi"):
         n = 8192 if what == "jacobi_c3" else 32768
