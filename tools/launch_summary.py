@@ -1,7 +1,7 @@
 """Summarise an ncu launch list (gpu__time_duration.sum per launch) of
 `bench.py` into profiles/<tag>_launch_summary.txt.
 
-    python tools/launch_summary.py <tag> gpurun_out/launches.csv [bench.log]
+    python tools/launch_summary.py <tag> gpurun_out/launches.csv [bench line of an UNINSTRUMENTED run]
 """
 import csv
 import json
