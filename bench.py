@@ -327,8 +327,19 @@ class Env:
             else:
                 idb = [U.upir_comm_unique_id() if self.rank == 0 else None]
                 dist.broadcast_object_list(idb, src=0)
-                self.ctx = U.upir_init(local, rank=self.rank, nranks=self.world, nccl_id=idb[0])
-                self.has_comm = True
+                try:
+                    self.ctx = U.upir_init(local, rank=self.rank, nranks=self.world, nccl_id=idb[0])
+                    self.has_comm = True
+                except U.UpirError as e:   # report, and keep the peer-window paths measurable
+                    sys.stderr.write(f"bench.py: rank {self.rank}: NCCL communicator init failed ({e}); "
+                                     "running communicator-less (peer windows only)\n")
+                    self.ctx = U.upir_init(local, rank=self.rank, nranks=self.world, nccl_id=None)
+                ok = self.ranks_max([0.0 if self.has_comm else 1.0])[0] == 0.0
+                if not ok and self.has_comm:
+                    # every rank must agree: a world with a communicator on some ranks only would hang
+                    U.upir_finalize(self.ctx)
+                    self.ctx = U.upir_init(local, rank=self.rank, nranks=self.world, nccl_id=None)
+                    self.has_comm = False
         else:
             self.ctx = U.upir_init(local)
         self.stream = torch.cuda.ExternalStream(U.upir_ctx_stream(self.ctx, 0))
