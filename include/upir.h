@@ -395,6 +395,19 @@ upir_status upir_schedule_chunks(int32_t policy, int64_t chunk, int64_t T, int64
 typedef enum { UPIR_SCOPE_DEVICE = 0, UPIR_SCOPE_WORLD = 1 } upir_scope;
 upir_status upir_reduce(upir_ctx ctx, int32_t op, int32_t dtype, const void *dev_in,
                         int64_t count, void *dev_out, int32_t scope);
+/* upir_reduce_async: the WORLD allreduce as the async two-step sync
+ * (PAPER.md:880-882 'arrive-compute' / 'wait-release'; SURVEY 8(f) NEXT #1
+ * 'async allreduce'): the all-gather and the ordered combine are enqueued on
+ * the copy stream after the compute work issued so far (they read dev_in as
+ * that work left it), into a stream-ordered scratch of their own; compute
+ * work issued afterwards does NOT wait for them.  *token (NULL on entry)
+ * receives their completion: upir_sync(JOIN, token) makes later compute work
+ * wait (device-side), upir_sync(WAIT, token) blocks the host.  dev_in must
+ * not be overwritten before the token is released.  nranks == 1: a device
+ * copy replaces the all-gather.  Errors as upir_reduce; a non-empty *token is
+ * UPIR_E_INVALID. */
+upir_status upir_reduce_async(upir_ctx ctx, int32_t op, int32_t dtype, const void *dev_in,
+                              int64_t count, void *dev_out, upir_event *token);
 
 /* upir_sync kinds:
  *   BARRIER       : host waits for all work of this context; reports sticky

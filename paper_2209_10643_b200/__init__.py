@@ -224,6 +224,14 @@ def upir_reduce(ctx, op, dtype, dev_in, count, dev_out, scope=_abi.SCOPE_DEVICE)
     check(lib().upir_reduce(ctx, op, dtype, dev_ptr(dev_in), count, dev_ptr(dev_out), scope))
 
 
+def upir_reduce_async(ctx, op, dtype, dev_in, count, dev_out):
+    """WORLD allreduce as async arrive-compute; returns the token for
+    upir_sync(JOIN / WAIT)."""
+    tok = ctypes.c_void_p()
+    check(lib().upir_reduce_async(ctx, op, dtype, dev_ptr(dev_in), count, dev_ptr(dev_out), ctypes.byref(tok)))
+    return tok
+
+
 def upir_sync(ctx, kind=_abi.SYNC_BARRIER, halo_map=None, token=None, async_=False):
     """Returns the token (ARRIVE, async HALO).  HALO is synchronous unless
     async_=True (then the C call receives a token out-param)."""

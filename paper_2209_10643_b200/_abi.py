@@ -89,6 +89,7 @@ _SIGS = {
     "upir_schedule_chunks": (i32, [i32, i64, i64, i64, i64, ctypes.POINTER(i64), ctypes.POINTER(i64), i64,
                                    ctypes.POINTER(i64)]),
     "upir_reduce": (i32, [vp, i32, i32, vp, i64, vp, i32]),
+    "upir_reduce_async": (i32, [vp, i32, i32, vp, i64, vp, vp]),
     "upir_sync": (i32, [vp, i32, vp, ctypes.POINTER(vp)]),
     "upir_graph_begin": (i32, [vp]),
     "upir_graph_end": (i32, [vp, ctypes.POINTER(vp)]),

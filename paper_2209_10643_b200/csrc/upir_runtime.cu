@@ -1710,6 +1710,57 @@ extern "C" upir_status upir_reduce(upir_ctx c, int32_t op, int32_t dtype, const 
   return UPIR_OK;
 }
 
+extern "C" upir_status upir_reduce_async(upir_ctx c, int32_t op, int32_t dtype, const void *dev_in, int64_t count,
+                                         void *dev_out, upir_event *token) {
+  if (!c || !dev_in || !dev_out || count < 1 || !token) return fail(UPIR_E_INVALID, "bad argument");
+  if (*token) return fail(UPIR_E_INVALID, "token out-param must be NULL on entry");
+  if (op < UPIR_OP_SUM || op > UPIR_OP_MIN) return fail(UPIR_E_INVALID, "bad op");
+  if (dtype != UPIR_I64 && dtype != UPIR_F32) return fail(UPIR_E_INVALID, "dtype must be I64 or F32");
+  if (c->nranks > 1 && !c->comm) return fail(UPIR_E_UNSUPPORTED, "upir_reduce_async needs a communicator");
+  if (c->sticky != cudaSuccess) return sticky_check(c);
+  cudaSetDevice(c->device);
+  const size_t esz = dtype == UPIR_I64 ? 8 : 4;
+  const size_t need = esz * (size_t)count * (size_t)c->nranks;
+  upir_event ev = new upir_event_s();
+  if (cudaEventCreateWithFlags(&ev->ev, cudaEventDisableTiming) != cudaSuccess) {
+    delete ev;
+    return fail(UPIR_E_CUDA, "event create failed");
+  }
+  auto undo = [&](upir_status st) {
+    cudaEventDestroy(ev->ev);
+    delete ev;
+    return st;
+  };
+  // arrive-compute: ordered after the compute work so far, on the copy stream
+  upir_status st = compute_to_copy(c);
+  if (st != UPIR_OK) return undo(st);
+  void *scr = nullptr;
+  cudaError_t e = cudaMallocAsync(&scr, need, c->copy);
+  if (e != cudaSuccess) return undo(fail(UPIR_E_OOM, "async allreduce scratch: %s", cudaGetErrorString(e)));
+  if (c->nranks > 1) {
+    ncclResult_t r = ncclAllGather(dev_in, scr, (size_t)count, dtype == UPIR_I64 ? ncclInt64 : ncclFloat32, c->comm,
+                                   c->copy);
+    if (r != ncclSuccess) {
+      cudaFreeAsync(scr, c->copy);
+      return undo(fail(UPIR_E_NCCL, "ncclAllGather: %s", ncclGetErrorString(r)));
+    }
+  } else {
+    e = cudaMemcpyAsync(scr, dev_in, esz * count, cudaMemcpyDeviceToDevice, c->copy);
+    if (e != cudaSuccess) {
+      cudaFreeAsync(scr, c->copy);
+      return undo(fail(UPIR_E_CUDA, "gather copy: %s", cudaGetErrorString(e)));
+    }
+  }
+  e = launch_rank_combine(op, dtype, scr, count, c->nranks, dev_out, c->copy);
+  cudaFreeAsync(scr, c->copy);
+  if (e != cudaSuccess) return undo(fail(UPIR_E_CUDA, "combine launch failed: %s", cudaGetErrorString(e)));
+  c->launches++;
+  e = cudaEventRecord(ev->ev, c->copy);
+  if (e != cudaSuccess) return undo(fail(UPIR_E_CUDA, "event record: %s", cudaGetErrorString(e)));
+  *token = ev;
+  return UPIR_OK;
+}
+
 static upir_status halo_exchange(upir_ctx c, upir_map m, cudaStream_t strm) {
   if (m->dist.pattern != UPIR_PATTERN_BLOCK || m->dist.halo_rows < 1)
     return fail(UPIR_E_INVALID, "HALO needs a BLOCK-distributed map with halo_rows >= 1");

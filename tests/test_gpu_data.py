@@ -351,3 +351,45 @@ def test_world_combine_path_world1_matches_plain(ctx, dt):
         assert outs[(0, ops)] == outs[(U.WORLD_REDUCE | U.WORLD_VIA_COMM, ops)]
     U.upir_data_unmap(ctx, m)
     U.upir_sync(ctx)
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_async_allreduce_join_and_wait(ctx, graph):
+    """upir_reduce_async (NEXT #1 async allreduce): ordered after the compute
+    work issued before it (it sees the fill), JOIN orders later compute work
+    after it (the device reduction of its result sees it), WAIT releases on the
+    host; world size 1 (the gather is a device copy); eager and captured."""
+    n = 1000
+    x = torch.zeros(n, dtype=torch.int64, device="cuda")
+    out = torch.zeros(n, dtype=torch.int64, device="cuda")
+    tot = torch.zeros(1, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    mx = U.upir_data_adopt(ctx, x)
+
+    def seq():
+        U.upir_synth_fill(ctx, mx, 2, 6)
+        tok = U.upir_reduce_async(ctx, U.OP_SUM, U.I64, x, n, out)
+        U.upir_sync(ctx, U.SYNC_JOIN, token=tok)
+        U.upir_reduce(ctx, U.OP_SUM, U.I64, out, n, tot, U.SCOPE_DEVICE)
+
+    if graph:
+        U.upir_graph_begin(ctx)
+        seq()
+        g = U.upir_graph_end(ctx)
+        U.upir_graph_launch(ctx, g)
+        U.upir_sync(ctx)
+        U.upir_graph_destroy(g)
+    else:
+        seq()
+        U.upir_sync(ctx)
+    ref = synth.i64_sym(6, 0, n)
+    assert (out.cpu().numpy() == ref).all()
+    assert tot.item() == oracle.reduce_i64(oracle.SUM, ref)
+    # host-side release
+    out.zero_()
+    torch.cuda.synchronize()
+    tok = U.upir_reduce_async(ctx, U.OP_MAX, U.I64, x, n, out)
+    U.upir_sync(ctx, U.SYNC_WAIT, token=tok)
+    assert (out.cpu().numpy() == ref).all()
+    U.upir_data_unmap(ctx, mx)
+    U.upir_sync(ctx)
