@@ -819,6 +819,14 @@ def line_c5b(E, S=100):
     r_lo, r_hi = max(lo, 1), min(hi, n - 1)
     inner = U.loop_desc([r_lo + 1, 1], [r_hi - 1, n - 1], tile=[bm, bn], policy=tpol, chunk=tch,
                         distribute=U.DIST_TEAMS, inner_chunk=4, flags=tfl)
+    # every other sweep enumerates the tiles from the last one (UPIR_TILE_REVERSE,
+    # reading c38): it starts on the rows the previous sweep wrote last
+    alt = os.environ.get("UPIR_JACOBI_ALT", "1") != "0"
+    rfl = tfl | (U.TILE_REVERSE if alt else 0)
+    fulls = [full, U.loop_desc([1, 1], [n - 1, n - 1], tile=[bm, bn], policy=tpol, chunk=tch,
+                               distribute=U.DIST_TEAMS, inner_chunk=4, flags=rfl)]
+    inners = [inner, U.loop_desc([r_lo + 1, 1], [r_hi - 1, n - 1], tile=[bm, bn], policy=tpol, chunk=tch,
+                                 distribute=U.DIST_TEAMS, inner_chunk=4, flags=rfl)]
     edges = [U.loop_desc([r, 1], [r + 1, n - 1], tile=[bm, bn], policy=U.SCHED_STATIC, chunk=1,
                          distribute=U.DIST_TEAMS, inner_chunk=4) for r in sorted({r_lo, r_hi - 1})]
 
@@ -826,19 +834,19 @@ def line_c5b(E, S=100):
         for k in range(S):
             src, body = bodies[k % 2]
             U.upir_sync(E.ctx, U.SYNC_HALO, halo_map=src)   # N = 1: no exchange
-            U.upir_loop_exec(s, full, body)
+            U.upir_loop_exec(s, fulls[k % 2], body)
 
     def sweeps_fused():
         # peer mode: each sweep stores its boundary rows into the neighbours'
         # halo rows (the initial halos come with the fill)
         for k in range(S):
-            U.upir_loop_exec(s, full, bodies[k % 2][1])
+            U.upir_loop_exec(s, fulls[k % 2], bodies[k % 2][1])
 
     def sweeps_async():
         for k in range(S):
             src, body = bodies[k % 2]
             tok = U.upir_sync(E.ctx, U.SYNC_HALO, halo_map=src, async_=True)
-            U.upir_loop_exec(s, inner, body)
+            U.upir_loop_exec(s, inners[k % 2], body)
             U.upir_sync(E.ctx, U.SYNC_JOIN, token=tok)
             for e in edges:
                 U.upir_loop_exec(s, e, body)
@@ -885,7 +893,7 @@ def line_c5b(E, S=100):
     vals = list(checks.values())
     return {"workload": f"C5b: Jacobi 5-point {n}x{n} fp32, {S} sweeps as one CUDA graph, BLOCK row slabs over "
                         f"{E.world} GPU(s) with 1-row halos, tiles {bm}x{bn} {tpol_name},{tch}{' column-major' if tfl else ''} "
-                        f"over {teams} teams",
+                        f"over {teams} teams{', tile order alternating per sweep' if alt else ''}",
             "grid_bytes": 4 * n * n,
             "metric": "GLUP/s of the whole job ((n-2)^2 x 100 lattice updates)", "scaling": "strong",
             "n_gpus": E.world, "rows_identical_across_paths": all(v == vals[0] for v in vals),
@@ -1004,9 +1012,14 @@ def bench_jacobi(E, ny=8192, nx=8192, S=100):
     s = U.upir_spmd_launch(E.ctx, U.spmd_desc(teams, 256))
     bodies = [U.body(U.BODY_JACOBI5, U.F32, in0=ma, out=mb, ld=(nx, 0, 0), dims=(ny, 0, 0)),
               U.body(U.BODY_JACOBI5, U.F32, in0=mb, out=ma, ld=(nx, 0, 0), dims=(ny, 0, 0))]
+    # alternate the tile order per sweep (UPIR_TILE_REVERSE): each sweep starts
+    # on the rows the previous one wrote last, still in L2 (hook UPIR_JACOBI_ALT=0)
+    alt = os.environ.get("UPIR_JACOBI_ALT", "1") != "0"
+    loops = [loop, U.loop_desc([1, 1], [ny - 1, nx - 1], tile=[bm, bn], policy=tpol, chunk=tch,
+                               distribute=U.DIST_TEAMS, inner_chunk=4, flags=tfl | U.TILE_REVERSE)]
     U.upir_graph_begin(E.ctx)
     for k in range(S):
-        U.upir_loop_exec(s, loop, bodies[k % 2])
+        U.upir_loop_exec(s, loops[k % 2] if alt else loop, bodies[k % 2])
     g = U.upir_graph_end(E.ctx)
     for _ in range(2):
         U.upir_graph_launch(E.ctx, g)
@@ -1021,7 +1034,8 @@ def bench_jacobi(E, ny=8192, nx=8192, S=100):
     U.upir_data_unmap(E.ctx, mb)
     U.upir_sync(E.ctx)
     return {"workload": f"C3: Jacobi 5-point {ny}x{nx} fp32, {S} sweeps (one CUDA graph), tiles {bm}x{bn} "
-                        f"{tpol_name},{tch}{' column-major' if tfl else ''} over {teams} teams, static,4 over 256 units",
+                        f"{tpol_name},{tch}{' column-major' if tfl else ''} over {teams} teams, static,4 over 256 units"
+                        f"{', tile order alternating per sweep (UPIR_TILE_REVERSE)' if alt else ''}",
             "ms_per_100_sweeps": ms, "GLUP/s": glups, "bound": "hbm",
             "summary": {"C3": dict(value=glups, unit="GLUP/s", **fracs(gbs, E.peak))},
             "roofline": {"achieved": gbs, "peak": E.peak, "unit": "GB/s", "frac": gbs / E.peak,

@@ -254,6 +254,13 @@ typedef enum { UPIR_DIST_TEAMS = 1, UPIR_DIST_UNITS = 2, UPIR_DIST_TEAMS_UNITS =
  * from L2 instead of a row another team fetched.  Trace records index tiles
  * by this id.  Other bodies: UPIR_E_UNSUPPORTED. */
 #define UPIR_TILE_COLMAJOR 4u
+/* UPIR_TILE_REVERSE (tiled JACOBI5 nests; reading c38 of DESIGN.md): tile id
+ * k enumerates the tile grid from its last tile -- id k is the tile the
+ * plain order numbers ntiles - 1 - k (row- or column-major) -- with the
+ * tile-loop schedule and the intra-tile rule unchanged; trace records index
+ * tiles by this id.  Sweeps that alternate it start on the rows the previous
+ * sweep wrote last (still in L2).  Other bodies: UPIR_E_UNSUPPORTED. */
+#define UPIR_TILE_REVERSE 16u
 /* UPIR_WORLD_REDUCE: the loop's reductions are combined over all ranks as part
  * of the loop (Fig. 7 'allreduce' with ranks as units fused into the loop's
  * end barrier): every rank receives

@@ -128,16 +128,17 @@ def tile_owner(R, C, tm, tn, policy, chunk, p):
     return owner[:nt]
 
 
-def tiled_owner(lb0, ub0, lb1, ub1, BM, BN, policy, chunk, p_teams, ic, units, colmajor=False):
+def tiled_owner(lb0, ub0, lb1, ub1, BM, BN, policy, chunk, p_teams, ic, units, colmajor=False, reverse=False):
     """(team, unit) of every box position of a tiled collapse(2) nest (c24);
-    colmajor: tile ids enumerate the tile grid column-major (c35)."""
+    colmajor: tile ids enumerate the tile grid column-major (c35); reverse:
+    id k is the tile the un-reversed order numbers nt - 1 - k (c38)."""
     if ub0 <= lb0 or ub1 <= lb1:
         return np.zeros(0, np.int64), np.zeros(0, np.int64)
     nt = (((ub0 + BM - 1) // BM) - lb0 // BM) * (((ub1 + BN - 1) // BN) - lb1 // BN)
     team = np.zeros(nt * BM * BN, dtype=np.int64)
     unit = np.zeros(nt * BM * BN, dtype=np.int64)
     r = lib().orc_tiled_owner_order(lb0, ub0, lb1, ub1, BM, BN, policy, chunk, p_teams, ic, units,
-                                    1 if colmajor else 0, _p(team), _p(unit))
+                                    (1 if colmajor else 0) | (2 if reverse else 0), _p(team), _p(unit))
     if r != nt:
         raise ValueError("tiled_owner failed")
     return team, unit

@@ -446,7 +446,7 @@ int orc_tile_owner(int64_t R, int64_t Cn, int64_t tm, int64_t tn, int policy,
  * number of tiles, or -1. */
 int64_t orc_tiled_owner_order(int64_t lb0, int64_t ub0, int64_t lb1, int64_t ub1, int64_t BM, int64_t BN,
                               int policy, int64_t chunk, int64_t p_teams, int64_t ic, int64_t units,
-                              int colmajor, int64_t *team, int64_t *unit);
+                              int order, int64_t *team, int64_t *unit);
 
 int64_t orc_tiled_owner(int64_t lb0, int64_t ub0, int64_t lb1, int64_t ub1, int64_t BM, int64_t BN,
                         int policy, int64_t chunk, int64_t p_teams, int64_t ic, int64_t units,
@@ -455,13 +455,16 @@ int64_t orc_tiled_owner(int64_t lb0, int64_t ub0, int64_t lb1, int64_t ub1, int6
     return orc_tiled_owner_order(lb0, ub0, lb1, ub1, BM, BN, policy, chunk, p_teams, ic, units, 0, team, unit);
 }
 
-/* As orc_tiled_owner, with the tile ids enumerated column-major when colmajor
- * != 0 (reading c35: tile id = (tj - tj0) * ntr + (ti - ti0); the paper's
- * tiling, fixes no order).  Arrays are indexed by that id. */
+/* As orc_tiled_owner, with the tile ids enumerated in another order (the
+ * paper's tiling, fixes none).  order bit 0: column-major
+ * (reading c35: tile id = (tj - tj0) * ntr + (ti - ti0)); order bit 1:
+ * reversed (reading c38: id k is the tile the un-reversed order numbers
+ * nt - 1 - k).  Arrays are indexed by that id. */
 int64_t orc_tiled_owner_order(int64_t lb0, int64_t ub0, int64_t lb1, int64_t ub1, int64_t BM, int64_t BN,
                               int policy, int64_t chunk, int64_t p_teams, int64_t ic, int64_t units,
-                              int colmajor, int64_t *team, int64_t *unit)
+                              int order, int64_t *team, int64_t *unit)
 {
+    int colmajor = order & 1;
     if (BM <= 0 || BN <= 0 || ic <= 0 || units <= 0 || p_teams <= 0) return -1;
     if (ub0 <= lb0 || ub1 <= lb1) return 0;
     int64_t ti0 = lb0 / BM, tj0 = lb1 / BN;
@@ -471,8 +474,9 @@ int64_t orc_tiled_owner_order(int64_t lb0, int64_t ub0, int64_t lb1, int64_t ub1
     if (!towner) return -1;
     if (orc_owner_map(policy, chunk, nt, p_teams, towner) != 0) { free(towner); return -1; }
     for (int64_t tile = 0; tile < nt; ++tile) {
-        int64_t ti = colmajor ? ti0 + tile % ntr : ti0 + tile / ntc;
-        int64_t tj = colmajor ? tj0 + tile / ntr : tj0 + tile % ntc;
+        int64_t seq = (order & 2) ? nt - 1 - tile : tile;
+        int64_t ti = colmajor ? ti0 + seq % ntr : ti0 + seq / ntc;
+        int64_t tj = colmajor ? tj0 + seq / ntr : tj0 + seq % ntc;
         for (int64_t pos = 0; pos < P; ++pos) {
             int64_t i = ti * BM + pos / BN, j = tj * BN + pos % BN;
             int64_t t = tile * P + pos;

@@ -164,8 +164,10 @@ __global__ void __launch_bounds__(1024) jacobi5_kernel(const __grid_constant__ J
       // interior tile: every position an iteration, no peer boundary row
       // tile id -> (row, column) of the tile grid: row-major (c24) or
       // column-major (UPIR_TILE_COLMAJOR, c35)
-      const int64_t i0 = (a.ti0 + (a.colmajor ? nx % a.ntr : nx / a.ntc)) * BM;
-      const int64_t j0 = (a.tj0 + (a.colmajor ? nx / a.ntr : nx % a.ntc)) * BN;
+      // UPIR_TILE_REVERSE: id k enumerates the tiles from the last one (c36)
+      const int64_t px = a.reverse ? nt - 1 - nx : nx;
+      const int64_t i0 = (a.ti0 + (a.colmajor ? px % a.ntr : px / a.ntc)) * BM;
+      const int64_t j0 = (a.tj0 + (a.colmajor ? px / a.ntr : px % a.ntc)) * BN;
       const bool fast = !TRACE && a.inner_chunk == 4 && (a.units & 31) == 0 && i0 >= a.lb0 && i0 + BM <= a.ub0 &&
                         j0 >= a.lb1 && j0 + BN <= a.ub1 && (a.ld & 3) == 0 && ((uintptr_t)a.out & 15) == 0 &&
                         (!a.win || ((a.send_up_row < i0 || a.send_up_row >= i0 + BM) &&

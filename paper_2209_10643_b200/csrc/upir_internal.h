@@ -132,6 +132,7 @@ struct JacobiArgs {
   int32_t *trace;       // [team | unit | hits] planes of ntiles*BM*BN int32, or null
   int32_t units;        // num_units (set by the launcher; the CTA may carry a producer warp)
   int32_t colmajor;     // tile ids column-major (UPIR_TILE_COLMAJOR, reading c35)
+  int32_t reverse;      // tile ids from the last tile (UPIR_TILE_REVERSE)
   // fused halo exchange with ranks r-1 / r+1 (peer mode): null win = off
   unsigned long long *win;          // local peer window
   unsigned long long *win_up, *win_dn;  // neighbours' windows (null at the ends)

@@ -897,8 +897,8 @@ static upir_status validate_loop(const upir_spmd_desc *sd, const upir_loop_desc 
   if (st != UPIR_OK) return st;
   if (!l) return fail(UPIR_E_INVALID, "loop descriptor is NULL");
   if (l->simdlen > 4096) return fail(UPIR_E_INVALID, "simdlen %u outside [0, 4096]", l->simdlen);
-  if ((l->flags & UPIR_TILE_COLMAJOR) && kind != UPIR_BODY_JACOBI5)
-    return fail(UPIR_E_UNSUPPORTED, "UPIR_TILE_COLMAJOR is implemented for JACOBI5 tiled nests only");
+  if ((l->flags & (UPIR_TILE_COLMAJOR | UPIR_TILE_REVERSE)) && kind != UPIR_BODY_JACOBI5)
+    return fail(UPIR_E_UNSUPPORTED, "UPIR_TILE_COLMAJOR / UPIR_TILE_REVERSE are implemented for JACOBI5 tiled nests only");
   int64_t T;
   st = upir_loop_normalize(l, &T, nullptr);
   if (st != UPIR_OK) return st;
@@ -1341,6 +1341,7 @@ static upir_status exec_jacobi(upir_spmd s, const upir_loop_desc *l, const upir_
   JacobiArgs a;
   memset(&a, 0, sizeof a);
   a.colmajor = (l->flags & UPIR_TILE_COLMAJOR) ? 1 : 0;
+  a.reverse = (l->flags & UPIR_TILE_REVERSE) ? 1 : 0;
   if (peer) {
     int64_t plan[8];
     if ((st = upir_halo_plan(mo->dist.n_rows, mo->dist.halo_rows, c->rank, c->nranks, plan)) != UPIR_OK) return st;

@@ -86,7 +86,7 @@ def test_c4_f32_3xtf32_8192_sampled_rows(ctx, teams, units, rows):
     _check_rows(C, rows, synth.f32_sym)
 
 
-def _jacobi_run(ctx, n, S, teams, bm, bn, cluster, policy=U.SCHED_STATIC):
+def _jacobi_run(ctx, n, S, teams, bm, bn, cluster, policy=U.SCHED_STATIC, alternate=True):
     """The bench's Jacobi geometry: S sweeps captured as one CUDA graph."""
     import torch
     if cluster:
@@ -98,14 +98,16 @@ def _jacobi_run(ctx, n, S, teams, bm, bn, cluster, policy=U.SCHED_STATIC):
     mb = U.upir_data_adopt(ctx, b_t, d) if cluster else U.upir_data_adopt(ctx, b_t)
     U.upir_synth_fill(ctx, ma, 4, 5, 0, n, n)
     U.upir_synth_fill(ctx, mb, 4, 5, 0, n, n)
-    loop = U.loop_desc([1, 1], [n - 1, n - 1], tile=[bm, bn], policy=policy, chunk=1,
-                       distribute=U.DIST_TEAMS, inner_chunk=4)
+    # the bench's form: the tile order alternates per sweep (UPIR_TILE_REVERSE, reading c38)
+    loops = [U.loop_desc([1, 1], [n - 1, n - 1], tile=[bm, bn], policy=policy, chunk=1,
+                         distribute=U.DIST_TEAMS, inner_chunk=4, flags=f)
+             for f in (0, U.TILE_REVERSE if alternate else 0)]
     s = U.upir_spmd_launch(ctx, U.spmd_desc(teams, 256, U.TARGET_CLUSTER if cluster else U.TARGET_GPU))
     bodies = [U.body(U.BODY_JACOBI5, U.F32, in0=ma, out=mb, ld=(n, 0, 0), dims=(n, 0, 0)),
               U.body(U.BODY_JACOBI5, U.F32, in0=mb, out=ma, ld=(n, 0, 0), dims=(n, 0, 0))]
     U.upir_graph_begin(ctx)
     for k in range(S):
-        U.upir_loop_exec(s, loop, bodies[k % 2])
+        U.upir_loop_exec(s, loops[k % 2], bodies[k % 2])
     g = U.upir_graph_end(ctx)
     U.upir_graph_launch(ctx, g)
     U.upir_sync(ctx)

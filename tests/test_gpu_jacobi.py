@@ -269,3 +269,61 @@ def test_colmajor_rejected_for_other_bodies(ctx):
     U.upir_spmd_end(s)
     U.upir_data_unmap(ctx, m)
     U.upir_sync(ctx)
+
+
+@pytest.mark.parametrize("colmajor", [False, True])
+@pytest.mark.parametrize("policy,chunk", [(U.SCHED_STATIC, 1), (U.SCHED_STATIC, 0), (U.SCHED_DYNAMIC, 1)])
+def test_jacobi_reverse_order_parity_and_trace(ctx, colmajor, policy, chunk):
+    """UPIR_TILE_REVERSE (reading c38): the same grid as the plain order, bit
+    for bit (the order only moves work in time / between teams); the tile ->
+    team and position -> unit maps bit-exact against the oracle's reversed
+    enumeration (dynamic: position -> unit and coverage)."""
+    g = synth.jacobi_init(150, 520)
+    teams, units, tile = 7, 128, (16, 256)
+    base = U.TILE_COLMAJOR if colmajor else 0
+    plain, _ = jacobi_gpu(ctx, g, 3, teams=teams, units=units, tile=tile, policy=policy, chunk=chunk, flags=base)
+    rev, _ = jacobi_gpu(ctx, g, 3, teams=teams, units=units, tile=tile, policy=policy, chunk=chunk,
+                        flags=base | U.TILE_REVERSE)
+    assert (rev == plain).all()
+    assert rel(rev, oracle.jacobi5(g, 3)) <= 1e-5
+    _, tr = jacobi_gpu(ctx, g, 1, teams=teams, units=units, tile=tile, policy=policy, chunk=chunk,
+                       trace=True, flags=base | U.TILE_REVERSE)
+    n = len(tr) // 3
+    team, unit, hits = tr[:n], tr[n:2 * n], tr[2 * n:]
+    ot, ou = oracle.tiled_owner(1, 149, 1, 519, tile[0], tile[1], OPOL[policy], chunk, teams, 4, units,
+                                colmajor=colmajor, reverse=True)
+    it = ot >= 0
+    assert (hits[it] == 1).all() and (hits[~it] == 0).all()
+    assert (unit[it] == ou[it]).all()
+    if policy == U.SCHED_STATIC:
+        assert (team[it] == ot[it]).all()
+
+
+def test_jacobi_alternating_order_sweeps_equal_plain(ctx):
+    """bench.py's C3 form: sweeps alternating the plain and the reversed tile
+    order in one CUDA graph give the plain sweeps' grid bit for bit."""
+    g = synth.jacobi_init(203, 1028)
+    ny, nx = g.shape
+    outs = []
+    for alternate in (False, True):
+        a, b = g.copy(), g.copy()
+        ma, mb = U.upir_data_map(ctx, a, U.MAP_TOFROM), U.upir_data_map(ctx, b, U.MAP_TOFROM)
+        s = U.upir_spmd_launch(ctx, U.spmd_desc(9, 256))
+        loops = [U.loop_desc([1, 1], [ny - 1, nx - 1], tile=[16, 256], chunk=1, distribute=U.DIST_TEAMS,
+                             inner_chunk=4, flags=f) for f in (0, U.TILE_REVERSE)]
+        bodies = [U.body(U.BODY_JACOBI5, U.F32, in0=ma, out=mb, ld=(nx, 0, 0), dims=(ny, 0, 0)),
+                  U.body(U.BODY_JACOBI5, U.F32, in0=mb, out=ma, ld=(nx, 0, 0), dims=(ny, 0, 0))]
+        U.upir_graph_begin(ctx)
+        for k in range(10):
+            U.upir_loop_exec(s, loops[k % 2] if alternate else loops[0], bodies[k % 2])
+        gr = U.upir_graph_end(ctx)
+        U.upir_graph_launch(ctx, gr)
+        U.upir_sync(ctx)
+        U.upir_graph_destroy(gr)
+        U.upir_spmd_end(s)
+        U.upir_data_unmap(ctx, mb)
+        U.upir_data_unmap(ctx, ma)
+        U.upir_sync(ctx)
+        outs.append(a)
+    assert (outs[0] == outs[1]).all()
+    assert rel(outs[1], oracle.jacobi5(g, 10)) <= 1e-5

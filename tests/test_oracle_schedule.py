@@ -321,3 +321,43 @@ def test_simdlen_one_is_plain():
     for pol, c in ((oracle.STATIC, 0), (oracle.STATIC, 7), (oracle.DYNAMIC, 3), (oracle.GUIDED, 2)):
         for u in range(4):
             assert oracle.schedule_chunks(pol, c, 99, 4, u, simdlen=1) == oracle.schedule_chunks(pol, c, 99, 4, u)
+
+
+@pytest.mark.parametrize("colmajor", [False, True])
+@pytest.mark.parametrize("chunk,p", [(1, 3), (0, 4), (2, 5)])
+def test_tiled_owner_reverse_bruteforce(colmajor, chunk, p):
+    """Reading c38: with the reversed tile order, id k is the tile the plain
+    (row- or column-major) order numbers nt - 1 - k; the tile-loop schedule
+    maps ids to teams unchanged and the intra-tile rule is unchanged.  Brute
+    force of the reading, and every iteration executed exactly once."""
+    lb0, ub0, lb1, ub1, BM, BN, ic, units = 1, 10, 1, 13, 4, 8, 4, 5
+    team, unit = oracle.tiled_owner(lb0, ub0, lb1, ub1, BM, BN, oracle.STATIC, chunk, p, ic, units,
+                                    colmajor=colmajor, reverse=True)
+    ntr, ntc = 3, 2
+    nt = ntr * ntc
+    plain = ([(ti, tj) for tj in range(ntc) for ti in range(ntr)] if colmajor
+             else [(ti, tj) for ti in range(ntr) for tj in range(ntc)])
+    tiles = [plain[nt - 1 - k] for k in range(nt)]
+
+    def tile_team(tid):
+        if chunk == 0:
+            q, r = divmod(nt, p)
+            lo = 0
+            for u in range(p):
+                n = q + (u < r)
+                if lo <= tid < lo + n:
+                    return u
+                lo += n
+        return (tid // chunk) % p
+    t = 0
+    seen = []
+    for tid, (ti, tj) in enumerate(tiles):
+        for pos in range(BM * BN):
+            i, j = ti * BM + pos // BN, tj * BN + pos % BN
+            if lb0 <= i < ub0 and lb1 <= j < ub1:
+                assert team[t] == tile_team(tid) and unit[t] == (pos // ic) % units
+                seen.append((i, j))
+            else:
+                assert team[t] == -1 and unit[t] == -1
+            t += 1
+    assert sorted(seen) == [(i, j) for i in range(lb0, ub0) for j in range(lb1, ub1)]
