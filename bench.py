@@ -1102,7 +1102,7 @@ def bench_matvec(E, n=16384):
     U.upir_synth_fill(E.ctx, ma, 1, 3)
     U.upir_synth_fill(E.ctx, mx, 1, 1)
     out = {}
-    for teams, units in ((592, 256), (296, 512)):
+    for teams, units in ((592, 256), (1184, 128), (296, 512)):
         s = U.upir_spmd_launch(E.ctx, U.spmd_desc(teams, units))
         loop = U.loop_desc(0, n, chunk=1, distribute=U.DIST_TEAMS, inner_chunk=4)
         body = U.body(U.BODY_MATVEC, U.F32, in0=ma, in1=mx, out=my, ld=(n, 0, 0), dims=(n, n, 0))
