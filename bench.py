@@ -418,7 +418,8 @@ def run_upir(args):
     if E.world == 1 and not args.no_kernels:
         # the tensor-core matmuls last: they drive the board into its power cap
         # (sw_power_cap), which would otherwise throttle the ALU-bound stencil
-        for name, fn in (("axpy", bench_axpy), ("jacobi", bench_jacobi), ("matvec", bench_matvec),
+        for name, fn in (("paper_sizes", bench_paper_sizes), ("axpy", bench_axpy), ("jacobi", bench_jacobi),
+                         ("matvec", bench_matvec),
                          ("stencil7", bench_stencil7), ("matmul", bench_matmul)):
             if want(args, name):
                 try:
@@ -434,7 +435,7 @@ def run_upir(args):
         out["kernels"] = kernels
         # the same summary, compact, as the line's last key: a reader of the
         # line's tail (driver logs keep the end) still sees every body
-        out["summary_tail"] = {k: next((round(v[f], 4) for f in ("frac", "value", "GB/s", "TFLOP/s") if f in v),
+        out["summary_tail"] = {k: next((round(v[f], 4) for f in ("frac", "value", "GB/s", "TFLOP/s", "e2e_ms") if f in v),
                                        v.get("error") or v.get("unavailable"))
                                for k, v in out["summary"].items()}
         print(json.dumps(clean(out)), flush=True)
@@ -1122,6 +1123,141 @@ def bench_matvec(E, n=16384):
                         "k static,4 over units + reduction(+); 4 B of A per iteration", "bound": "hbm",
             "summary": {"matvec_16384": dict(config=best, **{k: out[best][k] for k in ("GB/s", "frac", "frac_8TB")})},
             "peak_source": E.peak_src, "paper_v100_end_to_end_ms": 583.45, **out}
+
+
+def bench_paper_sizes(E):
+    """SURVEY 8(d) context runs at the paper's own sizes (PAPER.md:1276-1280,
+    1355-1359, 1426-1430, 1504-1509; V100 times incl. offload, BASELINE.md
+    §1a): each kernel alone, and end to end through the C-ABI with pinned
+    host buffers -- map(to) / map(tofrom) of the inputs, the loop, map(from)
+    of the output, unmap, sync.  Context only (another GPU, other compilers)."""
+    import ctypes
+    torch, U = E.torch, E.U
+    ctx = E.ctx
+
+    def host(shape, dt, dist_code=None, stream=0, rows=0, cols=0):
+        """pinned host buffer, filled by the on-device generator (dist_code) and copied back"""
+        t = torch.empty(shape, dtype=dt, pin_memory=True)
+        if dist_code is not None:
+            d = torch.empty(shape, dtype=dt, device="cuda")
+            torch.cuda.synchronize()
+            m = U.upir_data_adopt(ctx, d)
+            U.upir_synth_fill(ctx, m, dist_code, stream, 0, rows, cols)
+            U.upir_data_unmap(ctx, m)
+            U.upir_sync(ctx)
+            t.copy_(d)
+            del d
+        ct = {torch.float32: ctypes.c_float, torch.int64: ctypes.c_int64}[dt]
+        return t, np.ctypeslib.as_array(ctypes.cast(t.data_ptr(), ctypes.POINTER(ct)), shape=(t.numel(),))
+
+    def timed(fn, reps):
+        fn()
+        U.upir_sync(ctx)
+        t0 = time.perf_counter()
+        for _ in range(reps):
+            fn()
+        U.upir_sync(ctx)
+        return (time.perf_counter() - t0) * 1e3 / reps
+
+    out = {}
+    # AXPY, n = 102,400,000, a = 2 (the paper's int a)
+    n = 102_400_000
+    xt, xh = host(n, torch.float32, 0, 1)
+    yt, yh = host(n, torch.float32, 0, 2)
+
+    def axpy_e2e():
+        mx, my = U.upir_data_map(ctx, xh, U.MAP_TO), U.upir_data_map(ctx, yh, U.MAP_TOFROM)
+        sp = U.upir_spmd_launch(ctx, U.spmd_desc(592, 256))
+        U.upir_loop_exec(sp, U.loop_desc(0, n, chunk=4), U.body(U.BODY_AXPY, U.F32, in0=mx, out=my, alpha=2.0))
+        U.upir_spmd_end(sp)
+        U.upir_data_unmap(ctx, my)
+        U.upir_data_unmap(ctx, mx)
+
+    e2e = timed(axpy_e2e, 3)
+    mx, my = U.upir_data_map(ctx, xh, U.MAP_TO), U.upir_data_map(ctx, yh, U.MAP_TO)
+    sp = U.upir_spmd_launch(ctx, U.spmd_desc(592, 256))
+    k = E.time_stream(lambda: U.upir_loop_exec(sp, U.loop_desc(0, n, chunk=4),
+                                               U.body(U.BODY_AXPY, U.F32, in0=mx, out=my, alpha=2.0)), 10)
+    U.upir_spmd_end(sp)
+    U.upir_data_unmap(ctx, my)
+    U.upir_data_unmap(ctx, mx)
+    U.upir_sync(ctx)
+    out["axpy_n102400000"] = {"kernel_ms": k, "e2e_ms": e2e, "paper_v100_upir_ms": 702.39}
+    del xt, yt, xh, yh
+    # matmul N = 1024 (fp32 inputs via 3xTF32; the paper gives no precision)
+    N = 1024
+    at, ah = host(N * N, torch.float32, 1, 3)
+    bt, bh = host(N * N, torch.float32, 1, 4)
+    ct, ch_ = host(N * N, torch.float32)
+    body_of = lambda ma, mb, mc: U.body(U.BODY_MATMUL, U.F32, in0=ma, in1=mb, out=mc,  # noqa: E731
+                                        ld=(N, N, N), dims=(N, N, N))
+    mloop = U.loop_desc([0, 0], [N, N], chunk=1, distribute=U.DIST_TEAMS)
+
+    def mm_e2e():
+        ma, mb, mc = U.upir_data_map(ctx, ah, U.MAP_TO), U.upir_data_map(ctx, bh, U.MAP_TO), \
+            U.upir_data_map(ctx, ch_, U.MAP_FROM)
+        sp = U.upir_spmd_launch(ctx, U.spmd_desc(148, 384))
+        U.upir_loop_exec(sp, mloop, body_of(ma, mb, mc))
+        U.upir_spmd_end(sp)
+        for m in (mc, mb, ma):
+            U.upir_data_unmap(ctx, m)
+
+    e2e = timed(mm_e2e, 5)
+    ma, mb, mc = U.upir_data_map(ctx, ah, U.MAP_TO), U.upir_data_map(ctx, bh, U.MAP_TO), U.upir_data_map(ctx, ch_, U.MAP_FROM)
+    sp = U.upir_spmd_launch(ctx, U.spmd_desc(148, 384))
+    k = E.time_stream(lambda: U.upir_loop_exec(sp, mloop, body_of(ma, mb, mc)), 10)
+    U.upir_spmd_end(sp)
+    for m in (mc, mb, ma):
+        U.upir_data_unmap(ctx, m)
+    U.upir_sync(ctx)
+    out["matmul_n1024_fp32"] = {"kernel_ms": k, "e2e_ms": e2e, "paper_v100_upir_ms": 976.88}
+    del at, bt, ct
+    # matvec N = 16384
+    N = 16384
+    at, ah = host(N * N, torch.float32, 1, 3)
+    xt2, xh2 = host(N, torch.float32, 1, 1)
+    yt2, yh2 = host(N, torch.float32)
+    vloop = U.loop_desc(0, N, chunk=1, distribute=U.DIST_TEAMS, inner_chunk=4)
+
+    def mv_e2e():
+        ma, mx, my = U.upir_data_map(ctx, ah, U.MAP_TO), U.upir_data_map(ctx, xh2, U.MAP_TO), \
+            U.upir_data_map(ctx, yh2, U.MAP_FROM)
+        sp = U.upir_spmd_launch(ctx, U.spmd_desc(592, 256))
+        U.upir_loop_exec(sp, vloop, U.body(U.BODY_MATVEC, U.F32, in0=ma, in1=mx, out=my, ld=(N, 0, 0), dims=(N, N, 0)))
+        U.upir_spmd_end(sp)
+        for m in (my, mx, ma):
+            U.upir_data_unmap(ctx, m)
+
+    e2e = timed(mv_e2e, 3)
+    out["matvec_n16384"] = {"e2e_ms": e2e, "paper_v100_upir_ms": 583.45,
+                            "kernel_ms": "see kernels.matvec (same size)"}
+    del at, xt2, yt2
+    # 7x7 filter stencil N = 2048, one sweep
+    N = 2048
+    gt, gh = host(N * N, torch.float32, 4, 5, N, N)
+    ot, oh = host(N * N, torch.float32)
+    v = np.array([1, 2, 3, 4, 3, 2, 1], np.float64)
+    wh = (np.outer(v, v) / 256.0).astype(np.float32).reshape(-1)
+    sloop = U.loop_desc([3, 3], [N - 3, N - 3], tile=[8, 512], chunk=1, distribute=U.DIST_TEAMS, inner_chunk=4)
+
+    def st_e2e():
+        mi, mo, mw = U.upir_data_map(ctx, gh, U.MAP_TO), U.upir_data_map(ctx, oh, U.MAP_FROM), \
+            U.upir_data_map(ctx, wh, U.MAP_TO)
+        sp = U.upir_spmd_launch(ctx, U.spmd_desc(444, 128))
+        U.upir_loop_exec(sp, sloop, U.body(U.BODY_STENCIL2D, U.F32, in0=mi, in1=mw, out=mo, ld=(N, 0, 0),
+                                           dims=(N, 7, 0)))
+        U.upir_spmd_end(sp)
+        for m in (mw, mo, mi):
+            U.upir_data_unmap(ctx, m)
+
+    e2e = timed(st_e2e, 5)
+    out["stencil7_n2048"] = {"e2e_ms": e2e, "paper_v100_upir_ms": 56.47,
+                             "kernel_ms": "see kernels.stencil7 (2048^2 rows)"}
+    del gt, ot
+    summ = {k: {"e2e_ms": round(v["e2e_ms"], 3), "paper_v100_ms": v["paper_v100_upir_ms"]} for k, v in out.items()}
+    return {"workload": "the paper's own sizes (SURVEY 8(d) context runs): kernel alone and end to end through the "
+                        "C-ABI with pinned host buffers (map to / from in the step); paper = UPIR on one V100 incl. "
+                        "offload, mean of 10 (PAPER.md:1219)", "data": "synthetic", "summary": summ, **out}
 
 
 def bench_matmul(E, n=8192):
