@@ -18,4 +18,7 @@ timeout 900 $CS --tool memcheck --error-exitcode 9 python -m pytest tests/test_g
 timeout 1500 $CS --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_stream.py -q -x -k "misaligned and direct or axpy_misaligned or axpy_parity and 148-256 and direct" > gpurun_out/san_mem_align.log 2>&1; echo memcheck align rc=$?
 timeout 900 $CS --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_data.py -q -x -k "pipelined or graph_capture or async_halo" > gpurun_out/san_mem_data.log 2>&1; echo memcheck data rc=$?
 timeout 900 $CS --tool racecheck --racecheck-report all --error-exitcode 9 python -m pytest tests/test_gpu_stencil.py -q -x -k "strip_tiles" > gpurun_out/san_race_stencil.log 2>&1; echo racecheck stencil rc=$?
+# the reversed Jacobi tile order, the async allreduce, the world-1 communicator combine path
+timeout 900 $CS --tool memcheck --error-exitcode 9 python -m pytest tests/test_gpu_jacobi.py tests/test_gpu_data.py -q -x -k "reverse or alternating or async_allreduce or world_combine" > gpurun_out/san_mem_r2b.log 2>&1; echo memcheck r2b rc=$?
+timeout 900 $CS --tool racecheck --racecheck-report all --error-exitcode 9 python -m pytest tests/test_gpu_jacobi.py -q -x -k "reverse and 1-static" > gpurun_out/san_race_rev.log 2>&1; echo racecheck reverse rc=$?
 for f in gpurun_out/san_*.log; do echo "== $f"; grep -E "ERROR SUMMARY|passed|failed" $f | tail -3; done
