@@ -393,3 +393,29 @@ def test_async_allreduce_join_and_wait(ctx, graph):
     assert (out.cpu().numpy() == ref).all()
     U.upir_data_unmap(ctx, mx)
     U.upir_sync(ctx)
+
+
+def test_async_edges(ctx):
+    """Edge cases of the NEXT #1 calls: an empty FORWARD_ASYNC section is a
+    no-op, an out-of-range one is rejected; upir_reduce_async rejects bad
+    arguments before enqueueing anything; a count of 1 works."""
+    x = np.arange(1000, dtype=np.int64)
+    m = U.upir_data_map(ctx, x, U.MAP_ALLOC)
+    U.upir_data_update_section(ctx, m, 0, 0, U.UPDATE_FORWARD_ASYNC)
+    with pytest.raises(U.UpirError):
+        U.upir_data_update_section(ctx, m, 7992, 16, U.UPDATE_FORWARD_ASYNC)
+    with pytest.raises(U.UpirError):
+        U.upir_data_update_section(ctx, m, 0, 8, 3)
+    U.upir_data_unmap(ctx, m)
+    U.upir_sync(ctx)
+    a = torch.tensor([5], dtype=torch.int64, device="cuda")
+    b = torch.zeros(1, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    for bad in (dict(count=0), dict(dtype=U.BF16), dict(op=7)):
+        kw = dict(op=U.OP_SUM, dtype=U.I64, count=1)
+        kw.update(bad)
+        with pytest.raises(U.UpirError):
+            U.upir_reduce_async(ctx, kw["op"], kw["dtype"], a, kw["count"], b)
+    tok = U.upir_reduce_async(ctx, U.OP_SUM, U.I64, a, 1, b)
+    U.upir_sync(ctx, U.SYNC_WAIT, token=tok)
+    assert b.item() == 5

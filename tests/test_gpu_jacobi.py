@@ -327,3 +327,26 @@ def test_jacobi_alternating_order_sweeps_equal_plain(ctx):
         outs.append(a)
     assert (outs[0] == outs[1]).all()
     assert rel(outs[1], oracle.jacobi5(g, 10)) <= 1e-5
+
+
+def test_reverse_rejected_for_other_bodies_and_subspace_parity(ctx):
+    """UPIR_TILE_REVERSE is a JACOBI5 tile order: other bodies reject it
+    (UPIR_E_UNSUPPORTED, no side effect); on a sub-space that starts and ends
+    mid-tile the reversed order writes exactly the iterations of the plain
+    order."""
+    x = np.zeros(1024, np.float32)
+    m = U.upir_data_map(ctx, x, U.MAP_TO)
+    s = U.upir_spmd_launch(ctx, U.spmd_desc(4, 128))
+    r = torch.zeros(1, dtype=torch.float32, device="cuda")
+    with pytest.raises(U.UpirError) as ei:
+        U.upir_loop_exec(s, U.loop_desc(0, 1024, flags=U.TILE_REVERSE), U.body(U.BODY_REDUCE, U.F32, in0=m),
+                         [U.reduction(U.OP_SUM, U.F32, r)])
+    assert ei.value.status == U.E_UNSUPPORTED
+    U.upir_spmd_end(s)
+    U.upir_data_unmap(ctx, m)
+    U.upir_sync(ctx)
+    g = synth.jacobi_init(120, 700)
+    space = (7, 101, 13, 650)
+    plain, _ = jacobi_gpu(ctx, g, 2, teams=5, units=256, tile=(16, 256), space=space)
+    rev, _ = jacobi_gpu(ctx, g, 2, teams=5, units=256, tile=(16, 256), space=space, flags=U.TILE_REVERSE)
+    assert (rev == plain).all()
