@@ -159,3 +159,60 @@ def test_c5b_32768_one_gpu_windows(ctx, policy):
     for k in range(1, 8):   # the would-be slab boundaries of an 8-GPU split
         corners.append((4096 * k - 8, cols[k % 3]))
     _check_windows(res, n, S, corners)
+
+
+def _stencil_sweep(ctx, n, w, teams, units, tile):
+    """One STENCIL2D sweep over the seeded n x n grid (bench.py's
+    bench_stencil7 form: adopted device grids, synth fill, static,1 tiles,
+    static,4 units); returns the output grid."""
+    import torch
+    a_t = torch.empty(n * n, dtype=torch.float32, device="cuda")
+    b_t = torch.empty(n * n, dtype=torch.float32, device="cuda")
+    w_t = torch.from_numpy(np.ascontiguousarray(w, dtype=np.float32).ravel()).cuda()
+    torch.cuda.synchronize()
+    ma, mb, mw = U.upir_data_adopt(ctx, a_t), U.upir_data_adopt(ctx, b_t), U.upir_data_adopt(ctx, w_t)
+    U.upir_synth_fill(ctx, ma, 4, 5, 0, n, n)
+    U.upir_synth_fill(ctx, mb, 4, 5, 0, n, n)
+    F = w.shape[0]
+    R = (F - 1) // 2
+    s = U.upir_spmd_launch(ctx, U.spmd_desc(teams, units))
+    U.upir_loop_exec(s, U.loop_desc([R, R], [n - R, n - R], tile=list(tile), chunk=1, distribute=U.DIST_TEAMS,
+                                    inner_chunk=4),
+                     U.body(U.BODY_STENCIL2D, U.F32, in0=ma, in1=mw, out=mb, ld=(n, 0, 0), dims=(n, F, 0)))
+    U.upir_spmd_end(s)
+    for m in (mw, mb, ma):
+        U.upir_data_unmap(ctx, m)
+    U.upir_sync(ctx)
+    del a_t
+    return b_t.view(n, n)
+
+
+def test_stencil7_8192_bench_geometry_windows(ctx):
+    """The 7x7 stencil line of bench.py: 8192^2, 8 x 512 tiles static,1 over
+    444 teams x 128 units (the strip path: FFMA2 column pairs), checked on
+    windows against the fp64 oracle (reading c28), and the
+    whole grid bit-identical (by value) to the generic static,4 path
+    (96 units: one 4-output chunk at a time, scalar FMA in the same
+    (filter row, column) order)."""
+    import torch
+    n, R = 8192, 3
+    rng = np.random.default_rng(2209)
+    w = rng.uniform(-1, 1, (7, 7)).astype(np.float32)
+    got = _stencil_sweep(ctx, n, w, 444, 128, (8, 512))
+    # tile-row (8) / tile-column (512) / warp-strip (128) boundaries, the
+    # 444-team wrap (tile 444 = tile row 27, column 12), corners and edges
+    corners = [(0, 0), (0, n - 16), (n - 16, 0), (n - 16, n - 16), (8 - 8, 512 - 8), (27 * 8 - 4, 12 * 512 - 8),
+               (4096 - 8, 128 - 8), (5000, 3000), (3, 7), (n - 19, n - 23)]
+    h = 16
+    for (r0, c0) in corners:
+        r1, c1 = r0 + h, c0 + h
+        wr0, wr1 = max(0, r0 - R), min(n, r1 + R)
+        wc0, wc1 = max(0, c0 - R), min(n, c1 + R)
+        win = synth.jacobi_init_rows(n, n, wr0, wr1)[:, wc0:wc1]
+        ref = oracle.stencil2d(win, w, 1)[r0 - wr0:r1 - wr0, c0 - wc0:c1 - wc0]
+        scale = oracle.stencil2d(np.abs(win), np.abs(w), 1)[r0 - wr0:r1 - wr0, c0 - wc0:c1 - wc0]
+        g = got[r0:r1, c0:c1].cpu().numpy()
+        err = (np.abs(g - ref) / np.maximum(scale, 1e-30)).max()
+        assert err <= 1e-5, ((r0, c0), err)
+    generic = _stencil_sweep(ctx, n, w, 444, 96, (8, 512))
+    assert torch.equal(got, generic)
