@@ -1085,7 +1085,10 @@ def bench_stencil7(E):
                         "the teams, static,4 over the units; one sweep per launch",
             "bound": "alu",
             "summary": {"stencil7_8192": {"TFLOP/s": round(best, 2), "GLUP/s": round(out[best_k]["GLUP/s"], 1),
-                                          "frac": round(best / FFMA_TFLOPS, 4), "config": best_k}},
+                                          "frac": round(best / FFMA_TFLOPS, 4), "config": best_k,
+                                          # the ridge point: 8 B of HBM per update alongside
+                                          "hbm_GB/s": round(8 * out[best_k]["GLUP/s"], 1),
+                                          "hbm_frac": round(8 * out[best_k]["GLUP/s"] / E.peak, 4)}},
             "roofline": {"bound": "alu", "achieved": best, "peak": FFMA_TFLOPS, "unit": "TFLOP/s",
                          "frac": best / FFMA_TFLOPS, "peak_source": "measured FFMA microbenchmark (DESIGN.md §6)"},
             "paper_v100_end_to_end_ms_2048": 56.47, **out}
