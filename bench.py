@@ -899,7 +899,7 @@ def line_c5b(E, S=100):
             "metric": "GLUP/s of the whole job ((n-2)^2 x 100 lattice updates)", "scaling": "strong",
             "n_gpus": E.world, "rows_identical_across_paths": all(v == vals[0] for v in vals),
             "kernel": f"jacobi5_kernel<{bm},{bn}>", "paths": paths,
-            "traffic_per_sweep_1gpu": {"dynamic,2": ncu_traffic("jacobi32k"), "static,1": ncu_traffic("jacobi32k_static"),
+            "traffic_per_sweep_1gpu": {"dynamic,1": ncu_traffic("jacobi32k"), "static,1": ncu_traffic("jacobi32k_static"),
                                        "algorithmic": 8 * (n - 2) * (n - 2), "unit": "DRAM bytes (ncu)"}}
 
 

@@ -20,7 +20,7 @@ prof reduce_f32 stream_loop reduce_f32
 prof axpy stream_loop axpy_static
 prof axpy4 stream_loop axpy_static4
 prof jacobi jacobi5 jacobi_c3
-prof jacobi32k jacobi5 jacobi_c5b UPIR_JACOBI_POLICY=dynamic UPIR_JACOBI_CHUNK=2
+prof jacobi32k jacobi5 jacobi_c5b UPIR_JACOBI_POLICY=dynamic UPIR_JACOBI_CHUNK=1
 prof jacobi32k_static jacobi5 jacobi_c5b
 prof matmul_pair matmul_pair_kernel matmul_pair
 prof matmul_pair_f32 matmul_pair_f32 matmul_f32_pair
