@@ -792,7 +792,10 @@ def line_c5b(E, S=100):
     stream order) before every sweep; 'nccl_async' = async HALO (copy stream)
     overlapped with the interior rows, JOIN, then the two boundary rows;
     'peer' = boundary rows stored into the neighbours' halos inside each
-    sweep (fused).  Every variant is 100 sweeps captured as one CUDA graph.
+    sweep (fused); 'peer_halo' / 'peer_async' = the same mappings driven by
+    upir_sync(HALO) (UPIR_HALO_EXPLICIT sweeps; the exchange kernel in stream
+    order, or async on the copy stream behind the interior rows).  Every
+    variant is 100 sweeps captured as one CUDA graph.
     Strong scaling."""
     torch, U, args = E.torch, E.U, E.args
     n = int(os.environ.get("UPIR_C5B_N", 32768))
@@ -852,11 +855,38 @@ def line_c5b(E, S=100):
             for e in edges:
                 U.upir_loop_exec(s, e, body)
 
+    # explicit-halo forms over the peer mappings (UPIR_HALO_EXPLICIT sweeps,
+    # upir_sync(HALO) runs the peer-copy exchange kernel)
+    X = U.HALO_EXPLICIT
+    fulls_x = [U.loop_desc([1, 1], [n - 1, n - 1], tile=[bm, bn], policy=tpol, chunk=tch, distribute=U.DIST_TEAMS,
+                           inner_chunk=4, flags=f | X) for f in (tfl, rfl)]
+    inners_x = [U.loop_desc([r_lo + 1, 1], [r_hi - 1, n - 1], tile=[bm, bn], policy=tpol, chunk=tch,
+                            distribute=U.DIST_TEAMS, inner_chunk=4, flags=f | X) for f in (tfl, rfl)]
+    edges_x = [U.loop_desc([r, 1], [r + 1, n - 1], tile=[bm, bn], policy=U.SCHED_STATIC, chunk=1,
+                           distribute=U.DIST_TEAMS, inner_chunk=4, flags=X) for r in sorted({r_lo, r_hi - 1})]
+
+    def sweeps_peer_halo():
+        for k in range(S):
+            src, body = bodies[k % 2]
+            U.upir_sync(E.ctx, U.SYNC_HALO, halo_map=src)   # peer-copy exchange kernel, stream order
+            U.upir_loop_exec(s, fulls_x[k % 2], body)
+
+    def sweeps_peer_async():
+        for k in range(S):
+            src, body = bodies[k % 2]
+            tok = U.upir_sync(E.ctx, U.SYNC_HALO, halo_map=src, async_=True)   # copy stream
+            U.upir_loop_exec(s, inners_x[k % 2], body)
+            U.upir_sync(E.ctx, U.SYNC_JOIN, token=tok)
+            for e in edges_x:
+                U.upir_loop_exec(s, e, body)
+
     variants = [("local", sweeps_sync)] if E.world == 1 else []
     if E.world > 1:
         variants += [("nccl", sweeps_sync if E.has_comm else None),
                      ("nccl_async", sweeps_async if E.has_comm else None),
-                     ("peer", sweeps_fused if E.peer_ok() else None)]
+                     ("peer", sweeps_fused if E.peer_ok() else None),
+                     ("peer_halo", sweeps_peer_halo if E.peer_ok() else None),
+                     ("peer_async", sweeps_peer_async if E.peer_ok() else None)]
     if E.world == 1:
         variants.append(("split_async", sweeps_async))   # the async structure at N = 1 (empty exchange)
     paths, checks = {}, {}
@@ -867,7 +897,7 @@ def line_c5b(E, S=100):
             paths[path] = {"unavailable": "no communicator (shared-GPU test world)" if path.startswith("nccl")
                            else "GPUs cannot map each other's memory"}
             continue
-        if path == "peer":
+        if path == "peer":   # the peer_* variants after it reuse the imported mappings
             U.upir_peer_share(E.ctx, [ma, mb])
         U.upir_synth_fill(E.ctx, ma, 4, 5, 0, n, n)
         U.upir_synth_fill(E.ctx, mb, 4, 5, 0, n, n)

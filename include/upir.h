@@ -261,6 +261,13 @@ typedef enum { UPIR_DIST_TEAMS = 1, UPIR_DIST_UNITS = 2, UPIR_DIST_TEAMS_UNITS =
  * tiles by this id.  Sweeps that alternate it start on the rows the previous
  * sweep wrote last (still in L2).  Other bodies: UPIR_E_UNSUPPORTED. */
 #define UPIR_TILE_REVERSE 16u
+/* UPIR_HALO_EXPLICIT (JACOBI5 on a CLUSTER target whose out map has imported
+ * neighbour buffers): do not fuse the halo exchange into the sweep (no peer
+ * stores of the boundary rows, no in-kernel neighbour waits); the program
+ * exchanges with upir_sync(HALO), synchronously or async (arrive-compute /
+ * JOIN), over the same peer mappings.  Without imported buffers: no effect.
+ * Other bodies: ignored. */
+#define UPIR_HALO_EXPLICIT 32u
 /* UPIR_WORLD_REDUCE: the loop's reductions are combined over all ranks as part
  * of the loop (Fig. 7 'allreduce' with ranks as units fused into the loop's
  * end barrier): every rank receives
@@ -426,6 +433,16 @@ upir_status upir_reduce_async(upir_ctx ctx, int32_t op, int32_t dtype, const voi
  *   WAIT          : step 'wait-release': the host waits for *token and frees it.
  *   HALO          : send/recv of halo rows of a BLOCK-distributed map with
  *                   ranks r-1 / r+1 (Fig. 7 send/recv), in stream order.
+ *                   Transport: when the map has its neighbours' buffers
+ *                   imported (upir_peer_import) and every rank's peer window
+ *                   is imported, one kernel stores this rank's boundary rows
+ *                   into the neighbours' halo rows over the peer mappings
+ *                   (NVLink) and waits for theirs (release / acquire
+ *                   counters in the peer windows, shared with the fused
+ *                   sweeps' protocol); otherwise NCCL send/recv (a
+ *                   communicator-less world: UPIR_E_UNSUPPORTED).  A map
+ *                   last written by a fused peer-mode sweep is already
+ *                   exchanged (no-op).
  *                   With token != NULL (*token == NULL on entry) it is the
  *                   async 'arrive-compute' step: the exchange runs on the copy
  *                   stream, overlapping later compute work, and *token

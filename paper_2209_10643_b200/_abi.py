@@ -24,6 +24,7 @@ WORLD_REDUCE = 2
 TILE_COLMAJOR = 4
 WORLD_VIA_COMM = 8
 TILE_REVERSE = 16
+HALO_EXPLICIT = 32
 PEER_REC_BYTES = 256
 BODY_AXPY, BODY_REDUCE, BODY_JACOBI5, BODY_MATMUL, BODY_MATVEC, BODY_STENCIL2D = 0, 1, 2, 3, 4, 5
 OP_SUM, OP_MAX, OP_MIN = 0, 1, 2

@@ -134,6 +134,52 @@ cudaError_t launch_peer_barrier(unsigned long long *win, int nranks, cudaStream_
   return cudaGetLastError();
 }
 
+// ---- upir_sync(HALO) over peer mappings ------------------------------------
+// Generation g = exchanges + fused peer-mode sweeps this rank completed (the
+// fused sweeps' counter, so both kinds interleave).  (1) Wait until both
+// neighbours completed generation g - 1: they are done reading the halo rows
+// I overwrite (their previous use of this buffer ended before their
+// exchange g - 1 began).  (2) Store my boundary rows into their halo rows.
+// (3) Publish: system-scope fence, release-add on their delivery counters.
+// (4) Wait until both delivered generation g into my halo rows (acquire),
+// then count the generation.
+__device__ __forceinline__ void copy_bytes(char *dst, const char *src, int64_t n) {
+  if ((((uintptr_t)dst | (uintptr_t)src | (uintptr_t)n) & 15) == 0) {
+    uint4 *d = reinterpret_cast<uint4 *>(dst);
+    const uint4 *s = reinterpret_cast<const uint4 *>(src);
+    for (int64_t e = threadIdx.x; e < n / 16; e += blockDim.x) d[e] = s[e];
+  } else {
+    for (int64_t e = threadIdx.x; e < n; e += blockDim.x) dst[e] = src[e];
+  }
+}
+
+__global__ void __launch_bounds__(1024) peer_halo_kernel(PeerHaloArgs a) {
+  __shared__ unsigned long long g;
+  if (threadIdx.x == 0) {
+    g = *reinterpret_cast<volatile unsigned long long *>(a.win + WIN_HALO_GEN);
+    if (a.win_up) wait_geq_sys(a.win + WIN_HALO_FROM_UP, g);
+    if (a.win_dn) wait_geq_sys(a.win + WIN_HALO_FROM_DN, g);
+  }
+  __syncthreads();
+  if (a.win_up) copy_bytes(a.dst_up, a.src_up, a.bytes_up);
+  if (a.win_dn) copy_bytes(a.dst_dn, a.src_dn, a.bytes_dn);
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (a.win_up) red_release_sys_add(a.win_up + WIN_HALO_FROM_DN, 1ull);
+    if (a.win_dn) red_release_sys_add(a.win_dn + WIN_HALO_FROM_UP, 1ull);
+    if (a.win_up) wait_geq_sys(a.win + WIN_HALO_FROM_UP, g + 1ull);
+    if (a.win_dn) wait_geq_sys(a.win + WIN_HALO_FROM_DN, g + 1ull);
+    fence_proxy_async_global();   // later TMA reads of the halo rows see the delivery
+    *reinterpret_cast<volatile unsigned long long *>(a.win + WIN_HALO_GEN) = g + 1ull;
+  }
+}
+
+cudaError_t launch_peer_halo(const PeerHaloArgs &a, cudaStream_t s) {
+  peer_halo_kernel<<<1, 1024, 0, s>>>(a);
+  return cudaGetLastError();
+}
+
 // ---- synthetic inputs: counter-based splitmix64 -
 // An implementation of the recipe independent of synth/ (host numpy).
 __device__ __forceinline__ unsigned long long sm_mix(unsigned long long z) {

@@ -103,6 +103,15 @@ cudaError_t launch_reduce_array(int op, int dtype, const void *in, int64_t count
 cudaError_t launch_peer_drain(unsigned long long *win, int has_up, int has_dn, cudaStream_t s);
 // Barrier over all ranks through the peer windows (communicator-less worlds).
 cudaError_t launch_peer_barrier(unsigned long long *win, int nranks, cudaStream_t s);
+// upir_sync(HALO) over peer mappings: store my boundary rows [src, src +
+// bytes) into the neighbours' halo rows (dst), publish, wait for theirs.
+struct PeerHaloArgs {
+  unsigned long long *win, *win_up, *win_dn;   // my window, neighbours' windows (null: none)
+  const char *src_up, *src_dn;                 // my rows sent to rank - 1 / rank + 1
+  char *dst_up, *dst_dn;                       // their halo rows (peer mappings)
+  int64_t bytes_up, bytes_dn;
+};
+cudaError_t launch_peer_halo(const PeerHaloArgs &a, cudaStream_t s);
 // result_r = init_r (+) g[0][r] (+) ... (+) g[nranks-1][r] over gathered
 // [nranks][2] partial words of a loop's reductions (int64, or fp64 rounded once).
 cudaError_t launch_world_combine(const unsigned long long *gathered, int nranks, int nred, const RedSpec *reds,

@@ -1328,7 +1328,8 @@ static upir_status exec_jacobi(upir_spmd s, const upir_loop_desc *l, const upir_
     return fail(UPIR_E_INVALID, "JACOBI5 iteration space must lie in the grid interior [1,ny-1) x [1,ld-1)");
   // peer mode: the out map has imported neighbour buffers (fused halo)
   const upir_map mo = b->out;
-  const bool peer = sd.target == UPIR_TARGET_CLUSTER && c->nranks > 1 && (mo->peer_dev[0] || mo->peer_dev[1]);
+  const bool peer = sd.target == UPIR_TARGET_CLUSTER && c->nranks > 1 && (mo->peer_dev[0] || mo->peer_dev[1]) &&
+                    !(l->flags & UPIR_HALO_EXPLICIT);
   if (sd.target == UPIR_TARGET_CLUSTER && c->nranks > 1) {
     upir_map m = b->in0;
     if (m->dist.pattern != UPIR_PATTERN_BLOCK) return fail(UPIR_E_INVALID, "cluster JACOBI5 needs BLOCK-distributed maps");
@@ -1767,14 +1768,40 @@ static upir_status halo_exchange(upir_ctx c, upir_map m, cudaStream_t strm) {
     return fail(UPIR_E_INVALID, "HALO needs a BLOCK-distributed map with halo_rows >= 1");
   if (c->nranks == 1) return UPIR_OK;
   if (m->halo_fused) return UPIR_OK;   // exchanged inside the peer-mode sweep that wrote it
-  if (!c->comm)
-    return fail(UPIR_E_UNSUPPORTED, "communicator-less world: halos move only inside peer-mode sweeps");
   int64_t plan[8];
   upir_status st = upir_halo_plan(m->dist.n_rows, m->dist.halo_rows, c->rank, c->nranks, plan);
   if (st != UPIR_OK) return st;
   const int64_t rb = m->dist.row_elems * m->dist.elem_bytes;
   char *base = (char *)m->dev;
   auto at = [&](int64_t row) { return base + (row - m->loc_row_lo) * rb; };
+  const bool need_up = plan[1] > plan[0], need_dn = plan[5] > plan[4];
+  const bool peer_ok = world_ready(c) && (!need_up || m->peer_dev[0]) && (!need_dn || m->peer_dev[1]) &&
+                       (m->peer_dev[0] || m->peer_dev[1]);
+  if (peer_ok) {
+    // peer mappings: my send rows land at the same global rows of the neighbour's buffer
+    PeerHaloArgs a;
+    memset(&a, 0, sizeof a);
+    a.win = c->win;
+    if (need_up) {
+      a.win_up = c->peer_win[c->rank - 1];
+      a.src_up = at(plan[0]);
+      a.dst_up = (char *)m->peer_dev[0] + (plan[0] - m->peer_row0[0]) * rb;
+      a.bytes_up = (plan[1] - plan[0]) * rb;
+    }
+    if (need_dn) {
+      a.win_dn = c->peer_win[c->rank + 1];
+      a.src_dn = at(plan[4]);
+      a.dst_dn = (char *)m->peer_dev[1] + (plan[4] - m->peer_row0[1]) * rb;
+      a.bytes_dn = (plan[5] - plan[4]) * rb;
+    }
+    cudaError_t e = launch_peer_halo(a, strm);
+    if (e != cudaSuccess) return fail(UPIR_E_CUDA, "peer halo launch failed: %s", cudaGetErrorString(e));
+    c->launches++;
+    return UPIR_OK;
+  }
+  if (!c->comm)
+    return fail(UPIR_E_UNSUPPORTED,
+                "communicator-less world: halos move through imported peer buffers (upir_peer_import) only");
   // Fig. 7 send/recv with rank units, in stream order before the next sweep
   NCCL_TRY(ncclGroupStart());
   if (plan[1] > plan[0]) {

@@ -78,7 +78,11 @@ def world_reduce_worker(rank, world, port, out_dir, n, reps, use_graph):
     dist.destroy_process_group()
 
 
-def jacobi_worker(rank, world, port, out_dir, ny, nx, S, tile, use_graph, adopt):
+def jacobi_worker(rank, world, port, out_dir, ny, nx, S, tile, use_graph, adopt, mode="fused"):
+    """mode: 'fused' = peer-mode sweeps (halo stores inside the sweep);
+    'explicit' = UPIR_HALO_EXPLICIT sweeps + upir_sync(HALO) over the peer
+    mappings before each sweep; 'async' = async HALO on the copy stream
+    overlapping the interior rows, JOIN, then the boundary rows."""
     dist, U, ctx = _setup(rank, world, port)
     import torch
 
@@ -106,10 +110,30 @@ def jacobi_worker(rank, world, port, out_dir, ny, nx, S, tile, use_graph, adopt)
     bodies = [U.body(U.BODY_JACOBI5, U.F32, in0=ma, out=mb, ld=(nx, 0, 0), dims=(ny, 0, 0)),
               U.body(U.BODY_JACOBI5, U.F32, in0=mb, out=ma, ld=(nx, 0, 0), dims=(ny, 0, 0))]
 
+    lo, hi = U.upir_dist_owned_rows(ny, rank, world)
+    r_lo, r_hi = max(lo, 1), min(hi, ny - 1)
+    xl = U.loop_desc([1, 1], [ny - 1, nx - 1], tile=list(tile), distribute=U.DIST_TEAMS, inner_chunk=4,
+                     flags=U.HALO_EXPLICIT)
+    inner = U.loop_desc([r_lo + 1, 1], [r_hi - 1, nx - 1], tile=list(tile), distribute=U.DIST_TEAMS, inner_chunk=4,
+                        flags=U.HALO_EXPLICIT)
+    edges = [U.loop_desc([r, 1], [r + 1, nx - 1], tile=list(tile), distribute=U.DIST_TEAMS, inner_chunk=4,
+                         flags=U.HALO_EXPLICIT) for r in sorted({r_lo, r_hi - 1}) if r_lo < r_hi]
+
     def sweeps(k0, count):
         for k in range(k0, k0 + count):
-            U.upir_loop_exec(s, loop, bodies[k % 2])
-            U.upir_sync(ctx, U.SYNC_HALO, halo_map=bodies[k % 2].out)   # fused: returns at once
+            if mode == "fused":
+                U.upir_loop_exec(s, loop, bodies[k % 2])
+                U.upir_sync(ctx, U.SYNC_HALO, halo_map=bodies[k % 2].out)   # fused: returns at once
+            elif mode == "explicit":
+                U.upir_sync(ctx, U.SYNC_HALO, halo_map=bodies[k % 2].in0)   # peer-mapping exchange kernel
+                U.upir_loop_exec(s, xl, bodies[k % 2])
+            else:
+                tok = U.upir_sync(ctx, U.SYNC_HALO, halo_map=bodies[k % 2].in0, async_=True)
+                if r_hi - r_lo > 2:
+                    U.upir_loop_exec(s, inner, bodies[k % 2])
+                U.upir_sync(ctx, U.SYNC_JOIN, token=tok)
+                for e in edges:
+                    U.upir_loop_exec(s, e, bodies[k % 2])
 
     if use_graph:
         assert S % 4 == 0
@@ -122,7 +146,6 @@ def jacobi_worker(rank, world, port, out_dir, ny, nx, S, tile, use_graph, adopt)
     else:
         sweeps(0, S)
     U.upir_spmd_end(s)
-    lo, hi = U.upir_dist_owned_rows(ny, rank, world)
     if adopt:
         U.upir_sync(ctx)
         fin = (keep[0] if S % 2 == 0 else keep[1]).cpu().numpy()

@@ -28,6 +28,21 @@ def test_library_exports_every_declared_symbol():
     assert set(names) == set(U._abi.DECLARED)
 
 
+def test_header_flag_macros_match_the_binding():
+    """Every `#define UPIR_<NAME> <n>u` flag of include/upir.h has the same
+    value under the binding's name (argument marshalling must not drift)."""
+    src = open(os.path.join(ROOT, "include", "upir.h")).read()
+    defs = dict(re.findall(r"#define UPIR_([A-Z_0-9]+) (\d+)u?\b", src))
+    flags = {k: v for k, v in defs.items() if k not in ("H",) and not k.endswith("_H")}
+    assert {"NOWAIT", "WORLD_REDUCE", "TILE_COLMAJOR", "WORLD_VIA_COMM", "TILE_REVERSE", "HALO_EXPLICIT"} <= set(flags)
+    for k, v in flags.items():
+        if hasattr(U, k):
+            assert getattr(U, k) == int(v), k
+    vals = [int(flags[k]) for k in ("NOWAIT", "WORLD_REDUCE", "TILE_COLMAJOR", "WORLD_VIA_COMM", "TILE_REVERSE",
+                                    "HALO_EXPLICIT")]
+    assert len(set(vals)) == len(vals) and all(v & (v - 1) == 0 for v in vals)   # distinct single bits
+
+
 def test_version():
     assert "sm_100a" in U.upir_version()
 

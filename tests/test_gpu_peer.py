@@ -88,7 +88,30 @@ def _jacobi_one_rank(g, S, tile):
     (2, 70, 132, 4, (8, 64), False, True),
 ])
 def test_fused_halo_jacobi(upir, tmp_path, world, ny, nx, S, tile, use_graph, adopt):
-    _spawn(peer_worker.jacobi_worker, world, str(tmp_path), ny, nx, S, tile, use_graph, adopt)
+    _jacobi_multirank_check(tmp_path, world, ny, nx, S, tile, use_graph, adopt, "fused")
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("world,ny,nx,S,tile,use_graph,mode", [
+    (2, 70, 132, 6, (8, 64), False, "explicit"),
+    (3, 61, 200, 5, (8, 64), False, "explicit"),
+    (2, 67, 264, 8, (16, 256), True, "explicit"),
+    (2, 70, 132, 6, (8, 64), False, "async"),
+    (3, 61, 200, 5, (8, 64), False, "async"),
+    (3, 67, 264, 8, (16, 256), True, "async"),
+])
+def test_peer_halo_exchange_jacobi(upir, tmp_path, world, ny, nx, S, tile, use_graph, mode):
+    """upir_sync(HALO) over the peer mappings (Fig. 7 send/recv, PAPER.md:889;
+    SURVEY 8(e) 1-row halos) with a NON-empty exchange at world sizes 2 / 3:
+    UPIR_HALO_EXPLICIT sweeps with the exchange before each sweep, and the
+    async two-step form (arrive-compute on the copy stream
+    overlapping the interior rows, JOIN, then the boundary rows).  The
+    assembled grid equals one rank's bit for bit."""
+    _jacobi_multirank_check(tmp_path, world, ny, nx, S, tile, use_graph, False, mode)
+
+
+def _jacobi_multirank_check(tmp_path, world, ny, nx, S, tile, use_graph, adopt, mode):
+    _spawn(peer_worker.jacobi_worker, world, str(tmp_path), ny, nx, S, tile, use_graph, adopt, mode)
     g = synth.jacobi_init(ny, nx)
     got = np.concatenate([np.load(tmp_path / f"jac_{r}.npy") for r in range(world)])
     assert got.shape == (ny, nx)
