@@ -442,7 +442,10 @@ upir_status upir_reduce_async(upir_ctx ctx, int32_t op, int32_t dtype, const voi
  *                   sweeps' protocol); otherwise NCCL send/recv (a
  *                   communicator-less world: UPIR_E_UNSUPPORTED).  A map
  *                   last written by a fused peer-mode sweep is already
- *                   exchanged (no-op).
+ *                   exchanged: HALO then only waits (stream order) for the
+ *                   neighbours' deliveries of that sweep.  Both share one generation counter per
+ *                   rank: a fused sweep may not run while an async exchange
+ *                   of this rank is still in flight (JOIN first).
  *                   With token != NULL (*token == NULL on entry) it is the
  *                   async 'arrive-compute' step: the exchange runs on the copy
  *                   stream, overlapping later compute work, and *token

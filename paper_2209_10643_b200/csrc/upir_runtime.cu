@@ -1767,7 +1767,20 @@ static upir_status halo_exchange(upir_ctx c, upir_map m, cudaStream_t strm) {
   if (m->dist.pattern != UPIR_PATTERN_BLOCK || m->dist.halo_rows < 1)
     return fail(UPIR_E_INVALID, "HALO needs a BLOCK-distributed map with halo_rows >= 1");
   if (c->nranks == 1) return UPIR_OK;
-  if (m->halo_fused) return UPIR_OK;   // exchanged inside the peer-mode sweep that wrote it
+  if (m->halo_fused) {
+    // exchanged inside the peer-mode sweep that wrote it: a later peer-mode
+    // sweep waits for the neighbours' deliveries in-kernel, anything else
+    // (an explicit sweep, a read-back) needs them here -- drain them in
+    // stream order
+    const bool up = c->rank > 0 && c->peer_win[c->rank - 1];
+    const bool dn = c->rank + 1 < c->nranks && c->rank + 1 < WIN_MAX_RANKS && c->peer_win[c->rank + 1];
+    if (up || dn) {
+      cudaError_t e = launch_peer_drain(c->win, up, dn, strm);
+      if (e != cudaSuccess) return fail(UPIR_E_CUDA, "peer drain launch failed: %s", cudaGetErrorString(e));
+      c->launches++;
+    }
+    return UPIR_OK;
+  }
   int64_t plan[8];
   upir_status st = upir_halo_plan(m->dist.n_rows, m->dist.halo_rows, c->rank, c->nranks, plan);
   if (st != UPIR_OK) return st;

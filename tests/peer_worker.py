@@ -81,8 +81,9 @@ def world_reduce_worker(rank, world, port, out_dir, n, reps, use_graph):
 def jacobi_worker(rank, world, port, out_dir, ny, nx, S, tile, use_graph, adopt, mode="fused"):
     """mode: 'fused' = peer-mode sweeps (halo stores inside the sweep);
     'explicit' = UPIR_HALO_EXPLICIT sweeps + upir_sync(HALO) over the peer
-    mappings before each sweep; 'async' = async HALO on the copy stream
-    overlapping the interior rows, JOIN, then the boundary rows."""
+    mappings before each sweep; 'mixed' = every third sweep fused, the others
+    explicit; 'async' = async HALO on the copy stream overlapping the interior
+    rows, JOIN, then the boundary rows."""
     dist, U, ctx = _setup(rank, world, port)
     import torch
 
@@ -123,10 +124,15 @@ def jacobi_worker(rank, world, port, out_dir, ny, nx, S, tile, use_graph, adopt,
         for k in range(k0, k0 + count):
             if mode == "fused":
                 U.upir_loop_exec(s, loop, bodies[k % 2])
-                U.upir_sync(ctx, U.SYNC_HALO, halo_map=bodies[k % 2].out)   # fused: returns at once
+                U.upir_sync(ctx, U.SYNC_HALO, halo_map=bodies[k % 2].out)   # fused: drains the deliveries
             elif mode == "explicit":
                 U.upir_sync(ctx, U.SYNC_HALO, halo_map=bodies[k % 2].in0)   # peer-mapping exchange kernel
                 U.upir_loop_exec(s, xl, bodies[k % 2])
+            elif mode == "mixed":
+                # fused and explicit sweeps interleaved on one generation
+                # counter: HALO(in) is a no-op after a fused sweep
+                U.upir_sync(ctx, U.SYNC_HALO, halo_map=bodies[k % 2].in0)
+                U.upir_loop_exec(s, loop if k % 3 == 0 else xl, bodies[k % 2])
             else:
                 tok = U.upir_sync(ctx, U.SYNC_HALO, halo_map=bodies[k % 2].in0, async_=True)
                 if r_hi - r_lo > 2:

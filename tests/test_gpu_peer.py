@@ -99,6 +99,8 @@ def test_fused_halo_jacobi(upir, tmp_path, world, ny, nx, S, tile, use_graph, ad
     (2, 70, 132, 6, (8, 64), False, "async"),
     (3, 61, 200, 5, (8, 64), False, "async"),
     (3, 67, 264, 8, (16, 256), True, "async"),
+    (3, 61, 200, 7, (8, 64), False, "mixed"),
+    (2, 67, 264, 12, (16, 256), True, "mixed"),
 ])
 def test_peer_halo_exchange_jacobi(upir, tmp_path, world, ny, nx, S, tile, use_graph, mode):
     """upir_sync(HALO) over the peer mappings (Fig. 7 send/recv, PAPER.md:889;
