@@ -247,3 +247,42 @@ def matmul_rows_worker(rank, world, port, out_dir, M, N, K, dtype_name):
     dist.barrier()   # no collective on the data path: host barrier only
     U.upir_finalize(ctx)
     dist.destroy_process_group()
+
+
+def halo_unit_worker(rank, world, port, out_dir, n_rows, row_elems, dtype_name, halo_rows, use_async, reps):
+    """upir_sync(HALO) alone over the peer mappings: every rep each rank
+    writes a rank / rep / row pattern into its owned rows (torch, then a
+    device sync), exchanges, and records its halo rows."""
+    dist, U, ctx = _setup(rank, world, port)
+    import torch
+    tdt = {"i32": torch.int32, "i64": torch.int64, "u8": torch.uint8}[dtype_name]
+    esz = torch.tensor([], dtype=tdt).element_size()
+    d = U.dist(n_rows, row_elems, esz, halo_rows=halo_rows)
+    lo, hi = U.upir_dist_owned_rows(n_rows, rank, world)
+    r0, r1 = max(0, lo - halo_rows), min(n_rows, hi + halo_rows)
+    t = torch.full((r1 - r0, row_elems), -1 if dtype_name != "u8" else 255, dtype=tdt, device="cuda")
+    torch.cuda.synchronize()
+    m = U.upir_data_adopt(ctx, t, d, nbytes=n_rows * row_elems * esz)
+    U.upir_peer_share(ctx, [m])
+    rows = torch.arange(r0, r1, device="cuda", dtype=torch.int64)[:, None].expand(-1, row_elems)
+    cols = torch.arange(row_elems, device="cuda", dtype=torch.int64)[None, :]
+    got = []
+    for rep in range(reps):
+        val = (rank * 100000 + rep * 1000 + rows * 7 + cols) if dtype_name != "u8" else \
+            (rank * 37 + rep * 11 + rows * 3 + cols) % 251
+        t[lo - r0:hi - r0] = val[lo - r0:hi - r0].to(tdt)
+        torch.cuda.synchronize()
+        if use_async:
+            tok = U.upir_sync(ctx, U.SYNC_HALO, halo_map=m, async_=True)
+            U.upir_sync(ctx, U.SYNC_JOIN, token=tok)
+        else:
+            U.upir_sync(ctx, U.SYNC_HALO, halo_map=m)
+        U.upir_sync(ctx)
+        got.append(t.cpu().numpy().astype(np.int64))
+        U.upir_sync(ctx, U.SYNC_WORLD_BARRIER)   # every rank read its halos before the next rep's writes
+    np.save(os.path.join(out_dir, f"halo_{rank}.npy"), np.stack(got))
+    np.save(os.path.join(out_dir, f"halo_rng_{rank}.npy"), np.array([lo, hi, r0, r1]))
+    U.upir_data_unmap(ctx, m)
+    U.upir_sync(ctx, U.SYNC_WORLD_BARRIER)
+    U.upir_finalize(ctx)
+    dist.destroy_process_group()

@@ -170,3 +170,37 @@ def test_multirank_matmul_block_rows(upir, tmp_path, world, M, N, K, dt):
     one = np.load(tmp_path / "mm_0.npy")
     if dt == "bf16":
         assert (got == one).all()
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("world,n_rows,row_elems,dt,halo_rows,use_async", [
+    (2, 20, 36, "i64", 1, False),    # 288-B rows: 16-B vector copies
+    (3, 23, 37, "i32", 2, False),    # 148-B rows: byte copies, 2 halo rows
+    (3, 17, 50, "u8", 3, True),      # async (copy stream) + JOIN, 3 halo rows
+    (2, 9, 64, "i32", 2, True),
+])
+def test_peer_halo_exchange_rows(upir, tmp_path, world, n_rows, row_elems, dt, halo_rows, use_async):
+    """upir_sync(HALO) over the peer mappings on its own (Fig. 7 send/recv,
+    PAPER.md:889): after each of 3 exchanges every rank's halo rows hold its
+    neighbours' owned rows of that round (plan of upir_halo_plan, checked here
+    from the block rule), its own rows untouched, for several element sizes,
+    halo depths and row sizes that do / do not allow 16-B copies."""
+    reps = 3
+    _spawn(peer_worker.halo_unit_worker, world, str(tmp_path), n_rows, row_elems, dt, halo_rows, use_async, reps)
+    owner = {}
+    for r in range(world):
+        lo, hi = U.upir_dist_owned_rows(n_rows, r, world)
+        for i in range(lo, hi):
+            owner[i] = r
+
+    def val(r, rep, i, j):
+        return (r * 100000 + rep * 1000 + i * 7 + j) if dt != "u8" else (r * 37 + rep * 11 + i * 3 + j) % 251
+
+    j = np.arange(row_elems)
+    for r in range(world):
+        got = np.load(tmp_path / f"halo_{r}.npy")
+        lo, hi, r0, r1 = np.load(tmp_path / f"halo_rng_{r}.npy")
+        for rep in range(reps):
+            for i in range(r0, r1):
+                want = val(owner[i], rep, i, j)   # own rows: mine; halo rows: the neighbour's
+                assert (got[rep, i - r0] == want).all(), (r, rep, i)
