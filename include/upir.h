@@ -403,9 +403,13 @@ upir_status upir_schedule_chunks(int32_t policy, int64_t chunk, int64_t T, int64
  *   DEVICE : dev_out[0] = (+) over the count elements of dev_in (fixed tree).
  *   WORLD  : 'allreduce' with ranks as primary/secondary units: dev_in holds
  *            count elements on every rank; every rank receives, element-wise,
- *            the combination over ranks in ascending rank order (NCCL
- *            all-gather of the partials + ordered combine: deterministic and
- *            identical on every rank, reading c10). */
+ *            the combination over ranks in ascending rank order (fp32 in fp64,
+ *            rounded once: deterministic and identical on every rank, reading
+ *            c10).  Transport: with every rank's peer window imported and
+ *            count <= 65536, one kernel stages dev_in in this rank's window,
+ *            publishes it to every rank and combines all ranks' staged values
+ *            over NVLink; otherwise NCCL all-gather + the same ordered
+ *            combine (a communicator-less world: UPIR_E_UNSUPPORTED). */
 typedef enum { UPIR_SCOPE_DEVICE = 0, UPIR_SCOPE_WORLD = 1 } upir_scope;
 upir_status upir_reduce(upir_ctx ctx, int32_t op, int32_t dtype, const void *dev_in,
                         int64_t count, void *dev_out, int32_t scope);
@@ -417,8 +421,9 @@ upir_status upir_reduce(upir_ctx ctx, int32_t op, int32_t dtype, const void *dev
  * work issued afterwards does NOT wait for them.  *token (NULL on entry)
  * receives their completion: upir_sync(JOIN, token) makes later compute work
  * wait (device-side), upir_sync(WAIT, token) blocks the host.  dev_in must
- * not be overwritten before the token is released.  nranks == 1: a device
- * copy replaces the all-gather.  Errors as upir_reduce; a non-empty *token is
+ * not be overwritten before the token is released; until then this rank
+ * issues no other WORLD reduction.  nranks == 1: a device copy replaces the
+ * all-gather.  Transport as upir_reduce(WORLD).  Errors as upir_reduce; a non-empty *token is
  * UPIR_E_INVALID. */
 upir_status upir_reduce_async(upir_ctx ctx, int32_t op, int32_t dtype, const void *dev_in,
                               int64_t count, void *dev_out, upir_event *token);

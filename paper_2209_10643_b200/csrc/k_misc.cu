@@ -134,16 +134,8 @@ cudaError_t launch_peer_barrier(unsigned long long *win, int nranks, cudaStream_
   return cudaGetLastError();
 }
 
-// ---- upir_sync(HALO) over peer mappings ------------------------------------
-// Generation g = exchanges + fused peer-mode sweeps this rank completed (the
-// fused sweeps' counter, so both kinds interleave).  (1) Wait until both
-// neighbours completed generation g - 1: they are done reading the halo rows
-// I overwrite (their previous use of this buffer ended before their
-// exchange g - 1 began).  (2) Store my boundary rows into their halo rows.
-// (3) Publish: system-scope fence, release-add on their delivery counters.
-// (4) Wait until both delivered generation g into my halo rows (acquire),
-// then count the generation.
-__device__ __forceinline__ void copy_bytes(char *dst, const char *src, int64_t n) {
+// the CTA copies n bytes (16-B vectors when both ends and n allow)
+__device__ __forceinline__ void copy_bytes_all(char *dst, const char *src, int64_t n) {
   if ((((uintptr_t)dst | (uintptr_t)src | (uintptr_t)n) & 15) == 0) {
     uint4 *d = reinterpret_cast<uint4 *>(dst);
     const uint4 *s = reinterpret_cast<const uint4 *>(src);
@@ -153,6 +145,73 @@ __device__ __forceinline__ void copy_bytes(char *dst, const char *src, int64_t n
   }
 }
 
+// ---- upir_reduce(WORLD) over the peer windows -------------------------------
+// Generation e = peer allreduces this rank completed; its staging half is
+// e & 1.  Every rank: stage dev_in, publish (release add on every window's
+// arrival counter), wait for (e + 1) * N arrivals (acquire), combine rank 0,
+// 1, ... N-1 element-wise exactly as rank_combine_kernel (fp32 in fp64,
+// rounded once).  Staging half e & 1 is rewritten at generation e + 2 only:
+// by then every rank has arrived at e + 1, i.e. finished reading it at e.
+__global__ void __launch_bounds__(1024) peer_allreduce_kernel(unsigned long long *win, int nranks, int op, int dtype,
+                                                              const void *dev_in, int64_t count, void *dev_out) {
+  __shared__ unsigned long long e;
+  if (threadIdx.x == 0) e = *reinterpret_cast<volatile unsigned long long *>(win + WIN_AR_GEN);
+  __syncthreads();
+  const int64_t half = (int64_t)(e & 1ull) * WIN_AR_ELEMS * 8;
+  const int esz = dtype == UPIR_I64 ? 8 : 4;
+  copy_bytes_all(reinterpret_cast<char *>(win) + WIN_AR_OFF + half, reinterpret_cast<const char *>(dev_in),
+                 count * esz);
+  __threadfence_system();
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int q = 0; q < nranks; ++q)
+      red_release_sys_add(reinterpret_cast<unsigned long long *>(win[WIN_PEERS + q]) + WIN_AR_CNT, 1ull);
+    wait_geq_sys(win + WIN_AR_CNT, (e + 1ull) * (unsigned long long)nranks);
+  }
+  __syncthreads();
+  for (int64_t i = threadIdx.x; i < count; i += blockDim.x) {
+    auto staged = [&](int q) {
+      return reinterpret_cast<const char *>(win[WIN_PEERS + q]) + WIN_AR_OFF + half;
+    };
+    if (dtype == UPIR_I64) {
+      unsigned long long acc = (unsigned long long)reinterpret_cast<const long long *>(staged(0))[i];
+      for (int q = 1; q < nranks; ++q) {
+        const long long v = reinterpret_cast<const long long *>(staged(q))[i];
+        if (op == UPIR_OP_SUM) acc += (unsigned long long)v;
+        else if (op == UPIR_OP_MAX) acc = ((long long)acc > v) ? acc : (unsigned long long)v;
+        else acc = ((long long)acc < v) ? acc : (unsigned long long)v;
+      }
+      reinterpret_cast<long long *>(dev_out)[i] = (long long)acc;
+    } else {
+      double acc = reinterpret_cast<const float *>(staged(0))[i];
+      for (int q = 1; q < nranks; ++q) {
+        const double v = reinterpret_cast<const float *>(staged(q))[i];
+        if (op == UPIR_OP_SUM) acc += v;
+        else if (op == UPIR_OP_MAX) acc = fmax(acc, v);
+        else acc = fmin(acc, v);
+      }
+      reinterpret_cast<float *>(dev_out)[i] = (float)acc;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) *reinterpret_cast<volatile unsigned long long *>(win + WIN_AR_GEN) = e + 1ull;
+}
+
+cudaError_t launch_peer_allreduce(unsigned long long *win, int nranks, int op, int dtype, const void *dev_in,
+                                  int64_t count, void *dev_out, cudaStream_t s) {
+  peer_allreduce_kernel<<<1, 1024, 0, s>>>(win, nranks, op, dtype, dev_in, count, dev_out);
+  return cudaGetLastError();
+}
+
+// ---- upir_sync(HALO) over peer mappings ------------------------------------
+// Generation g = exchanges + fused peer-mode sweeps this rank completed (the
+// fused sweeps' counter, so both kinds interleave).  (1) Wait until both
+// neighbours completed generation g - 1: they are done reading the halo rows
+// I overwrite (their previous use of this buffer ended before their
+// exchange g - 1 began).  (2) Store my boundary rows into their halo rows.
+// (3) Publish: system-scope fence, release-add on their delivery counters.
+// (4) Wait until both delivered generation g into my halo rows (acquire),
+// then count the generation.
 __global__ void __launch_bounds__(1024) peer_halo_kernel(PeerHaloArgs a) {
   __shared__ unsigned long long g;
   if (threadIdx.x == 0) {
@@ -161,8 +220,8 @@ __global__ void __launch_bounds__(1024) peer_halo_kernel(PeerHaloArgs a) {
     if (a.win_dn) wait_geq_sys(a.win + WIN_HALO_FROM_DN, g);
   }
   __syncthreads();
-  if (a.win_up) copy_bytes(a.dst_up, a.src_up, a.bytes_up);
-  if (a.win_dn) copy_bytes(a.dst_dn, a.src_dn, a.bytes_dn);
+  if (a.win_up) copy_bytes_all(a.dst_up, a.src_up, a.bytes_up);
+  if (a.win_dn) copy_bytes_all(a.dst_dn, a.src_dn, a.bytes_dn);
   __threadfence_system();
   __syncthreads();
   if (threadIdx.x == 0) {

@@ -30,12 +30,22 @@ enum WinWord : int32_t {
   WIN_WR_GEN = 9,         // world reductions this rank completed
   WIN_BAR_CNT = 10,       // peer-barrier arrivals (monotonic, N per barrier)
   WIN_BAR_GEN = 11,       // peer barriers this rank completed
+  WIN_AR_CNT = 12,        // peer-allreduce arrivals (monotonic, N per upir_reduce(WORLD))
+  WIN_AR_GEN = 13,        // peer allreduces this rank completed
   WIN_WR_SLOTS = 16,      // [2 parity][WIN_MAX_RANKS][2 reductions] partials
   WIN_PEERS = 512,        // [WIN_MAX_RANKS] mapped window pointers
   WIN_WORDS = 576
 };
 constexpr int WIN_MAX_RANKS = 64;
-constexpr size_t WIN_BYTES = 8192;
+// after the 8 KiB of words: the allreduce staging, [2 parity][WIN_AR_ELEMS] x 8 B
+constexpr size_t WIN_AR_OFF = 8192;
+constexpr int64_t WIN_AR_ELEMS = 65536;
+constexpr size_t WIN_BYTES = WIN_AR_OFF + 2 * (size_t)WIN_AR_ELEMS * 8;
+// upir_reduce(WORLD) over the peer windows (count <= WIN_AR_ELEMS): one CTA
+// stages dev_in in its window, publishes to every rank, waits for all, and
+// combines the ranks' staged values in ascending rank order.
+cudaError_t launch_peer_allreduce(unsigned long long *win, int nranks, int op, int dtype, const void *dev_in,
+                                  int64_t count, void *dev_out, cudaStream_t s);
 
 // Streaming bodies.
 enum StreamBody : int32_t { SB_RED_I64 = 0, SB_RED_F32 = 1, SB_AXPY = 2 };

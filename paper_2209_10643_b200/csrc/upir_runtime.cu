@@ -1690,6 +1690,13 @@ extern "C" upir_status upir_reduce(upir_ctx c, int32_t op, int32_t dtype, const 
     return UPIR_OK;
   }
   if (scope != UPIR_SCOPE_WORLD) return fail(UPIR_E_INVALID, "bad scope");
+  if (c->nranks > 1 && world_ready(c) && count <= WIN_AR_ELEMS) {
+    // every rank's window imported: stage, publish and combine over NVLink
+    cudaError_t e = launch_peer_allreduce(c->win, c->nranks, op, dtype, dev_in, count, dev_out, c->compute);
+    if (e != cudaSuccess) return fail(UPIR_E_CUDA, "peer allreduce launch failed: %s", cudaGetErrorString(e));
+    c->launches++;
+    return UPIR_OK;
+  }
   // allreduce over ranks (Fig. 7): all-gather of the partials, then the
   // combine in ascending rank order on every rank (deterministic, c10).
   const size_t need = esz * (size_t)count * (size_t)c->nranks;
@@ -1718,7 +1725,10 @@ extern "C" upir_status upir_reduce_async(upir_ctx c, int32_t op, int32_t dtype, 
   if (*token) return fail(UPIR_E_INVALID, "token out-param must be NULL on entry");
   if (op < UPIR_OP_SUM || op > UPIR_OP_MIN) return fail(UPIR_E_INVALID, "bad op");
   if (dtype != UPIR_I64 && dtype != UPIR_F32) return fail(UPIR_E_INVALID, "dtype must be I64 or F32");
-  if (c->nranks > 1 && !c->comm) return fail(UPIR_E_UNSUPPORTED, "upir_reduce_async needs a communicator");
+  const bool via_peer = c->nranks > 1 && world_ready(c) && count <= WIN_AR_ELEMS;
+  if (c->nranks > 1 && !c->comm && !via_peer)
+    return fail(UPIR_E_UNSUPPORTED, "upir_reduce_async needs a communicator or every rank's peer window "
+                                    "(count <= %lld)", (long long)WIN_AR_ELEMS);
   if (c->sticky != cudaSuccess) return sticky_check(c);
   cudaSetDevice(c->device);
   const size_t esz = dtype == UPIR_I64 ? 8 : 4;
@@ -1736,6 +1746,15 @@ extern "C" upir_status upir_reduce_async(upir_ctx c, int32_t op, int32_t dtype, 
   // arrive-compute: ordered after the compute work so far, on the copy stream
   upir_status st = compute_to_copy(c);
   if (st != UPIR_OK) return undo(st);
+  if (via_peer) {
+    cudaError_t e = launch_peer_allreduce(c->win, c->nranks, op, dtype, dev_in, count, dev_out, c->copy);
+    if (e != cudaSuccess) return undo(fail(UPIR_E_CUDA, "peer allreduce launch failed: %s", cudaGetErrorString(e)));
+    c->launches++;
+    e = cudaEventRecord(ev->ev, c->copy);
+    if (e != cudaSuccess) return undo(fail(UPIR_E_CUDA, "event record: %s", cudaGetErrorString(e)));
+    *token = ev;
+    return UPIR_OK;
+  }
   void *scr = nullptr;
   cudaError_t e = cudaMallocAsync(&scr, need, c->copy);
   if (e != cudaSuccess) return undo(fail(UPIR_E_OOM, "async allreduce scratch: %s", cudaGetErrorString(e)));

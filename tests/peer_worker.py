@@ -286,3 +286,35 @@ def halo_unit_worker(rank, world, port, out_dir, n_rows, row_elems, dtype_name, 
     U.upir_sync(ctx, U.SYNC_WORLD_BARRIER)
     U.upir_finalize(ctx)
     dist.destroy_process_group()
+
+
+def allreduce_worker(rank, world, port, out_dir, count, dtype_name, ops, use_async, reps):
+    """upir_reduce(WORLD) / upir_reduce_async over the peer windows: each rep
+    every rank reduces its own seeded vector element-wise with every other
+    rank's (ascending rank order); interleaved with a device-scope loop to
+    show the async form overlaps nothing it should not."""
+    dist, U, ctx = _setup(rank, world, port)
+    import torch
+
+    import synth
+    U.upir_peer_share(ctx, [])
+    dt = U.I64 if dtype_name == "i64" else U.F32
+    out = []
+    for rep in range(reps):
+        for op in ops:
+            stream = 100 + 10 * rep + rank
+            host = synth.i64_sym(stream, 0, count) if dt == U.I64 else synth.f32_sym(stream, 0, count)
+            x = torch.from_numpy(host).cuda()
+            y = torch.zeros_like(x)
+            torch.cuda.synchronize()
+            if use_async:
+                tok = U.upir_reduce_async(ctx, op, dt, x, count, y)
+                U.upir_sync(ctx, U.SYNC_JOIN, token=tok)
+            else:
+                U.upir_reduce(ctx, op, dt, x, count, y, U.SCOPE_WORLD)
+            U.upir_sync(ctx)
+            out.append(y.cpu().numpy().view(np.int64 if dt == U.I64 else np.int32).astype(np.int64))
+    np.save(os.path.join(out_dir, f"ar_{rank}.npy"), np.stack(out))
+    U.upir_sync(ctx, U.SYNC_WORLD_BARRIER)
+    U.upir_finalize(ctx)
+    dist.destroy_process_group()

@@ -204,3 +204,35 @@ def test_peer_halo_exchange_rows(upir, tmp_path, world, n_rows, row_elems, dt, h
             for i in range(r0, r1):
                 want = val(owner[i], rep, i, j)   # own rows: mine; halo rows: the neighbour's
                 assert (got[rep, i - r0] == want).all(), (r, rep, i)
+
+
+@pytest.mark.timeout(600)
+@pytest.mark.parametrize("world,count,dt,use_async", [
+    (2, 1, "i64", False), (3, 1000, "i64", True), (3, 50_000, "f32", False), (2, 65_536, "f32", True),
+    (3, 777, "f32", True),
+])
+def test_peer_allreduce(upir, tmp_path, world, count, dt, use_async):
+    """upir_reduce(WORLD) and its async two-step form (PAPER.md:889
+    'allreduce', 880-882 arrive-compute / wait-release) over the peer
+    windows at world sizes 2 / 3: element-wise, every rank gets the combine
+    of all ranks in ascending rank order (oracle o8; int64 wrapping sum,
+    fp32 combined in fp64 and rounded once -- reading c10), bit-exact, for
+    sum / max / min over three rounds (both staging halves reused)."""
+    reps, ops = 3, [U.OP_SUM, U.OP_MAX, U.OP_MIN]
+    _spawn(peer_worker.allreduce_worker, world, str(tmp_path), count, dt, ops, use_async, reps)
+    oop = {U.OP_SUM: oracle.SUM, U.OP_MAX: oracle.MAX, U.OP_MIN: oracle.MIN}
+    k = 0
+    got = [np.load(tmp_path / f"ar_{r}.npy") for r in range(world)]
+    for rep in range(reps):
+        for op in ops:
+            vals = [(synth.i64_sym if dt == "i64" else synth.f32_sym)(100 + 10 * rep + r, 0, count)
+                    for r in range(world)]
+            if dt == "i64":
+                want = np.array([oracle.world_reduce(oop[op], [int(v[i]) for v in vals]) for i in range(count)],
+                                np.int64)
+            else:
+                want = np.array([oracle.world_reduce(oop[op], [float(v[i]) for v in vals]) for i in range(count)],
+                                np.float64).astype(np.float32).view(np.int32).astype(np.int64)
+            for r in range(world):
+                assert (got[r][k] == want).all(), (r, rep, op)
+            k += 1
