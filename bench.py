@@ -67,7 +67,8 @@ def parse():
     ap.add_argument("--no-kernels", action="store_true", help="skip the per-body kernel lines")
     ap.add_argument("--no-scaling", action="store_true", help="skip the C5a / C5b / matmul-rows lines")
     ap.add_argument("--lines", default=None,
-                    help="comma list restricting sub-lines: c5a,c5b,mmrows,axpy,jacobi,matvec,stencil7,matmul")
+                    help="comma list restricting sub-lines: c5a,c5b,mmrows,allreduce,axpy,jacobi,matvec,stencil7,"
+                         "matmul")
     return ap.parse_args()
 
 
@@ -407,7 +408,8 @@ def run_upir(args):
     out = bench_c2(E)
     lines = {}
     if not args.no_scaling:
-        for name, fn in (("c5a", line_c5a), ("c5b", line_c5b), ("mmrows", line_matmul_rows)):
+        for name, fn in (("c5a", line_c5a), ("c5b", line_c5b), ("mmrows", line_matmul_rows),
+                         ("allreduce", line_allreduce)):
             if want(args, name):
                 try:
                     lines[name] = fn(E)
@@ -931,6 +933,51 @@ def line_c5b(E, S=100):
             "kernel": f"jacobi5_kernel<{bm},{bn}>", "paths": paths,
             "traffic_per_sweep_1gpu": {"dynamic,1": ncu_traffic("jacobi32k"), "static,1": ncu_traffic("jacobi32k_static"),
                                        "algorithmic": 8 * (n - 2) * (n - 2), "unit": "DRAM bytes (ncu)"}}
+
+
+def line_allreduce(E, counts=(1, 4096, 65536)):
+    """a11 as a standalone collective: microseconds per upir_reduce(WORLD)
+    call (int64 sum, ascending-rank combine) through the peer windows and
+    through NCCL (UPIR_REDUCE_VIA_COMM); at N = 1 the device-copy path.
+    Checked: every rank gets N x the all-ones input."""
+    torch, U = E.torch, E.U
+    cmax = max(counts)
+    x = torch.ones(cmax, dtype=torch.int64, device="cuda")
+    y = torch.zeros(cmax, dtype=torch.int64, device="cuda")
+    torch.cuda.synchronize()
+    variants = [("local", None)] if E.world == 1 else []
+    if E.world > 1:
+        variants += [("nccl", "comm") if E.has_comm else ("nccl", None),
+                     ("peer", "peer") if E.peer_ok() else ("peer", None)]
+    paths, ok = {}, True
+    for path, how in variants:
+        if how is None and E.world > 1:
+            paths[path] = {"unavailable": "no communicator (shared-GPU test world)" if path == "nccl"
+                           else "GPUs cannot map each other's memory"}
+            continue
+        if how == "peer":
+            E.share_windows()
+        if how == "comm":
+            os.environ["UPIR_REDUCE_VIA_COMM"] = "1"
+        try:
+            us = {}
+            for c in counts:
+                step = lambda: U.upir_reduce(E.ctx, U.OP_SUM, U.I64, x, c, y, U.SCOPE_WORLD)   # noqa: E731
+                for _ in range(5):
+                    step()
+                E.barrier()
+                ms_local = E.time_stream(step, 50)
+                E.barrier()
+                (ms,) = E.ranks_max([ms_local])
+                us[str(c)] = ms * 1e3
+                ok = ok and bool((y[:c] == E.world).all().item())
+        finally:
+            os.environ.pop("UPIR_REDUCE_VIA_COMM", None)
+        paths[path] = {"value": us[str(counts[0])], "unit": f"us per call (count {counts[0]})", "us_by_count": us}
+    del x, y
+    return {"workload": "upir_reduce(WORLD) int64 sum, count 1 / 4096 / 65536 elements per rank",
+            "metric": "microseconds per call (max over ranks)", "n_gpus": E.world, "results_correct": ok,
+            "paths": paths}
 
 
 def line_matmul_rows(E, n=8192):

@@ -1690,7 +1690,9 @@ extern "C" upir_status upir_reduce(upir_ctx c, int32_t op, int32_t dtype, const 
     return UPIR_OK;
   }
   if (scope != UPIR_SCOPE_WORLD) return fail(UPIR_E_INVALID, "bad scope");
-  if (c->nranks > 1 && world_ready(c) && count <= WIN_AR_ELEMS) {
+  // measurement hook: UPIR_REDUCE_VIA_COMM=1 keeps the communicator path
+  const bool via_comm = c->comm && getenv("UPIR_REDUCE_VIA_COMM");
+  if (c->nranks > 1 && world_ready(c) && count <= WIN_AR_ELEMS && !via_comm) {
     // every rank's window imported: stage, publish and combine over NVLink
     cudaError_t e = launch_peer_allreduce(c->win, c->nranks, op, dtype, dev_in, count, dev_out, c->compute);
     if (e != cudaSuccess) return fail(UPIR_E_CUDA, "peer allreduce launch failed: %s", cudaGetErrorString(e));
@@ -1725,7 +1727,8 @@ extern "C" upir_status upir_reduce_async(upir_ctx c, int32_t op, int32_t dtype, 
   if (*token) return fail(UPIR_E_INVALID, "token out-param must be NULL on entry");
   if (op < UPIR_OP_SUM || op > UPIR_OP_MIN) return fail(UPIR_E_INVALID, "bad op");
   if (dtype != UPIR_I64 && dtype != UPIR_F32) return fail(UPIR_E_INVALID, "dtype must be I64 or F32");
-  const bool via_peer = c->nranks > 1 && world_ready(c) && count <= WIN_AR_ELEMS;
+  const bool via_peer = c->nranks > 1 && world_ready(c) && count <= WIN_AR_ELEMS &&
+                        !(c->comm && getenv("UPIR_REDUCE_VIA_COMM"));
   if (c->nranks > 1 && !c->comm && !via_peer)
     return fail(UPIR_E_UNSUPPORTED, "upir_reduce_async needs a communicator or every rank's peer window "
                                     "(count <= %lld)", (long long)WIN_AR_ELEMS);
