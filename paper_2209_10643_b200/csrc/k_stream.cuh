@@ -36,6 +36,13 @@
 #include "dev_peer.cuh"
 #include "sched.cuh"
 
+// one-vector-chunk reductions: chunks of a unit in flight (C2, 2^30 int64 /
+// fp32 at 592 x 256, measured on B200: 2 / 4 / 5 / 6 / 7 / 8 -> 6.19 / 7.06 /
+// 7.09 / 7.20 / 7.16 / 6.98 TB/s per C2 step)
+#ifndef UPIR_RED_UF
+#define UPIR_RED_UF 6
+#endif
+
 namespace upir {
 
 static constexpr unsigned FULL = 0xffffffffu;
@@ -304,7 +311,10 @@ __device__ void direct_run(const StreamArgs &a, const LaneWork &w, Acc<BODY, NRE
     int64_t nfull = 0;
     if (lim - VEC - w.lo0 >= 0) nfull = min(w.nk, (lim - VEC - w.lo0) / w.kstride + 1);
     const int64_t e0 = a.lb + w.lo0;
-    for (; j + 4 <= nfull; j += 4) {
+    // reductions: UF one-vector chunks of the unit in flight (loaded, then
+    // combined in chunk order: the unit's partial is the same sequence)
+    constexpr int UF = (BODY == SB_AXPY || TRACE) ? 4 : UPIR_RED_UF;
+    for (; j + UF <= nfull; j += UF) {
       if constexpr (BODY == SB_AXPY && !TRACE) {
         // the 4 chunks' x and y vectors are all loaded before any y' store
         // (the chunks are distinct elements, so this holds even when x and y
@@ -330,19 +340,19 @@ __device__ void direct_run(const StreamArgs &a, const LaneWork &w, Acc<BODY, NRE
 #pragma unroll
         for (int q = 0; q < 4; ++q) direct_vec<BODY, NRED, TRACE>(a, e0 + (j + q) * w.kstride, acc, team, unit);
       } else if constexpr (BODY == SB_RED_I64) {
-        longlong2 v[4];
+        longlong2 v[UF];
         const long long *p = reinterpret_cast<const long long *>(a.in0);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) v[q] = __ldcs(reinterpret_cast<const longlong2 *>(p + e0 + (j + q) * w.kstride));
+        for (int q = 0; q < UF; ++q) v[q] = __ldcs(reinterpret_cast<const longlong2 *>(p + e0 + (j + q) * w.kstride));
 #pragma unroll
-        for (int q = 0; q < 4; ++q) acc_l2(acc, v[q], true, true);
+        for (int q = 0; q < UF; ++q) acc_l2(acc, v[q], true, true);
       } else {
-        float4 v[4];
+        float4 v[UF];
         const float *p = reinterpret_cast<const float *>(a.in0);
 #pragma unroll
-        for (int q = 0; q < 4; ++q) v[q] = __ldcs(reinterpret_cast<const float4 *>(p + e0 + (j + q) * w.kstride));
+        for (int q = 0; q < UF; ++q) v[q] = __ldcs(reinterpret_cast<const float4 *>(p + e0 + (j + q) * w.kstride));
 #pragma unroll
-        for (int q = 0; q < 4; ++q) acc_f4(acc, v[q], true, true, true, true);
+        for (int q = 0; q < UF; ++q) acc_f4(acc, v[q], true, true, true, true);
       }
     }
     for (; j < nfull; ++j) direct_vec<BODY, NRED, TRACE>(a, e0 + j * w.kstride, acc, team, unit);
