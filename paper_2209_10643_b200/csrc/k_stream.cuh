@@ -12,7 +12,7 @@
 //  DIRECT (default): every unit loads its own elements.  One-vector chunks
 //           (chunked static / dynamic with c = one 16-B vector): adjacent
 //           units own adjacent vectors, so a warp's loads are coalesced (the
-//           x / y of 4 chunks in flight).  Long chunks (static block, large
+//           x / y of 4 chunks in flight; reductions 6 chunks).  Long chunks (static block, large
 //           c): each unit streams its own range with 256-bit loads
 //           (ld.global.cs.L2::256B), several in flight; vectors are aligned by
 //           ADDRESS (esh), so adopted views with a storage offset and BLOCK
